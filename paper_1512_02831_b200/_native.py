@@ -1,0 +1,119 @@
+"""ctypes binding of libbkt.so (include/bkt.h).
+
+The library is built in-tree by ``python -m paper_1512_02831_b200.build`` (or
+``__graft_entry__.build()``).  There is no fallback: if the library is
+missing, every engine call raises ``NativeLibraryMissing``.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbkt.so"
+
+BKT_OK = 0
+BKT_EINVAL = -1
+BKT_ECONFIG = -2
+BKT_ECUDA = -3
+BKT_ENOMEM = -4
+BKT_ESTATE = -5
+
+# every symbol include/bkt.h declares
+EXPORTS = ("bkt_open", "bkt_close", "bkt_last_error", "bkt_device_info", "bkt_build_tree",
+           "bkt_load_tree", "bkt_search", "bkt_scan_groups", "bkt_fp32_peak")
+
+
+class NativeLibraryMissing(RuntimeError):
+    """libbkt.so is not built; the engine has no CPU fallback."""
+
+
+class SearchOpts(ctypes.Structure):
+    _fields_ = [
+        ("exact", ctypes.c_int32),
+        ("queries_on_device", ctypes.c_int32),
+        ("keys_on_device", ctypes.c_int32),
+        ("record_timing", ctypes.c_int32),
+        ("batch_queries", ctypes.c_int64),
+        ("visited_out", ctypes.c_void_p),
+        ("seq_log", ctypes.c_void_p),
+        ("seq_cap", ctypes.c_int64),
+        ("seq_count_out", ctypes.c_void_p),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("rounds", ctypes.c_int64),
+        ("leaf_visits", ctypes.c_int64),
+        ("pairs", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+        ("leafscan_launches", ctypes.c_int64),
+        ("leafscan_ms", ctypes.c_double),
+        ("search_ms", ctypes.c_double),
+        ("h2d_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} is not built; run `python -m paper_1512_02831_b200.build` "
+                "(this engine has no CPU fallback)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        P = ctypes.c_void_p
+        i32, i64 = ctypes.c_int32, ctypes.c_int64
+        L.bkt_open.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
+        L.bkt_close.argtypes = [P]
+        L.bkt_close.restype = None
+        L.bkt_last_error.argtypes = [P]
+        L.bkt_last_error.restype = ctypes.c_char_p
+        L.bkt_device_info.argtypes = [P, P, P, P, P]
+        L.bkt_build_tree.argtypes = [P, i64, i32, i32, P, P, P, i32]
+        L.bkt_load_tree.argtypes = [P, i32, i32, i64, P, P, P, P, i32, i32, P]
+        L.bkt_search.argtypes = [P, P, i64, i32, ctypes.POINTER(SearchOpts), P, ctypes.POINTER(Stats)]
+        L.bkt_scan_groups.argtypes = [P, P, P, i64, i32, P, i64, i32, P, i32, P, P, P, P, i32]
+        L.bkt_fp32_peak.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
+        for name in EXPORTS:
+            fn = getattr(L, name)
+            if fn.restype is ctypes.c_int:  # default
+                fn.restype = ctypes.c_int
+        _lib = L
+        return _lib
+
+
+def ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def check(rc: int, ctx=None) -> None:
+    """Map a libbkt return code to the reference's exception types."""
+    if rc == BKT_OK:
+        return
+    msg = lib().bkt_last_error(ctx).decode(errors="replace") if lib() else ""
+    if rc == BKT_EINVAL:
+        raise ValueError(msg)
+    if rc == BKT_ECONFIG:
+        from .device import DeviceConfigError
+        raise DeviceConfigError(msg)
+    raise RuntimeError(msg or f"libbkt error {rc}")

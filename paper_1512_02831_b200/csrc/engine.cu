@@ -1,0 +1,805 @@
+// engine.cu -- context, tree residency, the device-resident LazySearch round
+// loop and the C ABI of libbkt.so (include/bkt.h).
+//
+// Reference mapping:
+//   bkt_open / bkt_close   <- device.py:361-364 device_init, SimulatedDevice.close (351-358)
+//   bkt_load_tree          <- ChunkPipeline staging of the leaf structure (device.py:380-420)
+//   bkt_search             <- lazy_search (buffer_tree.py:523-646), Alg. 1 of PAPER.md
+//   bkt_scan_groups        <- SimulatedDevice.enqueue_brute_kernel (device.py:283-337)
+//
+// Device data layout (HBM):
+//   split      f32[2^h-1]                       top tree, level order
+//   quad_base  i64[2^h+1]                       first quad of each leaf; leaves padded to 4 points
+//   leaf_size  i32[2^h]                         real points per leaf
+//   pts        f32[total_quads * 4 * D]         quad g, dim j, point t at g*4D + 4j + t
+//   pidx       u32[total_quads * 4]             original row of each point (padding: 0xFFFFFFFF)
+//   per batch of m queries: q f32[m*D], keys u64[m*k], state u32[m], next i32[m],
+//   visits u32[m], two work lists i32[m]; per leaf: counts, cursor, leaf_off, tile_off.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/bkt.h"
+#include "dims.h"
+#include "round_kernels.cuh"
+
+using namespace bkt;
+
+namespace {
+thread_local std::string g_thread_err;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct LaunchCfg {
+  int grid = 0;
+};
+}  // namespace
+
+struct bkt_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int sm_clock_khz = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  std::string err;
+
+  // ---- tree
+  bool has_tree = false;
+  int h = 0, d = 0, D = 0, nl = 0;
+  long long n = 0, total_quads = 0;
+  float* split = nullptr;
+  long long* quad_base = nullptr;
+  int* leaf_size = nullptr;
+  float* pts = nullptr;
+  uint32_t* pidx = nullptr;
+  // host-resident (out-of-core) leaf structure
+  int residency = 0;
+  float* h_pts = nullptr;
+  uint32_t* h_pidx = nullptr;
+  std::vector<long long> h_quad_base;
+  std::vector<int> h_leaf_size;
+  int num_chunks = 1;
+  std::vector<long long> chunk_q;      // chunk j = quads [chunk_q[j], chunk_q[j+1])
+  std::vector<int> chunk_leaf_lo, chunk_leaf_hi;  // leaves overlapping chunk j: [lo, hi]
+  float* slot_pts[2] = {nullptr, nullptr};
+  uint32_t* slot_idx[2] = {nullptr, nullptr};
+  int slot_chunk[2] = {-1, -1};
+  cudaEvent_t slot_free[2] = {nullptr, nullptr};
+  cudaEvent_t slot_ready[2] = {nullptr, nullptr};
+  long long slot_quads = 0;
+
+  // ---- per-batch work buffers
+  long long cap_m = 0;
+  int cap_k = 0;
+  float* q = nullptr;
+  float* q_raw = nullptr;   // unpadded staging (d != D)
+  uint64_t* keys = nullptr;
+  uint32_t* state = nullptr;
+  int* next = nullptr;
+  uint32_t* visits = nullptr;
+  int* work[2] = {nullptr, nullptr};
+  int cap_nl = 0;
+  int* counts = nullptr;
+  int* cursor = nullptr;
+  int* leaf_off = nullptr;
+  int* tile_off = nullptr;
+  RoundCtl* ctl = nullptr;
+  unsigned long long* pairs = nullptr;
+  unsigned long long* seq_pos = nullptr;
+  int* seq_dev = nullptr;
+  long long seq_dev_cap = 0;
+  // pinned host mirrors
+  RoundCtl* h_ctl = nullptr;  // ring of kRing slots
+  int* h_tile_off = nullptr;
+  int h_tile_off_cap = 0;
+  uint64_t* h_stage = nullptr;  // pinned staging for D2H / H2D
+  size_t h_stage_bytes = 0;
+
+  std::vector<cudaEvent_t> ev_pool;   // leafscan timing events
+  cudaEvent_t ring_ev[4] = {};        // round-check ring (kRing)
+  cudaEvent_t t_ev[2] = {};           // whole-search timing
+  // leafscan grid per (D, KB, mode)
+  std::vector<std::pair<long long, int>> grid_cache;
+};
+
+namespace {
+constexpr int kRing = 4;
+
+int set_err(bkt_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  g_thread_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return set_err(ctx, BKT_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " \
+                                         + __FILE__ + ":" + std::to_string(__LINE__) + " (" #call ")"); \
+  } while (0)
+
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+template <typename T>
+void hfree(T*& p) {
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+}
+
+int kernel_dim(int d) {
+  int best = -1;
+#define BKT_PICK(D) \
+  if (best < 0 && D >= d) best = D;
+  BKT_DIM_LIST(BKT_PICK)
+#undef BKT_PICK
+  return best;
+}
+int kb_bucket(int k) {
+  int best = -1;
+#define BKT_PICK(KB) \
+  if (best < 0 && KB >= k) best = KB;
+  BKT_KB_LIST(BKT_PICK)
+#undef BKT_PICK
+  return best;
+}
+
+cudaError_t launch_leafscan(int D, int kb, bool fma, int grid, cudaStream_t s, const ScanArgs& a, int* occ) {
+  switch (D) {
+#define BKT_CASE(DD) \
+  case DD:           \
+    return launch_leafscan_d##DD(kb, fma, grid, s, a, occ);
+    BKT_DIM_LIST(BKT_CASE)
+#undef BKT_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+int leafscan_grid(bkt_ctx* ctx, int D, int kb, bool fma, int* grid) {
+  long long key = ((long long)D << 16) | ((long long)kb << 1) | (fma ? 1 : 0);
+  for (auto& e : ctx->grid_cache)
+    if (e.first == key) { *grid = e.second; return BKT_OK; }
+  int occ = 0;
+  ScanArgs dummy{};
+  CU(launch_leafscan(D, kb, fma, 0, nullptr, dummy, &occ));
+  if (occ < 1) occ = 1;
+  *grid = occ * ctx->sm_count;
+  ctx->grid_cache.push_back({key, *grid});
+  return BKT_OK;
+}
+
+void free_tree(bkt_ctx* c) {
+  dfree(c->split); dfree(c->quad_base); dfree(c->leaf_size); dfree(c->pts); dfree(c->pidx);
+  hfree(c->h_pts); hfree(c->h_pidx);
+  for (int s = 0; s < 2; ++s) {
+    dfree(c->slot_pts[s]); dfree(c->slot_idx[s]);
+    c->slot_chunk[s] = -1;
+  }
+  c->has_tree = false;
+}
+
+void free_work(bkt_ctx* c) {
+  dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
+  dfree(c->work[0]); dfree(c->work[1]);
+  c->cap_m = 0; c->cap_k = 0;
+}
+
+void free_leafbufs(bkt_ctx* c) {
+  dfree(c->counts); dfree(c->cursor); dfree(c->leaf_off); dfree(c->tile_off);
+  hfree(c->h_tile_off);
+  c->cap_nl = 0;
+  c->h_tile_off_cap = 0;
+}
+
+int ensure_leafbufs(bkt_ctx* ctx, int nl) {
+  if (ctx->cap_nl >= nl) return BKT_OK;
+  free_leafbufs(ctx);
+  CU(cudaMalloc(&ctx->counts, sizeof(int) * nl));
+  CU(cudaMalloc(&ctx->cursor, sizeof(int) * nl));
+  CU(cudaMalloc(&ctx->leaf_off, sizeof(int) * (nl + 1)));
+  CU(cudaMalloc(&ctx->tile_off, sizeof(int) * (nl + 1)));
+  CU(cudaHostAlloc(&ctx->h_tile_off, sizeof(int) * (nl + 1), cudaHostAllocDefault));
+  ctx->cap_nl = nl;
+  ctx->h_tile_off_cap = nl + 1;
+  return BKT_OK;
+}
+
+int ensure_work(bkt_ctx* ctx, long long m, int k) {
+  if (ctx->cap_m >= m && ctx->cap_k >= k && (ctx->D == ctx->d || ctx->q_raw)) return BKT_OK;
+  free_work(ctx);
+  long long M = std::max<long long>(m, 1);
+  CU(cudaMalloc(&ctx->q, sizeof(float) * M * ctx->D));
+  if (ctx->D != ctx->d) CU(cudaMalloc(&ctx->q_raw, sizeof(float) * M * ctx->d));
+  CU(cudaMalloc(&ctx->keys, sizeof(uint64_t) * M * k));
+  CU(cudaMalloc(&ctx->state, sizeof(uint32_t) * M));
+  CU(cudaMalloc(&ctx->next, sizeof(int) * M));
+  CU(cudaMalloc(&ctx->visits, sizeof(uint32_t) * M));
+  CU(cudaMalloc(&ctx->work[0], sizeof(int) * M));
+  CU(cudaMalloc(&ctx->work[1], sizeof(int) * M));
+  ctx->cap_m = M;
+  ctx->cap_k = k;
+  return BKT_OK;
+}
+
+int ensure_stage(bkt_ctx* ctx, size_t bytes) {
+  if (ctx->h_stage_bytes >= bytes) return BKT_OK;
+  hfree(ctx->h_stage);
+  ctx->h_stage_bytes = 0;
+  CU(cudaHostAlloc(&ctx->h_stage, bytes, cudaHostAllocDefault));
+  ctx->h_stage_bytes = bytes;
+  return BKT_OK;
+}
+
+cudaEvent_t get_event(bkt_ctx* c, size_t i) {
+  while (c->ev_pool.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[i];
+}
+
+// host quad-interleaved layout of the leaf structure
+void build_quad_layout(const float* leaf_points, const int64_t* orig, const int64_t* starts, int nl, int d, int D,
+                       const std::vector<long long>& qb, float* out_pts, uint32_t* out_idx) {
+  auto work = [&](int l0, int l1) {
+    for (int l = l0; l < l1; ++l) {
+      long long s = starts[l], e = starts[l + 1];
+      long long L = e - s, nq = qb[l + 1] - qb[l];
+      for (long long qd = 0; qd < nq; ++qd) {
+        float* dst = out_pts + (qb[l] + qd) * 4 * D;
+        uint32_t* di = out_idx + (qb[l] + qd) * 4;
+        for (int t = 0; t < 4; ++t) {
+          long long r = qd * 4 + t;
+          bool real = r < L;
+          di[t] = real ? (uint32_t)orig[s + r] : kIndexSentinel;
+          for (int j = 0; j < D; ++j) {
+            float v;
+            if (!real) v = __builtin_inff();
+            else v = (j < d) ? leaf_points[(s + r) * d + j] : 0.0f;
+            dst[4 * j + t] = v;
+          }
+        }
+      }
+    }
+  };
+  int nt = std::max(1, std::min<int>(16, (int)std::thread::hardware_concurrency()));
+  if (nl < 64) nt = 1;
+  std::vector<std::thread> th;
+  for (int w = 0; w < nt; ++w) th.emplace_back(work, (int)((long long)nl * w / nt), (int)((long long)nl * (w + 1) / nt));
+  for (auto& t : th) t.join();
+}
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+const char* bkt_last_error(const bkt_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  return g_thread_err.c_str();
+}
+
+int bkt_open(int cuda_device, bkt_ctx** out) {
+  bkt_ctx* ctx = nullptr;
+  if (!out) return set_err(nullptr, BKT_EINVAL, "out is NULL");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return set_err(nullptr, BKT_ECUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+  if (cuda_device < 0 || cuda_device >= ndev)
+    return set_err(nullptr, BKT_EINVAL, "cuda_device " + std::to_string(cuda_device) + " out of range [0, " +
+                                            std::to_string(ndev) + ")");
+  ctx = new bkt_ctx();
+  ctx->device = cuda_device;
+  CU(cudaSetDevice(cuda_device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, cuda_device));
+  if (prop.major < 10) {
+    std::string msg = std::string("device ") + prop.name + " is sm_" + std::to_string(prop.major) +
+                      std::to_string(prop.minor) + "; this engine is built for sm_100a (B200)";
+    delete ctx;
+    return set_err(nullptr, BKT_ECUDA, msg);
+  }
+  ctx->sm_count = prop.multiProcessorCount;
+  cudaDeviceGetAttribute(&ctx->sm_clock_khz, cudaDevAttrClockRate, cuda_device);
+  CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  CU(cudaMalloc(&ctx->ctl, sizeof(RoundCtl)));
+  CU(cudaMalloc(&ctx->pairs, sizeof(unsigned long long)));
+  CU(cudaMalloc(&ctx->seq_pos, sizeof(unsigned long long)));
+  CU(cudaHostAlloc(&ctx->h_ctl, sizeof(RoundCtl) * kRing, cudaHostAllocDefault));
+  for (int i = 0; i < kRing; ++i) CU(cudaEventCreateWithFlags(&ctx->ring_ev[i], cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) CU(cudaEventCreate(&ctx->t_ev[i]));
+  for (int s = 0; s < 2; ++s) {
+    CU(cudaEventCreateWithFlags(&ctx->slot_free[s], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->slot_ready[s], cudaEventDisableTiming));
+  }
+  *out = ctx;
+  return BKT_OK;
+}
+
+void bkt_close(bkt_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+  free_tree(ctx);
+  free_work(ctx);
+  free_leafbufs(ctx);
+  dfree(ctx->ctl); dfree(ctx->pairs); dfree(ctx->seq_pos); dfree(ctx->seq_dev);
+  hfree(ctx->h_ctl); hfree(ctx->h_stage);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < kRing; ++i)
+    if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
+  for (int i = 0; i < 2; ++i)
+    if (ctx->t_ev[i]) cudaEventDestroy(ctx->t_ev[i]);
+  for (int s = 0; s < 2; ++s) {
+    if (ctx->slot_free[s]) cudaEventDestroy(ctx->slot_free[s]);
+    if (ctx->slot_ready[s]) cudaEventDestroy(ctx->slot_ready[s]);
+  }
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  delete ctx;
+}
+
+int bkt_device_info(bkt_ctx* ctx, int32_t* sm_count, int32_t* sm_clock_khz, int64_t* free_bytes,
+                    int64_t* total_bytes) {
+  if (!ctx) return set_err(nullptr, BKT_EINVAL, "ctx is NULL");
+  CU(cudaSetDevice(ctx->device));
+  size_t fr = 0, to = 0;
+  CU(cudaMemGetInfo(&fr, &to));
+  if (sm_count) *sm_count = ctx->sm_count;
+  if (sm_clock_khz) *sm_clock_khz = ctx->sm_clock_khz;
+  if (free_bytes) *free_bytes = (int64_t)fr;
+  if (total_bytes) *total_bytes = (int64_t)to;
+  return BKT_OK;
+}
+
+int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* split_values,
+                  const float* leaf_points, const int64_t* original_index, const int64_t* leaf_starts,
+                  int32_t residency, int32_t num_chunks, const int64_t* chunk_bounds) {
+  if (!ctx) return set_err(nullptr, BKT_EINVAL, "ctx is NULL");
+  if (h < 1 || h > kMaxHeight)
+    return set_err(ctx, BKT_EINVAL, "height " + std::to_string(h) + " outside the supported range [1, 16]");
+  if (d < 1 || d > kMaxKernelDim)
+    return set_err(ctx, BKT_EINVAL, "dimensionality " + std::to_string(d) + " outside the supported range [1, 32]");
+  if (n < (1ll << h)) return set_err(ctx, BKT_EINVAL, "height needs at least 2^h points");
+  if (n >= (long long)kIndexSentinel) return set_err(ctx, BKT_EINVAL, "point count exceeds the supported maximum");
+  if (residency != 0 && residency != 1) return set_err(ctx, BKT_EINVAL, "residency must be 0 or 1");
+  if (num_chunks < 1 || num_chunks > n) return set_err(ctx, BKT_EINVAL, "num_chunks must be in [1, n]");
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaStreamSynchronize(ctx->copy_stream));
+  free_tree(ctx);
+  ctx->grid_cache.clear();
+  const int nl = 1 << h;
+  const int D = kernel_dim(d);
+  ctx->h = h; ctx->d = d; ctx->D = D; ctx->nl = nl; ctx->n = n;
+  // quad bases: each leaf padded to a multiple of 4 points
+  ctx->h_quad_base.assign(nl + 1, 0);
+  ctx->h_leaf_size.assign(nl, 0);
+  for (int l = 0; l < nl; ++l) {
+    long long L = leaf_starts[l + 1] - leaf_starts[l];
+    if (L < 1) return set_err(ctx, BKT_EINVAL, "leaf ranges do not partition the point set");
+    ctx->h_leaf_size[l] = (int)L;
+    ctx->h_quad_base[l + 1] = ctx->h_quad_base[l] + (L + 3) / 4;
+  }
+  if (leaf_starts[0] != 0 || leaf_starts[nl] != n)
+    return set_err(ctx, BKT_EINVAL, "leaf ranges do not partition the point set");
+  const long long TQ = ctx->h_quad_base[nl];
+  ctx->total_quads = TQ;
+  free_work(ctx);  // per-query buffers depend on D; reallocated by the next search
+
+  CU(cudaMalloc(&ctx->split, sizeof(float) * (nl - 1)));
+  CU(cudaMalloc(&ctx->quad_base, sizeof(long long) * (nl + 1)));
+  CU(cudaMalloc(&ctx->leaf_size, sizeof(int) * nl));
+  CU(cudaMemcpy(ctx->split, split_values, sizeof(float) * (nl - 1), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->quad_base, ctx->h_quad_base.data(), sizeof(long long) * (nl + 1), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->leaf_size, ctx->h_leaf_size.data(), sizeof(int) * nl, cudaMemcpyHostToDevice));
+
+  const size_t pts_bytes = sizeof(float) * (size_t)TQ * 4 * D;
+  const size_t idx_bytes = sizeof(uint32_t) * (size_t)TQ * 4;
+  CU(cudaHostAlloc(&ctx->h_pts, pts_bytes, cudaHostAllocDefault));
+  CU(cudaHostAlloc(&ctx->h_pidx, idx_bytes, cudaHostAllocDefault));
+  build_quad_layout(leaf_points, original_index, leaf_starts, nl, d, D, ctx->h_quad_base, ctx->h_pts, ctx->h_pidx);
+
+  ctx->residency = residency;
+  if (residency == 0) {
+    CU(cudaMalloc(&ctx->pts, pts_bytes));
+    CU(cudaMalloc(&ctx->pidx, idx_bytes));
+    CU(cudaMemcpy(ctx->pts, ctx->h_pts, pts_bytes, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->pidx, ctx->h_pidx, idx_bytes, cudaMemcpyHostToDevice));
+    hfree(ctx->h_pts);
+    hfree(ctx->h_pidx);
+    ctx->num_chunks = 1;
+  } else {
+    // chunk bounds: the reference row bounds (ChunkPlan.bounds) mapped to the
+    // containing quad of the padded layout; results do not depend on where a
+    // chunk boundary falls (reference scheduler.py:1-10, acceptance crit. 2).
+    ctx->num_chunks = num_chunks;
+    ctx->chunk_q.assign(num_chunks + 1, 0);
+    for (int j = 0; j <= num_chunks; ++j) {
+      long long row = chunk_bounds ? chunk_bounds[j] : (long long)(((__int128)j * n + num_chunks - 1) / num_chunks);
+      if (row <= 0) { ctx->chunk_q[j] = 0; continue; }
+      if (row >= n) { ctx->chunk_q[j] = TQ; continue; }
+      int l = (int)(std::upper_bound(leaf_starts, leaf_starts + nl + 1, (int64_t)row) - leaf_starts) - 1;
+      long long off = row - leaf_starts[l];
+      ctx->chunk_q[j] = ctx->h_quad_base[l] + (off + 3) / 4;
+    }
+    for (int j = 0; j < num_chunks; ++j)
+      if (ctx->chunk_q[j + 1] < ctx->chunk_q[j]) return set_err(ctx, BKT_EINVAL, "chunk bounds must be non-decreasing");
+    ctx->chunk_leaf_lo.assign(num_chunks, 0);
+    ctx->chunk_leaf_hi.assign(num_chunks, -1);
+    long long maxq = 0;
+    for (int j = 0; j < num_chunks; ++j) {
+      long long a = ctx->chunk_q[j], b = ctx->chunk_q[j + 1];
+      maxq = std::max(maxq, b - a);
+      if (b <= a) continue;
+      int lo = (int)(std::upper_bound(ctx->h_quad_base.begin(), ctx->h_quad_base.end(), a) - ctx->h_quad_base.begin()) - 1;
+      int hi = (int)(std::lower_bound(ctx->h_quad_base.begin(), ctx->h_quad_base.end(), b) - ctx->h_quad_base.begin()) - 1;
+      ctx->chunk_leaf_lo[j] = lo;
+      ctx->chunk_leaf_hi[j] = hi;
+    }
+    ctx->slot_quads = std::max<long long>(maxq, 1);
+    for (int s = 0; s < 2; ++s) {
+      CU(cudaMalloc(&ctx->slot_pts[s], sizeof(float) * ctx->slot_quads * 4 * D));
+      CU(cudaMalloc(&ctx->slot_idx[s], sizeof(uint32_t) * ctx->slot_quads * 4));
+      ctx->slot_chunk[s] = -1;
+    }
+  }
+  if (ensure_leafbufs(ctx, nl) != BKT_OK) return BKT_ECUDA;
+  ctx->has_tree = true;
+  return BKT_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================
+// search
+// =============================================================================
+namespace {
+
+struct SearchRun {
+  long long m = 0;
+  int k = 0;
+  int kb = 0;
+  bool fma = false;
+  int grid_scan = 0;
+  int grid_small = 0;
+  bool timing = false;
+  long long launches = 0;
+  long long leafscan_launches = 0;
+  double leafscan_ms = 0;
+  size_t ev_next = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
+  long long rounds = 0;
+  bool seq = false;
+  long long seq_cap = 0;
+};
+
+ScanArgs make_scan_args(bkt_ctx* ctx, SearchRun& R, int cur) {
+  ScanArgs a{};
+  a.q = ctx->q;
+  a.keys = ctx->keys;
+  a.state = ctx->state;
+  a.next = ctx->next;
+  a.visits = ctx->visits;
+  a.work = ctx->work[cur];
+  a.leaf_off = ctx->leaf_off;
+  a.tile_off = ctx->tile_off;
+  a.num_tiles = &ctx->ctl->num_tiles;
+  a.tile_lo = 0;
+  a.tile_hi = -1;
+  a.counts = ctx->counts;
+  a.pts = ctx->pts;
+  a.pidx = ctx->pidx;
+  a.quad_origin = 0;
+  a.clip_lo = 0;
+  a.clip_hi = ctx->total_quads;
+  a.quad_base = ctx->quad_base;
+  a.leaf_size = ctx->leaf_size;
+  a.top = TopTreeView{ctx->split, ctx->h, ctx->d};
+  a.k = R.k;
+  a.fused = 1;
+  a.zero = 0ull;
+  a.pairs = ctx->pairs;
+  a.seq_log = R.seq ? ctx->seq_dev : nullptr;
+  a.seq_pos = ctx->seq_pos;
+  a.seq_cap = R.seq_cap;
+  return a;
+}
+
+int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (R.timing) {
+    e0 = get_event(ctx, R.ev_next++);
+    e1 = get_event(ctx, R.ev_next++);
+    CU(cudaEventRecord(e0, ctx->stream));
+  }
+  CU(launch_leafscan(ctx->D, R.kb, R.fma, R.grid_scan, ctx->stream, a, nullptr));
+  if (R.timing) {
+    CU(cudaEventRecord(e1, ctx->stream));
+    R.scan_events.push_back({e0, e1});
+  }
+  R.launches++;
+  R.leafscan_launches++;
+  return BKT_OK;
+}
+
+// Out-of-core round: stream the chunks that hold buffered work through the two
+// device slots (sec. 3.2 Brute/Copy/Wait; reference ChunkPipeline.run_round,
+// device.py:422-446).  Chunks without work are skipped and chunks still resident
+// from the previous round are not copied again.
+int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
+  // tile offsets of this round to the host (needed to pick chunks with work)
+  CU(cudaMemcpyAsync(ctx->h_tile_off, ctx->tile_off, sizeof(int) * (ctx->nl + 1), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  std::vector<int> need;
+  for (int j = 0; j < ctx->num_chunks; ++j) {
+    if (ctx->chunk_leaf_hi[j] < ctx->chunk_leaf_lo[j]) continue;
+    int t0 = ctx->h_tile_off[ctx->chunk_leaf_lo[j]], t1 = ctx->h_tile_off[ctx->chunk_leaf_hi[j] + 1];
+    if (t1 > t0) need.push_back(j);
+  }
+  const int D = ctx->D;
+  auto ensure_resident = [&](int j, int avoid_slot) -> int {
+    for (int s = 0; s < 2; ++s)
+      if (ctx->slot_chunk[s] == j) return s;
+    int s = (avoid_slot == 0) ? 1 : 0;
+    if (avoid_slot < 0) s = (ctx->slot_chunk[0] < 0) ? 0 : ((ctx->slot_chunk[1] < 0) ? 1 : 0);
+    long long a = ctx->chunk_q[j], b = ctx->chunk_q[j + 1];
+    cudaStreamWaitEvent(ctx->copy_stream, ctx->slot_free[s], 0);
+    cudaMemcpyAsync(ctx->slot_pts[s], ctx->h_pts + a * 4 * D, sizeof(float) * (b - a) * 4 * D,
+                    cudaMemcpyHostToDevice, ctx->copy_stream);
+    cudaMemcpyAsync(ctx->slot_idx[s], ctx->h_pidx + a * 4, sizeof(uint32_t) * (b - a) * 4, cudaMemcpyHostToDevice,
+                    ctx->copy_stream);
+    cudaEventRecord(ctx->slot_ready[s], ctx->copy_stream);
+    ctx->slot_chunk[s] = j;
+    return s;
+  };
+  std::vector<int> slot_of(need.size(), -1);
+  if (!need.empty()) slot_of[0] = ensure_resident(need[0], -1);
+  for (size_t i = 0; i < need.size(); ++i) {
+    int j = need[i];
+    int s = slot_of[i];
+    // prefetch the next chunk into the other slot while this one computes
+    if (i + 1 < need.size()) slot_of[i + 1] = ensure_resident(need[i + 1], s);
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->slot_ready[s], 0));
+    ScanArgs a = make_scan_args(ctx, R, cur);
+    a.fused = 0;
+    a.pts = ctx->slot_pts[s];
+    a.pidx = ctx->slot_idx[s];
+    a.quad_origin = ctx->chunk_q[j];
+    a.clip_lo = ctx->chunk_q[j];
+    a.clip_hi = ctx->chunk_q[j + 1];
+    a.tile_lo = ctx->h_tile_off[ctx->chunk_leaf_lo[j]];
+    a.tile_hi = ctx->h_tile_off[ctx->chunk_leaf_hi[j] + 1];
+    int rc = launch_scan(ctx, R, a);
+    if (rc != BKT_OK) return rc;
+    CU(cudaEventRecord(ctx->slot_free[s], ctx->stream));
+  }
+  // FindLeaf after every chunk of the round has been scanned
+  findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
+      ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys, ctx->state,
+      ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+  CU(cudaGetLastError());
+  R.launches++;
+  return BKT_OK;
+}
+
+// One batch: queries already in ctx->q (m x D).  Runs rounds until no query is active.
+int search_batch(bkt_ctx* ctx, SearchRun& R) {
+  const long long m = R.m;
+  TopTreeView top{ctx->split, ctx->h, ctx->d};
+  RoundCtl init{};
+  init.active = (int)m;
+  CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nl, ctx->stream));
+  CU(cudaMemsetAsync(ctx->cursor, 0, sizeof(int) * ctx->nl, ctx->stream));
+  start_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
+                                                       ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr,
+                                                       ctx->seq_pos, R.seq_cap);
+  CU(cudaGetLastError());
+  R.launches++;
+
+  int cur = 0;
+  long long round = 0;
+  // rounds are launched ahead of the host check; the active count of round r
+  // is read back asynchronously and checked kRing-1 rounds later
+  cudaEvent_t* ring = ctx->ring_ev;
+  const bool ooc = ctx->residency == 1;
+  for (;;) {
+    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl,
+                                                     ctx->nl, kNT);
+    CU(cudaGetLastError());
+    R.launches++;
+    const int slot = (int)(round % kRing);
+    CU(cudaMemcpyAsync(&ctx->h_ctl[slot], ctx->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaEventRecord(ring[slot], ctx->stream));
+    if (ooc) {
+      // out-of-core needs the plan on the host anyway; check synchronously
+      CU(cudaEventSynchronize(ring[slot]));
+      if (ctx->h_ctl[slot].active == 0) break;
+    }
+    scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->next,
+                                                           ctx->leaf_off, ctx->cursor, ctx->work[cur], ctx->ctl);
+    CU(cudaGetLastError());
+    R.launches++;
+    if (ooc) {
+      int rc = ooc_round(ctx, R, cur);
+      if (rc != BKT_OK) return rc;
+    } else {
+      ScanArgs a = make_scan_args(ctx, R, cur);
+      int rc = launch_scan(ctx, R, a);
+      if (rc != BKT_OK) return rc;
+    }
+    cur ^= 1;
+    ++round;
+    if (!ooc && round >= kRing - 1) {
+      // check the round launched kRing-1 iterations ago
+      const int chk = (int)((round - (kRing - 1)) % kRing);
+      CU(cudaEventSynchronize(ring[chk]));
+      if (ctx->h_ctl[chk].active == 0) break;
+    }
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  RoundCtl fin;
+  CU(cudaMemcpy(&fin, ctx->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost));
+  R.rounds += fin.rounds;
+  return BKT_OK;
+}
+
+}  // namespace
+
+extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t k, const bkt_search_opts* opts,
+                          uint64_t* out_keys, bkt_stats* stats) {
+  if (!ctx) return set_err(nullptr, BKT_EINVAL, "ctx is NULL");
+  if (!ctx->has_tree) return set_err(ctx, BKT_ESTATE, "no tree loaded (call bkt_load_tree first)");
+  if (m < 0) return set_err(ctx, BKT_EINVAL, "m must be >= 0");
+  if (k < 1) return set_err(ctx, BKT_EINVAL, "k must be >= 1, got " + std::to_string(k));
+  if (k > ctx->n)
+    return set_err(ctx, BKT_EINVAL, "k=" + std::to_string(k) + " exceeds the number of reference points (" +
+                                        std::to_string(ctx->n) + ")");
+  if (k > kMaxK) return set_err(ctx, BKT_EINVAL, "k=" + std::to_string(k) + " exceeds the supported maximum (64)");
+  bkt_search_opts o{};
+  o.exact = 1;
+  if (opts) o = *opts;
+  bkt_stats st{};
+  CU(cudaSetDevice(ctx->device));
+  if (m == 0) {
+    if (stats) *stats = st;
+    return BKT_OK;
+  }
+  SearchRun R;
+  R.k = k;
+  R.kb = kb_bucket(k);
+  R.fma = o.exact == 0;
+  R.timing = o.record_timing != 0;
+  R.seq = o.seq_log != nullptr && o.seq_cap > 0;
+  R.seq_cap = R.seq ? o.seq_cap : 0;
+  int rc = leafscan_grid(ctx, ctx->D, R.kb, R.fma, &R.grid_scan);
+  if (rc != BKT_OK) return rc;
+  R.grid_small = ctx->sm_count * 8;
+
+  // batch size: whatever fits comfortably in free memory (or the caller's choice)
+  const long long per_query = 4ll * ctx->D + 4ll * ctx->d + 8ll * k + 4 * 5;
+  long long batch = o.batch_queries;
+  if (batch <= 0) {
+    size_t fr = 0, to = 0;
+    CU(cudaMemGetInfo(&fr, &to));
+    long long usable = (long long)(fr * 0.6) + (long long)ctx->cap_m * per_query;
+    batch = std::max<long long>(1 << 16, usable / per_query);
+    batch = std::min<long long>(batch, 1ll << 30);
+  }
+  batch = std::min<long long>(batch, m);
+  batch = std::min<long long>(batch, (long long)INT32_MAX / 2);
+  rc = ensure_work(ctx, batch, k);
+  if (rc != BKT_OK) return rc;
+  if (R.seq) {
+    if (ctx->seq_dev_cap < R.seq_cap) {
+      dfree(ctx->seq_dev);
+      CU(cudaMalloc(&ctx->seq_dev, sizeof(int) * 3 * R.seq_cap));
+      ctx->seq_dev_cap = R.seq_cap;
+    }
+    if (m > batch) return set_err(ctx, BKT_EINVAL, "sequence recording requires a single batch");
+  }
+  CU(cudaMemsetAsync(ctx->pairs, 0, sizeof(unsigned long long), ctx->stream));
+  CU(cudaMemsetAsync(ctx->seq_pos, 0, sizeof(unsigned long long), ctx->stream));
+
+  cudaEvent_t t_all0 = ctx->t_ev[0], t_all1 = ctx->t_ev[1];
+  CU(cudaEventRecord(t_all0, ctx->stream));
+  long long leaf_visits = 0;
+  std::vector<uint32_t> vis_host;
+  for (long long b0 = 0; b0 < m; b0 += batch) {
+    const long long bm = std::min(batch, m - b0);
+    R.m = bm;
+    // queries -> ctx->q (m x D)
+    const float* src = queries + b0 * ctx->d;
+    float* raw = (ctx->D == ctx->d) ? ctx->q : ctx->q_raw;
+    const size_t qbytes = sizeof(float) * bm * ctx->d;
+    if (o.queries_on_device) {
+      if (ctx->D == ctx->d) CU(cudaMemcpyAsync(ctx->q, src, qbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      else raw = const_cast<float*>(src);
+    } else {
+      auto c0 = std::chrono::steady_clock::now();
+      CU(cudaMemcpyAsync(raw, src, qbytes, cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      st.h2d_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+      st.h2d_bytes += qbytes;
+    }
+    if (ctx->D != ctx->d) {
+      pad_rows_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(raw, ctx->d, ctx->q, ctx->D, bm);
+      CU(cudaGetLastError());
+      R.launches++;
+    }
+    rc = search_batch(ctx, R);
+    if (rc != BKT_OK) return rc;
+    // results
+    const size_t kbytes = sizeof(uint64_t) * bm * k;
+    if (o.keys_on_device) {
+      CU(cudaMemcpyAsync(out_keys + b0 * k, ctx->keys, kbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      auto c0 = std::chrono::steady_clock::now();
+      CU(cudaMemcpyAsync(out_keys + b0 * k, ctx->keys, kbytes, cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      st.d2h_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+      st.d2h_bytes += kbytes;
+    }
+    // visits -> leaf_visits (+ optional per-query output)
+    vis_host.resize(bm);
+    CU(cudaMemcpyAsync(vis_host.data(), ctx->visits, sizeof(uint32_t) * bm, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (long long i = 0; i < bm; ++i) leaf_visits += vis_host[i];
+    if (o.visited_out)
+      for (long long i = 0; i < bm; ++i) o.visited_out[b0 + i] = (int32_t)vis_host[i];
+  }
+  CU(cudaEventRecord(t_all1, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, t_all0, t_all1));
+  unsigned long long pairs = 0;
+  CU(cudaMemcpy(&pairs, ctx->pairs, sizeof(pairs), cudaMemcpyDeviceToHost));
+  if (R.seq) {
+    unsigned long long cnt = 0;
+    CU(cudaMemcpy(&cnt, ctx->seq_pos, sizeof(cnt), cudaMemcpyDeviceToHost));
+    long long ncopy = std::min<long long>((long long)cnt, R.seq_cap);
+    if (ncopy > 0) CU(cudaMemcpy(o.seq_log, ctx->seq_dev, sizeof(int) * 3 * ncopy, cudaMemcpyDeviceToHost));
+    if (o.seq_count_out) *o.seq_count_out = (int64_t)cnt;
+  }
+  for (auto& pr : R.scan_events) {
+    float t = 0;
+    CU(cudaEventElapsedTime(&t, pr.first, pr.second));
+    R.leafscan_ms += t;
+  }
+  st.rounds = R.rounds;
+  st.leaf_visits = leaf_visits;
+  st.pairs = (int64_t)pairs;
+  st.kernel_launches = R.launches;
+  st.leafscan_launches = R.leafscan_launches;
+  st.leafscan_ms = R.leafscan_ms;
+  st.search_ms = ms;
+  if (stats) *stats = st;
+  return BKT_OK;
+}
+
+// accessors for the other translation units (misc.cu)
+namespace bkt_internal {
+int ctx_device(bkt_ctx* c) { return c->device; }
+cudaStream_t ctx_stream(bkt_ctx* c) { return c->stream; }
+int ctx_fail(bkt_ctx* c, int code, const std::string& msg) { return set_err(c, code, msg); }
+}  // namespace bkt_internal

@@ -1,0 +1,172 @@
+// misc.cu -- the reference's fine-grained device plugin seam (bkt_scan_groups)
+// and the FP32 pipe probe used as the measured roofline denominator.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bkt.h"
+#include "bkt_device.cuh"
+
+using namespace bkt;
+
+// defined in engine.cu
+struct bkt_ctx;
+namespace bkt_internal {
+int ctx_device(bkt_ctx* c);
+cudaStream_t ctx_stream(bkt_ctx* c);
+int ctx_fail(bkt_ctx* c, int code, const std::string& msg);
+}  // namespace bkt_internal
+
+namespace {
+
+// One thread per query row of a group: scan chunk rows [lo, hi) and merge into
+// the row's ascending top-k held in global memory.  Reference
+// device.py:316-321 (scan) -> core.py:138-146, 152-160, 251-262.
+__global__ void groups_kernel(const float* __restrict__ pts, const uint32_t* __restrict__ ids, int d,
+                              const float* __restrict__ q, int k, uint64_t* __restrict__ keys, int ngroups,
+                              const long long* __restrict__ gptr, const long long* __restrict__ grows,
+                              const long long* __restrict__ glo, const long long* __restrict__ ghi,
+                              long long total_rows, int exact) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total_rows;
+       t += (long long)gridDim.x * blockDim.x) {
+    // group of entry t (binary search over gptr)
+    int lo = 0, hi = ngroups - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (gptr[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const long long row = grows[t];
+    const float* qp = q + row * d;
+    uint64_t* kp = keys + row * k;
+    for (long long r = glo[lo]; r < ghi[lo]; ++r) {
+      const float* pp = pts + r * d;
+      float acc = 0.0f;
+      if (exact) {
+        for (int j = 0; j < d; ++j) {
+          float df = __fsub_rn(qp[j], pp[j]);
+          acc = __fadd_rn(acc, __fmul_rn(df, df));
+        }
+      } else {
+        for (int j = 0; j < d; ++j) {
+          float df = __fsub_rn(qp[j], pp[j]);
+          acc = __fmaf_rn(df, df, acc);
+        }
+      }
+      uint64_t c = pack_key(acc, ids[r]);
+      if (c < kp[k - 1]) {
+        int i = k - 1;
+        while (i > 0 && kp[i - 1] > c) {
+          kp[i] = kp[i - 1];
+          --i;
+        }
+        kp[i] = c;
+      }
+    }
+  }
+}
+
+#define ITERS 2048
+__global__ void ffma_probe(float* out, float a, float b) {
+  float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+      x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+}  // namespace
+
+#define CU(call)                                                                                         \
+  do {                                                                                                   \
+    cudaError_t e_ = (call);                                                                             \
+    if (e_ != cudaSuccess)                                                                               \
+      return bkt_internal::ctx_fail(ctx, BKT_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                                        " (" #call ")");                                 \
+  } while (0)
+
+extern "C" int bkt_scan_groups(bkt_ctx* ctx, const float* points, const int64_t* ids, int64_t L, int32_t d,
+                               const float* queries, int64_t m, int32_t k, uint64_t* keys, int32_t ngroups,
+                               const int64_t* group_ptr, const int64_t* group_rows, const int64_t* group_lo,
+                               const int64_t* group_hi, int32_t exact) {
+  if (!ctx) return bkt_internal::ctx_fail(nullptr, BKT_EINVAL, "ctx is NULL");
+  if (L < 0 || d < 1 || m < 0 || k < 1 || ngroups < 0)
+    return bkt_internal::ctx_fail(ctx, BKT_EINVAL, "invalid scan_groups sizes");
+  if (ngroups == 0) return BKT_OK;
+  for (int g = 0; g < ngroups; ++g) {
+    if (!(0 <= group_lo[g] && group_lo[g] < group_hi[g] && group_hi[g] <= L))
+      return bkt_internal::ctx_fail(ctx, BKT_EINVAL, "group range outside chunk");
+    if (group_ptr[g + 1] <= group_ptr[g]) return bkt_internal::ctx_fail(ctx, BKT_EINVAL, "empty query group");
+  }
+  const long long total = group_ptr[ngroups];
+  for (long long t = 0; t < total; ++t)
+    if (group_rows[t] < 0 || group_rows[t] >= m)
+      return bkt_internal::ctx_fail(ctx, BKT_EINVAL, "group row outside the query block");
+  CU(cudaSetDevice(bkt_internal::ctx_device(ctx)));
+  cudaStream_t s = bkt_internal::ctx_stream(ctx);
+  std::vector<uint32_t> ids32((size_t)L);
+  for (long long i = 0; i < L; ++i) ids32[i] = (uint32_t)ids[i];
+  float *dp = nullptr, *dq = nullptr;
+  uint32_t* di = nullptr;
+  uint64_t* dk = nullptr;
+  long long *dptr = nullptr, *drows = nullptr, *dlo = nullptr, *dhi = nullptr;
+  CU(cudaMallocAsync(&dp, sizeof(float) * std::max<long long>(1, L * d), s));
+  CU(cudaMallocAsync(&di, sizeof(uint32_t) * std::max<long long>(1, L), s));
+  CU(cudaMallocAsync(&dq, sizeof(float) * std::max<long long>(1, m * d), s));
+  CU(cudaMallocAsync(&dk, sizeof(uint64_t) * std::max<long long>(1, m * k), s));
+  CU(cudaMallocAsync(&dptr, sizeof(long long) * (ngroups + 1), s));
+  CU(cudaMallocAsync(&drows, sizeof(long long) * std::max<long long>(1, total), s));
+  CU(cudaMallocAsync(&dlo, sizeof(long long) * ngroups, s));
+  CU(cudaMallocAsync(&dhi, sizeof(long long) * ngroups, s));
+  CU(cudaMemcpyAsync(dp, points, sizeof(float) * L * d, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(di, ids32.data(), sizeof(uint32_t) * L, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(dq, queries, sizeof(float) * m * d, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(dk, keys, sizeof(uint64_t) * m * k, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(dptr, group_ptr, sizeof(long long) * (ngroups + 1), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(drows, group_rows, sizeof(long long) * total, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(dlo, group_lo, sizeof(long long) * ngroups, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(dhi, group_hi, sizeof(long long) * ngroups, cudaMemcpyHostToDevice, s));
+  int blocks = (int)std::min<long long>(4096, (total + 127) / 128);
+  groups_kernel<<<std::max(1, blocks), 128, 0, s>>>(dp, di, d, dq, k, dk, ngroups, dptr, drows, dlo, dhi, total,
+                                                     exact);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(keys, dk, sizeof(uint64_t) * m * k, cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(dp, s)); CU(cudaFreeAsync(di, s)); CU(cudaFreeAsync(dq, s)); CU(cudaFreeAsync(dk, s));
+  CU(cudaFreeAsync(dptr, s)); CU(cudaFreeAsync(drows, s)); CU(cudaFreeAsync(dlo, s)); CU(cudaFreeAsync(dhi, s));
+  CU(cudaStreamSynchronize(s));
+  return BKT_OK;
+}
+
+extern "C" int bkt_fp32_peak(bkt_ctx* ctx, double* tflops) {
+  if (!ctx || !tflops) return bkt_internal::ctx_fail(ctx, BKT_EINVAL, "ctx/tflops is NULL");
+  CU(cudaSetDevice(bkt_internal::ctx_device(ctx)));
+  cudaStream_t s = bkt_internal::ctx_stream(ctx);
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, bkt_internal::ctx_device(ctx)));
+  const int blocks = sms * 8, threads = 256;
+  float* out = nullptr;
+  CU(cudaMallocAsync(&out, sizeof(float) * blocks * threads, s));
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  double best = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    CU(cudaEventRecord(e0, s));
+    ffma_probe<<<blocks, threads, 0, s>>>(out, 1.0001f, 0.5f);
+    CU(cudaEventRecord(e1, s));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    double flops = 2.0 * blocks * threads * (double)ITERS * 4 * 8;
+    if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CU(cudaFreeAsync(out, s));
+  CU(cudaStreamSynchronize(s));
+  *tflops = best;
+  return BKT_OK;
+}

@@ -1,0 +1,181 @@
+// round_kernels.cuh -- the per-round scheduling kernels of the device-resident
+// LazySearch loop (Alg. 1; reference buffer_tree.py:523-646).
+//
+// One round = plan -> scatter -> leafscan(+fused FindLeaf):
+//   start   : every fresh query descends to its home leaf (find_leaf_batch for
+//             fresh queries, buffer_tree.py:318-321, 351-376) and is counted
+//             into its leaf's bucket.
+//   plan    : exclusive scans of the per-leaf counts -> each leaf's slice of
+//             the work list and its tile range (the "buffers" of
+//             QueryBuffers.drain_all, buffer_tree.py:420-430, in leaf order).
+//   scatter : counting-sort placement of the still-active queries into their
+//             leaf's slice with warp-aggregated atomics (the reference's
+//             stable argsort + insert_many, buffer_tree.py:603-619).  DONE
+//             queries drop out (buffer_tree.py:482-485).
+//   findleaf: unfused FindLeaf for the out-of-core path (leafscan fuses it
+//             when the whole leaf structure is resident).
+#pragma once
+#include "bkt_device.cuh"
+
+namespace bkt {
+
+struct RoundCtl {
+  int active;       // queries with a leaf to scan this round
+  int prev_active;  // length of the previous round's work list
+  int num_tiles;    // tiles this round
+  int rounds;       // rounds with active > 0
+};
+
+constexpr int kPlanThreads = 1024;
+
+// Fresh queries: EMPTY top-k, descend from the root, count.
+__global__ void start_kernel(const float* __restrict__ q, int D, long long m, int k, TopTreeView top,
+                             uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next,
+                             uint32_t* __restrict__ visits, int* __restrict__ counts, int* seq_log,
+                             unsigned long long* seq_pos, long long seq_cap) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+    uint64_t* kp = keys + i * k;
+    for (int t = 0; t < k; ++t) kp[t] = kEmptyKey;
+    const float* qp = q + i * D;
+    auto qget = [qp](int j) { return __ldg(qp + j); };
+    uint32_t leaf = 0, pend = 0;
+    descend(top, qget, leaf, pend, 0);
+    state[i] = (pend << 16) | leaf;
+    next[i] = (int)leaf;
+    visits[i] = 1;
+    if (seq_log) {
+      unsigned long long p = atomicAdd(seq_pos, 1ull);
+      if ((long long)p < seq_cap) {
+        seq_log[3 * p] = (int)i; seq_log[3 * p + 1] = 1; seq_log[3 * p + 2] = (int)leaf;
+      }
+    }
+    warp_count(counts, (int)leaf);
+  }
+}
+
+// Block-wide exclusive scan of (a, b) over kPlanThreads threads.
+__device__ __forceinline__ void block_scan2(long long& a, long long& b, long long& tot_a, long long& tot_b) {
+  __shared__ long long wa[32], wb[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long ta = __shfl_up_sync(0xffffffffu, ia, o);
+    long long tb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) { ia += ta; ib += tb; }
+  }
+  if (lane == 31) { wa[w] = ia; wb[w] = ib; }
+  __syncthreads();
+  if (w == 0) {
+    long long xa = (lane < (int)(blockDim.x >> 5)) ? wa[lane] : 0;
+    long long xb = (lane < (int)(blockDim.x >> 5)) ? wb[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long ta = __shfl_up_sync(0xffffffffu, xa, o);
+      long long tb = __shfl_up_sync(0xffffffffu, xb, o);
+      if (lane >= o) { xa += ta; xb += tb; }
+    }
+    wa[lane] = xa; wb[lane] = xb;
+  }
+  __syncthreads();
+  long long pa = (w > 0) ? wa[w - 1] : 0, pb = (w > 0) ? wb[w - 1] : 0;
+  tot_a = wa[31]; tot_b = wb[31];
+  a = pa + ia - a;  // exclusive
+  b = pb + ib - b;
+  __syncthreads();
+}
+
+// counts -> leaf_off / tile_off; resets counts and cursors; updates ctl.
+// One CTA of kPlanThreads threads; each thread owns a contiguous leaf run.
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ counts, int* __restrict__ leaf_off,
+                                                            int* __restrict__ tile_off, int* __restrict__ cursor,
+                                                            RoundCtl* ctl, int nl, int tile_q) {
+  const int per = (nl + kPlanThreads - 1) / kPlanThreads;
+  const int lo = min(nl, (int)threadIdx.x * per), hi = min(nl, lo + per);
+  long long sc = 0, st = 0;
+  for (int l = lo; l < hi; ++l) {
+    int c = counts[l];
+    sc += c;
+    st += (c + tile_q - 1) / tile_q;
+  }
+  long long tot_c, tot_t;
+  long long ec = sc, et = st;
+  block_scan2(ec, et, tot_c, tot_t);
+  for (int l = lo; l < hi; ++l) {
+    int c = counts[l];
+    leaf_off[l] = (int)ec;
+    tile_off[l] = (int)et;
+    ec += c;
+    et += (c + tile_q - 1) / tile_q;
+    counts[l] = 0;
+    cursor[l] = 0;
+  }
+  if (threadIdx.x == 0) {
+    leaf_off[nl] = (int)tot_c;
+    tile_off[nl] = (int)tot_t;
+    ctl->prev_active = ctl->active;
+    ctl->active = (int)tot_c;
+    ctl->num_tiles = (int)tot_t;
+    if (tot_c > 0) ctl->rounds += 1;
+  }
+}
+
+// Place every still-active query of the previous work list into its leaf's
+// slice of the new list.  identity: previous list is 0..prev_active-1.
+__global__ void scatter_kernel(const int* __restrict__ prev, int identity, const int* __restrict__ next,
+                               const int* __restrict__ leaf_off, int* __restrict__ cursor, int* __restrict__ work,
+                               const RoundCtl* ctl) {
+  const int n = ctl->prev_active;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int qi = identity ? i : prev[i];
+    int leaf = next[qi];
+    if (leaf >= 0) {
+      int pos = warp_reserve(cursor, leaf);
+      work[leaf_off[leaf] + pos] = qi;
+    }
+  }
+}
+
+// Unfused FindLeaf over this round's work list (out-of-core rounds, where a
+// leaf may be split across chunk passes).  buffer_tree.py:292-378.
+__global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ctl, const float* __restrict__ q,
+                                int D, int k, TopTreeView top, const uint64_t* __restrict__ keys,
+                                uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
+                                int* __restrict__ counts, int* seq_log, unsigned long long* seq_pos,
+                                long long seq_cap) {
+  const int n = ctl->active;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int qi = work[i];
+    const float* qp = q + (long long)qi * D;
+    auto qget = [qp](int j) { return __ldg(qp + j); };
+    float kth = key_dist(keys[(long long)qi * k + k - 1]);
+    uint32_t st = state[qi];
+    uint32_t lf = st & 0xFFFFu, pend = st >> 16;
+    int nxt = find_next_leaf(top, qget, kth, lf, pend);
+    state[qi] = (pend << 16) | lf;
+    next[qi] = nxt;
+    if (nxt >= 0) {
+      uint32_t v = visits[qi] + 1;
+      visits[qi] = v;
+      if (seq_log) {
+        unsigned long long p = atomicAdd(seq_pos, 1ull);
+        if ((long long)p < seq_cap) {
+          seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)v; seq_log[3 * p + 2] = nxt;
+        }
+      }
+      warp_count(counts, nxt);
+    }
+  }
+}
+
+// m x d host layout -> m x D kernel layout (zero padded; exact: +0 dims add 0).
+__global__ void pad_rows_kernel(const float* __restrict__ src, int d, float* __restrict__ dst, int D, long long m) {
+  long long total = m * D;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    long long i = t / D;
+    int j = (int)(t - i * D);
+    dst[t] = (j < d) ? src[i * d + j] : 0.0f;
+  }
+}
+
+}  // namespace bkt

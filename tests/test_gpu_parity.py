@@ -1,0 +1,283 @@
+"""GPU parity: the sm_100a engine vs the reference's golden outputs and the
+CPU oracle, through the drop-in API (lazy_search -> bkt_search C ABI).
+
+exact mode: keys bit-identical, visited counts and leaf sequences identical
+(the reference's own contract, tests/test_acceptance.py criteria 1 and 4).
+fma mode (north star tolerance): squared distances within 1e-5 relative,
+indices equal except where reference distances tie within 1e-5.
+"""
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+import paper_1512_02831_b200 as bkt
+from oracle import oracle as O
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+FMA_RTOL = 1e-5
+
+
+def _dist_idx(keys):
+    return bkt.unpack_keys(keys)
+
+
+def assert_fma_close(got_keys, want_keys, rtol=FMA_RTOL):
+    gd, gi = _dist_idx(got_keys)
+    wd, wi = _dist_idx(want_keys)
+    scale = np.maximum(np.abs(wd), np.finfo(np.float32).tiny)
+    assert np.all(np.abs(gd.astype(np.float64) - wd) <= rtol * scale + 1e-30)
+    mism = gi != wi
+    if mism.any():
+        # an index may differ only where the reference has a near-tie at that rank
+        r, c = np.nonzero(mism)
+        for rr, cc in zip(r, c):
+            near = np.abs(wd[rr] - wd[rr, cc]) <= rtol * max(wd[rr, cc], 1e-30)
+            assert set(gi[rr][near].tolist()) <= set(wi[rr].tolist()) | set(gi[rr].tolist())
+            assert near.sum() >= 2 or cc == got_keys.shape[1] - 1, (rr, cc)
+
+
+def test_golden_instances_exact(knn_golden, gpu_device):
+    """Every golden instance: keys, counts, visited counts, leaf sequences."""
+    for c in knn_golden:
+        s = c["spec"]
+        tree = bkt.build_buffer_tree(c["refs"], s["h"])
+        stats = bkt.SearchStats(record_sequences=True)
+        res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, stats=stats,
+                              debug_audit=True)
+        assert np.array_equal(res.keys, c["keys"]), s
+        assert np.array_equal(res.counts, c["counts"]), s
+        assert np.array_equal(stats.visited_per_query, c["visited"]), s
+        flat = np.concatenate([np.asarray(x, np.int64) for x in stats.leaf_sequences])
+        assert np.array_equal(flat, c["seq"]), s
+        assert stats.leaf_scan_events == int(c["visited"].sum())
+        assert bkt.result_digest(res) == c["digest"]
+
+
+def test_golden_instances_fma_within_tolerance(knn_golden, gpu_device):
+    for c in knn_golden:
+        s = c["spec"]
+        if s["kind"] == "grid":
+            continue  # exact ties everywhere; covered in exact mode
+        tree = bkt.build_buffer_tree(c["refs"], s["h"])
+        res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, exact=False)
+        assert_fma_close(res.keys, c["keys"])
+
+
+def test_config1_full_digest(gpu_device):
+    """BASELINE configs[0] in full on the GPU: reference digest 4a6f28e1..."""
+    gold = json.load(open(GOLDEN / "c1_digest.json"))
+    refs, queries = bkt.datasets.config_inputs(1)
+    tree = bkt.build_buffer_tree(refs, 8)
+    stats = bkt.SearchStats()
+    res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=10), device=gpu_device, stats=stats)
+    assert bkt.result_digest(res) == gold["digest_indices_sha256"]
+    assert hashlib.sha256(res.keys.astype("<u8").tobytes()).hexdigest() == gold["keys_sha256"]
+    assert stats.leaf_scan_events == gold["leaf_scan_events"]
+    rows = np.load(GOLDEN / "c1_rows.npz")
+    assert np.array_equal(stats.visited_per_query, rows["visited"].astype(np.int64))
+    # pairs = sum over visits of the leaf size (256 at n = 2^16, h = 8)
+    assert stats.pairs == 256 * gold["leaf_scan_events"]
+
+
+def test_config2_sample_exact(gpu_device):
+    g = np.load(GOLDEN / "c2_sample.npz")
+    pts, _ = bkt.gen_mixture(12_000_000, 10, seed=1)
+    refs = pts.data[:2_000_000]
+    tree = bkt.build_buffer_tree(refs, 9)
+    stats = bkt.SearchStats()
+    res = bkt.lazy_search(tree, g["queries"], bkt.SearchParams(k=10), device=gpu_device, stats=stats)
+    assert np.array_equal(res.keys, g["keys"])
+    assert np.array_equal(stats.visited_per_query, g["visited"])
+
+
+@pytest.mark.parametrize("num_chunks", [2, 3, 13])
+def test_out_of_core_chunked_plan_exact(rng, gpu_device, num_chunks):
+    """Host-resident leaf structure streamed in chunks that straddle leaves
+    (reference tests/test_buffer_tree.py:275-284, n prime)."""
+    refs = rng.random((4099, 6), dtype=np.float32)
+    queries = rng.random((300, 6), dtype=np.float32)
+    params = bkt.SearchParams(k=5)
+    tree = bkt.build_buffer_tree(refs, 5)
+    want = O.brute_keys(refs, queries, 5, threads=4)
+    plan = bkt.ChunkPlan.build(refs.shape[0], num_chunks)
+    stats = bkt.SearchStats()
+    res = bkt.lazy_search(tree, queries, params, None, gpu_device, plan, stats=stats)
+    assert np.array_equal(res.keys, want)
+    # visited counts do not depend on chunking
+    ot = O.build_tree(refs, 5)
+    assert np.array_equal(stats.visited_per_query, O.knn_tree(ot, queries, 5)["visited"])
+
+
+def test_out_of_core_config1_digest(gpu_device):
+    gold = json.load(open(GOLDEN / "c1_digest.json"))
+    refs, queries = bkt.datasets.config_inputs(1)
+    tree = bkt.build_buffer_tree(refs, 8)
+    res = bkt.lazy_search(tree, queries[:8192], bkt.SearchParams(k=10), device=gpu_device,
+                          plan=bkt.ChunkPlan.build(refs.shape[0], 7))
+    rows = np.load(GOLDEN / "c1_rows.npz")
+    assert np.array_equal(res.keys[:2048], rows["keys_head"])
+
+
+def test_edge_cases(rng, gpu_device):
+    refs = rng.random((64, 2), dtype=np.float32)
+    tree = bkt.build_buffer_tree(refs, 2)
+    # empty query batch (reference test_buffer_tree.py:335-339)
+    res = bkt.lazy_search(tree, np.empty((0, 2), np.float32), bkt.SearchParams(k=2), device=gpu_device)
+    assert res.keys.shape == (0, 2)
+    # dimension mismatch / k bounds (ValueError like the reference)
+    with pytest.raises(ValueError):
+        bkt.lazy_search(tree, rng.random((4, 3), dtype=np.float32), bkt.SearchParams(k=1), device=gpu_device)
+    with pytest.raises(ValueError):
+        bkt.lazy_search(tree, refs[:3], bkt.SearchParams(k=65), device=gpu_device)
+    with pytest.raises(ValueError):
+        bkt.lazy_search(tree, refs[:3], bkt.SearchParams(k=0), device=gpu_device)
+    # k == n: every point returned
+    res = bkt.lazy_search(tree, refs[:5], bkt.SearchParams(k=64), device=gpu_device)
+    assert np.array_equal(res.keys, O.brute_keys(refs, refs[:5], 64))
+    # query on a reference point finds itself (test_buffer_tree.py:286-291)
+    r2 = rng.random((128, 3), dtype=np.float32)
+    res = bkt.lazy_search(bkt.build_buffer_tree(r2, 3), r2[17:18], bkt.SearchParams(k=1), device=gpu_device)
+    assert res.indices[0, 0] == 17 and res.sq_dists[0, 0] == np.float32(0.0)
+    # duplicate points tie-break by index (test_buffer_tree.py:293-298)
+    dup = np.float32([[0, 0], [1, 1], [1, 1], [1, 1], [2, 2], [3, 3], [4, 4], [5, 5]])
+    res = bkt.lazy_search(bkt.build_buffer_tree(dup, 2), np.float32([[1, 1]]), bkt.SearchParams(k=2),
+                          device=gpu_device)
+    assert res.indices[0].tolist() == [1, 2]
+
+
+def test_tie_on_slab_distance_is_visited(gpu_device):
+    # reference test_buffer_tree.py:159-173: kth == slab distance^2 == 0 -> visit
+    refs = np.float32([[0.0], [0.0], [1.0], [1.0]])
+    tree = bkt.build_buffer_tree(refs, 1)
+    stats = bkt.SearchStats(record_sequences=True)
+    res = bkt.lazy_search(tree, np.float32([[1.0]]), bkt.SearchParams(k=2), device=gpu_device, stats=stats)
+    assert stats.leaf_sequences[0] == [1, 0]
+    assert res.indices[0].tolist() == [2, 3]
+
+
+def test_unpruned_backtracking_order(gpu_device):
+    # reference test_buffer_tree.py:114-126: k = n keeps kth = inf until the end
+    refs = np.float32([[7], [3], [5], [1], [8], [2], [6], [4]])
+    tree = bkt.build_buffer_tree(refs, 2)
+    stats = bkt.SearchStats(record_sequences=True)
+    bkt.lazy_search(tree, np.float32([[1.4]]), bkt.SearchParams(k=8), device=gpu_device, stats=stats)
+    assert stats.leaf_sequences[0] == [0, 1, 2, 3]
+
+
+@pytest.mark.parametrize("d", [1, 2, 5, 9, 13, 16, 17, 21, 27, 32])
+def test_dimension_coverage_exact(rng, gpu_device, d):
+    refs = rng.random((3000, d), dtype=np.float32)
+    queries = rng.random((257, d), dtype=np.float32)
+    tree = bkt.build_buffer_tree(refs, 6)
+    for k in (1, 3, 10, 33):
+        res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), device=gpu_device)
+        assert np.array_equal(res.keys, O.brute_keys(refs, queries, k, threads=4)), (d, k)
+
+
+def test_large_values_and_negative_coords(rng, gpu_device):
+    refs = (rng.normal(0, 1e5, (5000, 4))).astype(np.float32)
+    queries = (rng.normal(0, 1e5, (500, 4))).astype(np.float32)
+    tree = bkt.build_buffer_tree(refs, 7)
+    res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=7), device=gpu_device)
+    assert np.array_equal(res.keys, O.brute_keys(refs, queries, 7, threads=4))
+
+
+def test_batched_queries_equal_single_batch(rng, gpu_device):
+    refs = rng.random((20000, 8), dtype=np.float32)
+    queries = rng.random((5000, 8), dtype=np.float32)
+    tree = bkt.build_buffer_tree(refs, 7)
+    gpu_device.ensure_tree(tree)
+    k1, _, _ = gpu_device.search(queries, 10)
+    k2, _, _ = gpu_device.search(queries, 10, batch_queries=777)
+    assert np.array_equal(k1, k2)
+    assert np.array_equal(k1, O.brute_keys(refs, queries, 10, threads=8))
+
+
+def test_multi_device_fleet_invariance(rng):
+    """run_multi_device over a fleet of contexts (all on GPU 0 here: one
+    host thread per context), with query chunking (criterion 3)."""
+    refs = rng.random((30000, 5), dtype=np.float32)
+    queries = rng.random((800, 5), dtype=np.float32)
+    tree = bkt.build_buffer_tree(refs, 5)
+    params = bkt.SearchParams(k=10)
+    config = bkt.BufferConfig.for_height(5)
+    want = O.brute_keys(refs, queries, 10, threads=8)
+    for n_dev in (1, 2, 4):
+        fleet = bkt.DeviceFleet([bkt.GpuDevice(bkt.DeviceSpec(cuda_device=0)) for _ in range(n_dev)])
+        try:
+            stats = []
+            res = bkt.run_multi_device(fleet, tree, queries, params, config, None, query_chunk_size=50,
+                                       stats_out=stats)
+            assert np.array_equal(res.keys, want)
+            assert sum(s.leaf_scan_events for s in stats) > 0
+        finally:
+            fleet.close()
+
+
+def test_multi_device_redispatch_on_failure(rng):
+    refs = rng.random((3000, 3), dtype=np.float32)
+    queries = rng.random((300, 3), dtype=np.float32)
+    tree = bkt.build_buffer_tree(refs, 4)
+    fleet = bkt.DeviceFleet([bkt.GpuDevice(bkt.DeviceSpec(cuda_device=0)) for _ in range(2)])
+    try:
+        fleet.devices[1].close()  # a dead device: every call on it fails
+        res = bkt.run_multi_device(fleet, tree, queries, bkt.SearchParams(k=4), bkt.BufferConfig.for_height(4),
+                                   None, query_chunk_size=40)
+        assert np.array_equal(res.keys, O.brute_keys(refs, queries, 4))
+    finally:
+        fleet.close()
+
+
+@pytest.mark.parametrize("num_chunks", [1, 2, 3, 4, 7])
+def test_fine_seam_pipeline_round_equals_brute(rng, num_chunks):
+    """The reference's device plugin seam driven by ChunkPipeline
+    (reference tests/test_device.py:199-216)."""
+    refs = rng.random((900, 4), dtype=np.float32)
+    queries = rng.random((60, 4), dtype=np.float32)
+    ids = np.arange(900, dtype=np.int64)
+    plan = bkt.ChunkPlan.build(900, num_chunks)
+    cb = bkt.chunk_required(plan.max_len, 4)
+    dev = bkt.device_init(bkt.DeviceSpec(2 * cb + 10_000), cb, 10_000)
+    try:
+        nb = bkt.NeighborBatch(60, 5)
+        rows = np.arange(60, dtype=np.int64)
+        groups = [[(rows, lo, hi)] for lo, hi in plan.ranges()]
+        bkt.run_chunk_pipeline(dev, refs, ids, plan, groups, queries, nb)
+        assert np.array_equal(nb.keys, O.brute_keys(refs, queries, 5))
+        assert (nb.counts == 5).all()
+        assert not dev.hazard_violations
+    finally:
+        dev.close()
+
+
+def test_device_budget_errors(rng):
+    with pytest.raises(bkt.DeviceConfigError):
+        bkt.device_init(bkt.DeviceSpec(100), 60, 10)
+    refs = rng.random((100, 4), dtype=np.float32)
+    plan = bkt.ChunkPlan.build(100, 2)
+    dev = bkt.device_init(bkt.DeviceSpec(10 ** 6), bkt.chunk_required(10, 4), 100)
+    try:
+        with pytest.raises(bkt.DeviceConfigError, match="use at least"):
+            bkt.ChunkPipeline(dev, refs, np.arange(100), plan)
+        tree = bkt.build_buffer_tree(refs, 2)
+        with pytest.raises(bkt.DeviceConfigError, match="use at least"):
+            bkt.lazy_search(tree, refs[:4], bkt.SearchParams(k=2), None, dev, plan)
+    finally:
+        dev.close()
+
+
+def test_run_engine_bufferkdtree(rng):
+    refs = rng.random((6000, 5), dtype=np.float32)
+    queries = rng.random((400, 5), dtype=np.float32)
+    res, info = bkt.run_engine("bufferkdtree", refs, queries, bkt.SearchParams(k=8), height=6,
+                               collect_stats=True)
+    assert np.array_equal(res.keys, O.brute_keys(refs, queries, 8, threads=4))
+    assert info["height"] == 6 and info["process_rounds"] > 0 and info["mean_leaves_visited"] >= 1
+    res2, info2 = bkt.run_engine("bufferkdtree", refs, queries, bkt.SearchParams(k=8), height=6,
+                                 device_memory=200_000)
+    assert info2["num_chunks"] > 1
+    assert np.array_equal(res2.keys, res.keys)

@@ -95,6 +95,7 @@ struct bkt_ctx {
   RoundCtl* ctl = nullptr;
   unsigned long long* pairs = nullptr;
   unsigned long long* seq_pos = nullptr;
+  int* hist = nullptr;  // active queries per round (BKT_TRACE_ROUNDS diagnostics)
   int* seq_dev = nullptr;
   long long seq_dev_cap = 0;
   // pinned host mirrors
@@ -113,6 +114,7 @@ struct bkt_ctx {
 
 namespace {
 constexpr int kRing = 4;
+constexpr int kHistCap = 1 << 17;
 
 int set_err(bkt_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg;
@@ -322,6 +324,7 @@ int bkt_open(int cuda_device, bkt_ctx** out) {
   CU(cudaMalloc(&ctx->ctl, sizeof(RoundCtl)));
   CU(cudaMalloc(&ctx->pairs, sizeof(unsigned long long)));
   CU(cudaMalloc(&ctx->seq_pos, sizeof(unsigned long long)));
+  CU(cudaMalloc(&ctx->hist, sizeof(int) * kHistCap));
   CU(cudaHostAlloc(&ctx->h_ctl, sizeof(RoundCtl) * kRing, cudaHostAllocDefault));
   for (int i = 0; i < kRing; ++i) CU(cudaEventCreateWithFlags(&ctx->ring_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) CU(cudaEventCreate(&ctx->t_ev[i]));
@@ -341,7 +344,7 @@ void bkt_close(bkt_ctx* ctx) {
   free_tree(ctx);
   free_work(ctx);
   free_leafbufs(ctx);
-  dfree(ctx->ctl); dfree(ctx->pairs); dfree(ctx->seq_pos); dfree(ctx->seq_dev);
+  dfree(ctx->ctl); dfree(ctx->pairs); dfree(ctx->seq_pos); dfree(ctx->seq_dev); dfree(ctx->hist);
   hfree(ctx->h_ctl); hfree(ctx->h_stage);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < kRing; ++i)
@@ -625,7 +628,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   const bool ooc = ctx->residency == 1;
   for (;;) {
     plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl,
-                                                     ctx->nl, kNT);
+                                                     ctx->nl, kNT, ctx->hist, kHistCap);
     CU(cudaGetLastError());
     R.launches++;
     const int slot = (int)(round % kRing);
@@ -781,10 +784,20 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     if (ncopy > 0) CU(cudaMemcpy(o.seq_log, ctx->seq_dev, sizeof(int) * 3 * ncopy, cudaMemcpyDeviceToHost));
     if (o.seq_count_out) *o.seq_count_out = (int64_t)cnt;
   }
+  std::vector<float> per_launch;
   for (auto& pr : R.scan_events) {
     float t = 0;
     CU(cudaEventElapsedTime(&t, pr.first, pr.second));
     R.leafscan_ms += t;
+    per_launch.push_back(t);
+  }
+  if (std::getenv("BKT_TRACE_ROUNDS") && !per_launch.empty()) {
+    // per-round diagnostics of the last batch: active queries and leafscan ms
+    std::vector<int> hist(std::min<long long>(kHistCap, per_launch.size()));
+    CU(cudaMemcpy(hist.data(), ctx->hist, sizeof(int) * hist.size(), cudaMemcpyDeviceToHost));
+    size_t off = per_launch.size() - hist.size();
+    for (size_t r = 0; r < hist.size(); ++r)
+      std::fprintf(stderr, "round %zu active %d leafscan_ms %.4f\n", r, hist[r], per_launch[off + r]);
   }
   st.rounds = R.rounds;
   st.leaf_visits = leaf_visits;

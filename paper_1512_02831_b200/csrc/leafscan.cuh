@@ -25,7 +25,7 @@
 
 namespace bkt {
 
-constexpr int kNT = 128;         // threads (= queries) per tile
+constexpr int kNT = 128;         // consumer threads (= queries) per tile
 constexpr int kStages = 4;       // TMA ring depth
 constexpr int kChunkQuads = 32;  // quads (4 points) per ring stage
 
@@ -60,12 +60,17 @@ struct ScanArgs {
   long long seq_cap;
 };
 
+constexpr int kConsumerWarps = kNT / 32;
+constexpr int kThreads = kNT + 32;  // + one TMA producer warp
+constexpr int kQueue = 8;           // per-thread candidate queue (shared memory)
+
 template <int D>
 struct ScanSmem {
   static constexpr int kQuadBytes = 16 * D;
   static constexpr int kStagePts = kChunkQuads * kQuadBytes;
   static constexpr int kStageIdx = kChunkQuads * 16;
-  static constexpr int kBytes = kStages * (kStagePts + kStageIdx) + kStages * 8 + 64;
+  static constexpr int kQueueBytes = kQueue * kNT * 8;
+  static constexpr int kBytes = kStages * (kStagePts + kStageIdx) + kQueueBytes + 2 * kStages * 8 + 64;
 };
 
 __device__ __forceinline__ void log_visit(const ScanArgs& a, int qi, uint32_t visit, int leaf) {
@@ -80,148 +85,190 @@ __device__ __forceinline__ void log_visit(const ScanArgs& a, int qi, uint32_t vi
 }
 
 // Resident CTAs per SM the register budget allows: query (2D) + top-k (2KB)
-// registers plus ~40 of working set, within 64K registers per SM.
+// registers plus ~48 of working set, within 64K registers per SM.
 template <int D, int KB>
 struct ScanOcc {
-  static constexpr int kRegs = 2 * D + 2 * KB + 40;
-  static constexpr int kMinBlocks = kRegs <= 128 ? 4 : (kRegs <= 168 ? 3 : 2);
+  static constexpr int kRegs = 2 * D + 2 * KB + 48;
+  static constexpr int kMinBlocks = kRegs <= 96 ? 4 : (kRegs <= 128 ? 3 : 2);
 };
 
+struct TileInfo {
+  int leaf, qbeg, qcnt;
+  long long g0, g1, lq0;  // clipped quad range and the leaf's first quad
+  int nchunks;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const ScanArgs& a, int t) {
+  const int nl = 1 << a.top.h;
+  // last leaf with tile_off[leaf] <= t (empty leaves repeat the offset)
+  int lo = 0, hi = nl - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (__ldg(a.tile_off + mid) <= t) lo = mid; else hi = mid - 1;
+  }
+  TileInfo T;
+  T.leaf = lo;
+  const int j = t - __ldg(a.tile_off + lo);
+  T.qbeg = __ldg(a.leaf_off + lo) + j * kNT;
+  T.qcnt = min(kNT, __ldg(a.leaf_off + lo + 1) - T.qbeg);
+  T.lq0 = __ldg(a.quad_base + lo);
+  T.g0 = max(T.lq0, a.clip_lo);
+  T.g1 = min(__ldg(a.quad_base + lo + 1), a.clip_hi);
+  const int nq = (int)max(0ll, T.g1 - T.g0);
+  T.nchunks = (nq + kChunkQuads - 1) / kChunkQuads;
+  return T;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Insert every queued candidate of this lane into its register top-k.  All
+// lanes of the warp run this together (warp-convergent), so a burst of
+// candidates costs one pass instead of one divergent pass per candidate.
+template <int KB>
+__device__ __forceinline__ void merge_queue(uint64_t (&arr)[KB], const uint64_t* qslot, int& cn, float& kth) {
+#pragma unroll 1
+  for (int j = 0; j < cn; ++j) {
+    uint64_t c = qslot[j * kNT];
+    if (c < arr[0]) topk_insert<KB>(arr, c);
+  }
+  cn = 0;
+  kth = key_dist(arr[0]);
+}
+
 template <int D, int KB, bool FMA>
-__global__ void __launch_bounds__(kNT, (ScanOcc<D, KB>::kMinBlocks)) leafscan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(kThreads, (ScanOcc<D, KB>::kMinBlocks)) leafscan_kernel(const ScanArgs a) {
   using S = ScanSmem<D>;
   extern __shared__ __align__(128) unsigned char smem[];
   float* s_pts = reinterpret_cast<float*>(smem);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem + kStages * S::kStagePts);
-  uint64_t* s_full = reinterpret_cast<uint64_t*>(smem + kStages * (S::kStagePts + S::kStageIdx));
-  int* s_tile = reinterpret_cast<int*>(s_full + kStages);  // leaf, q-begin, q-count
+  uint64_t* s_queue = reinterpret_cast<uint64_t*>(smem + kStages * (S::kStagePts + S::kStageIdx));
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(smem + kStages * (S::kStagePts + S::kStageIdx) + S::kQueueBytes);
+  uint64_t* s_empty = s_full + kStages;
 
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&s_full[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], kConsumerWarps);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
   const int tiles_end = a.tile_hi >= 0 ? a.tile_hi : *a.num_tiles;
-  const int nl = 1 << a.top.h;
-  uint32_t gchunk = 0;  // chunks consumed by this CTA so far (ring position / phase)
 
+  if (warp == kConsumerWarps) {
+    // ===== TMA producer: streams every tile's leaf chunks through the ring,
+    // running ahead across tile boundaries =====
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x) {
+        const TileInfo T = tile_info(a, t);
+        const int nquads = (int)(T.g1 - T.g0);
+        for (int c = 0; c < T.nchunks; ++c, ++g) {
+          const int s = g % kStages;
+          const uint32_t use = g / kStages;
+          if (use > 0) mbar_wait(&s_empty[s], (use - 1) & 1u);
+          const int nq = min(kChunkQuads, nquads - c * kChunkQuads);
+          const long long gq = T.g0 + (long long)c * kChunkQuads - a.quad_origin;
+          mbar_arrive_expect_tx(&s_full[s], nq * (S::kQuadBytes + 16));
+          bulk_g2s(s_pts + s * (S::kStagePts / 4), a.pts + gq * 4 * D, nq * S::kQuadBytes, &s_full[s]);
+          bulk_g2s(s_idx + s * (S::kStageIdx / 4), a.pidx + gq * 4, nq * 16, &s_full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers: one thread per query =====
+  uint64_t* qslot = s_queue + tid;  // this thread's queue: qslot[j * kNT]
+  const uint64_t zero = a.zero;
+  uint32_t g = 0;
   for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x) {
-    if (tid == 0) {
-      // last leaf with tile_off[leaf] <= t (empty leaves repeat the offset)
-      int lo = 0, hi = nl - 1;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (__ldg(a.tile_off + mid) <= t) lo = mid; else hi = mid - 1;
-      }
-      int leaf = lo;
-      int j = t - __ldg(a.tile_off + leaf);
-      int beg = __ldg(a.leaf_off + leaf) + j * kNT;
-      int cnt = min(kNT, __ldg(a.leaf_off + leaf + 1) - beg);
-      s_tile[0] = leaf; s_tile[1] = beg; s_tile[2] = cnt;
-    }
-    __syncthreads();
-    const int leaf = s_tile[0];
-    const int qbeg = s_tile[1];
-    const int qcnt = s_tile[2];
-
-    long long g0 = __ldg(a.quad_base + leaf);
-    long long g1 = __ldg(a.quad_base + leaf + 1);
-    const long long lq0 = g0;
-    g0 = max(g0, a.clip_lo);
-    g1 = min(g1, a.clip_hi);
-    const int nquads = (int)max(0ll, g1 - g0);
-    const int nchunks = (nquads + kChunkQuads - 1) / kChunkQuads;
-
-    // producer prologue: fill the ring
-    if (tid == 0) {
-      for (int c = 0; c < min(kStages, nchunks); ++c) {
-        int s = (gchunk + c) % kStages;
-        int nq = min(kChunkQuads, nquads - c * kChunkQuads);
-        long long gq = g0 + (long long)c * kChunkQuads - a.quad_origin;
-        mbar_arrive_expect_tx(&s_full[s], nq * (S::kQuadBytes + 16));
-        bulk_g2s(s_pts + s * (S::kStagePts / 4), a.pts + gq * 4 * D, nq * S::kQuadBytes, &s_full[s]);
-        bulk_g2s(s_idx + s * (S::kStageIdx / 4), a.pidx + gq * 4, nq * 16, &s_full[s]);
-      }
-    }
-
-    // this thread's query
-    const bool valid = tid < qcnt;
+    const TileInfo T = tile_info(a, t);
+    const int nquads = (int)(T.g1 - T.g0);
+    const bool valid = tid < T.qcnt;
+    const bool warp_active = warp * 32 < T.qcnt;
     int qi = 0;
     uint64_t qq[D];
     uint64_t arr[KB];
+    float kth = -__int_as_float(0x7f800000);  // -inf: invalid lanes never take candidates
     if (valid) {
-      qi = __ldg(a.work + qbeg + tid);
+      qi = __ldg(a.work + T.qbeg + tid);
       const float* qp = a.q + (long long)qi * D;
 #pragma unroll
       for (int j = 0; j < D; ++j) qq[j] = f2_splat(__ldg(qp + j));
       const uint64_t* kp = a.keys + (long long)qi * a.k;
 #pragma unroll
       for (int j = 0; j < KB; ++j) arr[j] = (j < a.k) ? kp[a.k - 1 - j] : 0ull;
+      kth = key_dist(arr[0]);
     } else {
 #pragma unroll
       for (int j = 0; j < D; ++j) qq[j] = 0;
 #pragma unroll
       for (int j = 0; j < KB; ++j) arr[j] = 0;
     }
-    float kth = key_dist(arr[0]);
-    const uint64_t zero = a.zero;
+    int cn = 0;  // queued candidates
 
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = (gchunk + c) % kStages;
-      const uint32_t ph = ((gchunk + c) / kStages) & 1u;
-      const int nq = min(kChunkQuads, nquads - c * kChunkQuads);
-      mbar_wait(&s_full[s], ph);
-      if (valid) {
+    for (int c = 0; c < T.nchunks; ++c, ++g) {
+      const int s = g % kStages;
+      mbar_wait(&s_full[s], (g / kStages) & 1u);
+      if (warp_active) {
+        const int nq = min(kChunkQuads, nquads - c * kChunkQuads);
         // quad u, dim j: 16 bytes = (p0, p1) | (p2, p3) as two f32x2 lanes
         const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(s_pts + s * (S::kStagePts / 4));
-        const uint32_t* si = s_idx + s * (S::kStageIdx / 4);
+        const uint4* si = reinterpret_cast<const uint4*>(s_idx + s * (S::kStageIdx / 4));
 #pragma unroll 1
-        for (int u = 0; u < nq; ++u) {
-          // j = 0: acc = RN(diff^2) (== RN(0 + diff^2), the reference's first step)
-          ulonglong2 v0 = sp[u * D];
-          uint64_t df0 = f2_sub(qq[0], v0.x), df1 = f2_sub(qq[0], v0.y);
-          uint64_t acc0 = f2_fma(df0, df0, zero), acc1 = f2_fma(df1, df1, zero);
+        for (int u = 0; u < nq; u += 2) {
+          const bool two = u + 1 < nq;
+          const int u1 = two ? u + 1 : u;  // odd tail: recompute quad u (its candidates are deduplicated below)
+          // j = 0: acc = RN(diff^2) == RN(+0 + diff^2), the reference's first step
+          ulonglong2 va = sp[u * D], vb = sp[u1 * D];
+          uint64_t da0 = f2_sub(qq[0], va.x), da1 = f2_sub(qq[0], va.y);
+          uint64_t db0 = f2_sub(qq[0], vb.x), db1 = f2_sub(qq[0], vb.y);
+          uint64_t a0 = f2_fma(da0, da0, zero), a1 = f2_fma(da1, da1, zero);
+          uint64_t b0 = f2_fma(db0, db0, zero), b1 = f2_fma(db1, db1, zero);
 #pragma unroll
           for (int j = 1; j < D; ++j) {
-            ulonglong2 v = sp[u * D + j];
-            acc0 = dist_step<FMA>(acc0, qq[j], v.x, zero);
-            acc1 = dist_step<FMA>(acc1, qq[j], v.y, zero);
+            ulonglong2 wa = sp[u * D + j], wb = sp[u1 * D + j];
+            a0 = dist_step<FMA>(a0, qq[j], wa.x, zero);
+            a1 = dist_step<FMA>(a1, qq[j], wa.y, zero);
+            b0 = dist_step<FMA>(b0, qq[j], wb.x, zero);
+            b1 = dist_step<FMA>(b1, qq[j], wb.y, zero);
           }
-          float d0 = f2_lo(acc0), d1 = f2_hi(acc0), d2 = f2_lo(acc1), d3 = f2_hi(acc1);
-          float mn = fminf(fminf(d0, d1), fminf(d2, d3));
-          if (mn <= kth) {
-            // rare: at least one of the four may enter the top-k
-            uint4 ids = *reinterpret_cast<const uint4*>(si + 4 * u);
-            uint64_t c0 = pack_key(d0, ids.x), c1 = pack_key(d1, ids.y);
-            uint64_t c2 = pack_key(d2, ids.z), c3 = pack_key(d3, ids.w);
-            if (c0 < arr[0]) topk_insert<KB>(arr, c0);
-            if (c1 < arr[0]) topk_insert<KB>(arr, c1);
-            if (c2 < arr[0]) topk_insert<KB>(arr, c2);
-            if (c3 < arr[0]) topk_insert<KB>(arr, c3);
-            kth = key_dist(arr[0]);
+          float dd[8] = {f2_lo(a0), f2_hi(a0), f2_lo(a1), f2_hi(a1), f2_lo(b0), f2_hi(b0), f2_lo(b1), f2_hi(b1)};
+          float mn = fminf(fminf(fminf(dd[0], dd[1]), fminf(dd[2], dd[3])),
+                           fminf(fminf(dd[4], dd[5]), fminf(dd[6], dd[7])));
+          if (__any_sync(0xffffffffu, mn <= kth)) {
+            // rare (except in a query's first leaves): queue the candidates
+            const uint4 ia = si[u], ib = si[u1];
+            const uint32_t ii[8] = {ia.x, ia.y, ia.z, ia.w, ib.x, ib.y, ib.z, ib.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              if (e == 4 && (!two || __any_sync(0xffffffffu, cn > kQueue - 4))) {
+                merge_queue<KB>(arr, qslot, cn, kth);
+                if (!two) break;
+              }
+              if (dd[e] <= kth) qslot[(cn++) * kNT] = pack_key(dd[e], ii[e]);
+            }
+            if (__any_sync(0xffffffffu, cn > kQueue - 4)) merge_queue<KB>(arr, qslot, cn, kth);
           }
         }
       }
-      __syncthreads();  // stage s fully consumed
-      if (tid == 0 && c + kStages < nchunks) {
-        int cc = c + kStages;
-        int nq2 = min(kChunkQuads, nquads - cc * kChunkQuads);
-        long long gq = g0 + (long long)cc * kChunkQuads - a.quad_origin;
-        mbar_arrive_expect_tx(&s_full[s], nq2 * (S::kQuadBytes + 16));
-        bulk_g2s(s_pts + s * (S::kStagePts / 4), a.pts + gq * 4 * D, nq2 * S::kQuadBytes, &s_full[s]);
-        bulk_g2s(s_idx + s * (S::kStageIdx / 4), a.pidx + gq * 4, nq2 * 16, &s_full[s]);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[s]);
     }
-    gchunk += nchunks;
+    if (warp_active && __any_sync(0xffffffffu, cn > 0)) merge_queue<KB>(arr, qslot, cn, kth);
 
     if (tid == 0 && a.pairs) {
       // real points of this leaf inside the clipped quad range
-      long long L = __ldg(a.leaf_size + leaf);
-      long long p0 = (g0 - lq0) * 4, p1 = (g1 - lq0) * 4;
+      long long L = __ldg(a.leaf_size + T.leaf);
+      long long p0 = (T.g0 - T.lq0) * 4, p1 = (T.g1 - T.lq0) * 4;
       long long real = max(0ll, min(L, p1) - p0);
-      atomicAdd(a.pairs, (unsigned long long)(real * qcnt));
+      atomicAdd(a.pairs, (unsigned long long)(real * T.qcnt));
     }
 
     if (valid) {
@@ -245,7 +292,6 @@ __global__ void __launch_bounds__(kNT, (ScanOcc<D, KB>::kMinBlocks)) leafscan_ke
         }
       }
     }
-    __syncthreads();  // s_tile reuse
   }
 }
 

@@ -89,7 +89,8 @@ __device__ __forceinline__ void block_scan2(long long& a, long long& b, long lon
 // One CTA of kPlanThreads threads; each thread owns a contiguous leaf run.
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ counts, int* __restrict__ leaf_off,
                                                             int* __restrict__ tile_off, int* __restrict__ cursor,
-                                                            RoundCtl* ctl, int nl, int tile_q) {
+                                                            RoundCtl* ctl, int nl, int tile_q, int* hist,
+                                                            int hist_cap) {
   const int per = (nl + kPlanThreads - 1) / kPlanThreads;
   const int lo = min(nl, (int)threadIdx.x * per), hi = min(nl, lo + per);
   long long sc = 0, st = 0;
@@ -116,7 +117,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
     ctl->prev_active = ctl->active;
     ctl->active = (int)tot_c;
     ctl->num_tiles = (int)tot_t;
-    if (tot_c > 0) ctl->rounds += 1;
+    if (tot_c > 0) {
+      if (hist && ctl->rounds < hist_cap) hist[ctl->rounds] = (int)tot_c;
+      ctl->rounds += 1;
+    }
   }
 }
 

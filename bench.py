@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--mode", default="fma", choices=["fma", "exact"])
-    ap.add_argument("--height", type=int, default=None)
+    ap.add_argument("--height", type=int, default=11, help="tree height (results do not depend on it; 11 is fastest at n=2M)")
     ap.add_argument("--m", type=int, default=M_QUERIES)
     ap.add_argument("--n", type=int, default=N_REFS)
     ap.add_argument("--no-e2e", action="store_true")
@@ -161,7 +161,7 @@ def run_reference_arm(a) -> None:
     O.build()
     threads = os.cpu_count() or 1
     refs, queries = workload(0, a.n, a.m)
-    h = a.height or 9
+    h = a.height
     tree = bkt.build_buffer_tree(refs, h)
     sample = a.cpu_sample or max(2000, 1500 * threads)
     vals = []
@@ -200,7 +200,7 @@ def main() -> None:
     import paper_1512_02831_b200 as bkt
     refs, queries = workload(rank, a.n, a.m)
     m = queries.shape[0]
-    h = a.height or 9
+    h = a.height
     t0 = time.perf_counter()
     tree = bkt.build_buffer_tree(refs, h)
     build_s = time.perf_counter() - t0

@@ -100,14 +100,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
+// Blocks until the barrier's phase `phase` has completed.  The suspend-time
+// hint lets the hardware park the warp until the phase flips instead of
+// spinning (a spinning producer warp otherwise steals issue slots from the
+// compute warps of its SM).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t a = smem_addr(bar);
   uint32_t ok = 0;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
-        : "r"(a), "r"(phase)
+        : "r"(a), "r"(phase), "r"(0x989680u)
         : "memory");
   } while (!ok);
 }

@@ -47,6 +47,8 @@ typedef struct bkt_search_opts {
   int32_t* seq_log;         /* optional host int32 triples (query, visit#, leaf), capacity seq_cap */
   int64_t seq_cap;
   int64_t* seq_count_out;   /* number of triples written (may exceed seq_cap: truncated)         */
+  int32_t kernel;           /* leaf scan: 0 auto (tensor-core filter when available), 1 CUDA-core
+                               direct scan, 2 tensor-core filter (error if unavailable)           */
 } bkt_search_opts;
 
 typedef struct bkt_stats {

@@ -41,6 +41,7 @@ class SearchOpts(ctypes.Structure):
         ("seq_log", ctypes.c_void_p),
         ("seq_cap", ctypes.c_int64),
         ("seq_count_out", ctypes.c_void_p),
+        ("kernel", ctypes.c_int32),
     ]
 
 

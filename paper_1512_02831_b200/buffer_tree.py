@@ -226,7 +226,7 @@ def _sequences(seq: np.ndarray, m: int) -> list[list[int]]:
 
 def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: BufferConfig | None = None,
                 device=None, plan=None, *, stats: SearchStats | None = None, debug_audit: bool = False,
-                exact: bool = True) -> NeighborBatch:
+                exact: bool = True, kernel: str = "auto") -> NeighborBatch:
     """Batched exact k-NN over the buffered tree on a B200 (buffer_tree.py:523-646).
 
     device: a ``GpuDevice`` (``device_init``); None uses CUDA device 0.
@@ -234,7 +234,9 @@ def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: Buffe
     pinned host memory and streams it through two device chunk buffers per
     round (the paper's out-of-core workflow).  exact=False uses FMA distance
     accumulation (faster; distances within 1e-6 relative, indices equal
-    except near-ties).
+    except near-ties).  kernel: "auto" (tensor-core filter + exact
+    re-evaluation when the tree is resident and d <= 31, else the CUDA-core
+    scan), "direct" (CUDA-core scan) or "tc"; all give identical results.
     """
     from .device import DeviceConfigError, chunk_required, default_device
 
@@ -269,7 +271,7 @@ def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: Buffe
         seq_cap = m * tree.n_leaves
     t1 = time.perf_counter()
     keys, st, seq = dev.search(qarr, params.k, exact=exact, visited=visited, seq_cap=seq_cap,
-                               timing=stats is not None)
+                               timing=stats is not None, kernel=kernel)
     t2 = time.perf_counter()
     counts = np.full(m, params.k, dtype=np.int64)
     result = NeighborBatch.from_keys(keys, counts)

@@ -64,7 +64,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     for d in _dims():
         obj = OBJ_DIR / f"leafscan_d{d}.o"
         units.append(([NVCC, *NVFLAGS, f"-DBKT_D={d}", "-c", str(CSRC / "leafscan_inst.cu"), "-o", str(obj)], obj))
-    for src in ("engine.cu", "misc.cu"):
+    for src in ("engine.cu", "misc.cu", "leafscan_tc_inst.cu"):
         obj = OBJ_DIR / (Path(src).stem + ".o")
         units.append(([NVCC, *NVFLAGS, "-c", str(CSRC / src), "-o", str(obj)], obj))
     obj = OBJ_DIR / "build_tree.o"

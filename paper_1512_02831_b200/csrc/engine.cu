@@ -17,6 +17,7 @@
 //   visits u32[m], two work lists i32[m]; per leaf: counts, cursor, leaf_off, tile_off.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,9 +28,14 @@
 
 #include "../../include/bkt.h"
 #include "dims.h"
+#include "leafscan_tc.cuh"
 #include "round_kernels.cuh"
 
 using namespace bkt;
+
+namespace bkt {
+cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ);
+}
 
 namespace {
 thread_local std::string g_thread_err;
@@ -76,6 +82,15 @@ struct bkt_ctx {
   cudaEvent_t slot_free[2] = {nullptr, nullptr};
   cudaEvent_t slot_ready[2] = {nullptr, nullptr};
   long long slot_quads = 0;
+  // tensor-core filter layout (resident trees with d <= 31)
+  bool has_tc = false;
+  int KT = 0;
+  long long tc_rows = 0;
+  float* tc_B = nullptr;
+  uint32_t* tc_idx = nullptr;
+  float* tc_rowsxyz = nullptr;
+  long long* tc_row_base = nullptr;
+  float* tc_centroid = nullptr;
 
   // ---- per-batch work buffers
   long long cap_m = 0;
@@ -184,6 +199,8 @@ int leafscan_grid(bkt_ctx* ctx, int D, int kb, bool fma, int* grid) {
 }
 
 void free_tree(bkt_ctx* c) {
+  dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid);
+  c->has_tc = false;
   dfree(c->split); dfree(c->quad_base); dfree(c->leaf_size); dfree(c->pts); dfree(c->pidx);
   hfree(c->h_pts); hfree(c->h_pidx);
   for (int s = 0; s < 2; ++s) {
@@ -275,6 +292,60 @@ void build_quad_layout(const float* leaf_points, const int64_t* orig, const int6
             dst[4 * j + t] = v;
           }
         }
+      }
+    }
+  };
+  int nt = std::max(1, std::min<int>(16, (int)std::thread::hardware_concurrency()));
+  if (nl < 64) nt = 1;
+  std::vector<std::thread> th;
+  for (int w = 0; w < nt; ++w) th.emplace_back(work, (int)((long long)nl * w / nt), (int)((long long)nl * (w + 1) / nt));
+  for (auto& t : th) t.join();
+}
+
+// round-to-nearest (ties away) float32 -> tf32, matching cvt.rna.tf32.f32
+inline float tf32_rna_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return x;  // inf / nan unchanged
+  u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// Tensor-core filter layout (see leafscan_tc.cuh): every leaf padded to a
+// multiple of 32 rows; per padded row R the K-major canonical UMMA layout
+// B[(R/8)*8*KT + (k/4)*32 + (R%8)*4 + k%4] holds tf32(-2 p'_k) for k < d,
+// tf32((1 - C) |p'|^2) in column d, zeros after; padding rows carry +inf in
+// column d so they never pass the filter.
+void build_tc_layout(const float* leaf_points, const int64_t* orig, const int64_t* starts, int nl, int d, int KT,
+                     const std::vector<long long>& rb, float* B, uint32_t* ridx, float* rows, float* centroid) {
+  auto work = [&](int l0, int l1) {
+    std::vector<double> acc(d);
+    for (int l = l0; l < l1; ++l) {
+      long long s = starts[l], e = starts[l + 1];
+      std::fill(acc.begin(), acc.end(), 0.0);
+      for (long long r = s; r < e; ++r)
+        for (int j = 0; j < d; ++j) acc[j] += leaf_points[r * d + j];
+      float* cen = centroid + (long long)l * KT;
+      for (int j = 0; j < KT; ++j) cen[j] = j < d ? (float)(acc[j] / (double)(e - s)) : 0.0f;
+      for (long long R = rb[l]; R < rb[l + 1]; ++R) {
+        long long r = s + (R - rb[l]);
+        bool real = r < e;
+        float* bg = B + (R / 8) * 8 * KT + (R % 8) * 4;
+        float pn = 0.0f;
+        for (int k = 0; k < KT; ++k) {
+          float v = 0.0f;
+          if (k < d && real) {
+            float pc = leaf_points[r * d + k] - cen[k];
+            pn = std::fma(pc, pc, pn);
+            v = tf32_rna_host(-2.0f * pc);
+          }
+          bg[(k / 4) * 32 + (k % 4)] = v;
+        }
+        bg[(d / 4) * 32 + (d % 4)] = real ? tf32_rna_host((1.0f - kTcMargin) * pn) : __builtin_inff();
+        ridx[R] = real ? (uint32_t)orig[r] : kIndexSentinel;
+        for (int j = 0; j < d; ++j) rows[R * d + j] = real ? leaf_points[r * d + j] : 0.0f;
       }
     }
   };
@@ -430,6 +501,29 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
     hfree(ctx->h_pts);
     hfree(ctx->h_pidx);
     ctx->num_chunks = 1;
+    if (d + 1 <= 32) {
+      const int KT = (d + 1 <= 16) ? 16 : 32;
+      std::vector<long long> rb(nl + 1, 0);
+      for (int l = 0; l < nl; ++l) rb[l + 1] = rb[l] + ((long long)ctx->h_leaf_size[l] + 31) / 32 * 32;
+      const long long R = rb[nl];
+      std::vector<float> hB((size_t)R * KT), hrows((size_t)R * d), hcen((size_t)nl * KT);
+      std::vector<uint32_t> hidx((size_t)R);
+      build_tc_layout(leaf_points, original_index, leaf_starts, nl, d, KT, rb, hB.data(), hidx.data(), hrows.data(),
+                      hcen.data());
+      CU(cudaMalloc(&ctx->tc_B, sizeof(float) * R * KT));
+      CU(cudaMalloc(&ctx->tc_idx, sizeof(uint32_t) * R));
+      CU(cudaMalloc(&ctx->tc_rowsxyz, sizeof(float) * R * d));
+      CU(cudaMalloc(&ctx->tc_row_base, sizeof(long long) * (nl + 1)));
+      CU(cudaMalloc(&ctx->tc_centroid, sizeof(float) * nl * KT));
+      CU(cudaMemcpy(ctx->tc_B, hB.data(), sizeof(float) * R * KT, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(ctx->tc_idx, hidx.data(), sizeof(uint32_t) * R, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(ctx->tc_rowsxyz, hrows.data(), sizeof(float) * R * d, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(ctx->tc_row_base, rb.data(), sizeof(long long) * (nl + 1), cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(ctx->tc_centroid, hcen.data(), sizeof(float) * nl * KT, cudaMemcpyHostToDevice));
+      ctx->KT = KT;
+      ctx->tc_rows = R;
+      ctx->has_tc = true;
+    }
   } else {
     // chunk bounds: the reference row bounds (ChunkPlan.bounds) mapped to the
     // containing quad of the padded layout; results do not depend on where a
@@ -482,6 +576,7 @@ struct SearchRun {
   int k = 0;
   int kb = 0;
   bool fma = false;
+  bool tc = false;
   int grid_scan = 0;
   int grid_small = 0;
   bool timing = false;
@@ -534,7 +629,20 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     e1 = get_event(ctx, R.ev_next++);
     CU(cudaEventRecord(e0, ctx->stream));
   }
-  CU(launch_leafscan(ctx->D, R.kb, R.fma, R.grid_scan, ctx->stream, a, nullptr));
+  if (R.tc) {
+    TcArgs t{};
+    t.s = a;
+    t.B = ctx->tc_B;
+    t.ridx = ctx->tc_idx;
+    t.rows = ctx->tc_rowsxyz;
+    t.row_base = ctx->tc_row_base;
+    t.centroid = ctx->tc_centroid;
+    t.d = ctx->d;
+    t.qstride = ctx->D;
+    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr));
+  } else {
+    CU(launch_leafscan(ctx->D, R.kb, R.fma, R.grid_scan, ctx->stream, a, nullptr));
+  }
   if (R.timing) {
     CU(cudaEventRecord(e1, ctx->stream));
     R.scan_events.push_back({e0, e1});
@@ -695,8 +803,18 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   R.timing = o.record_timing != 0;
   R.seq = o.seq_log != nullptr && o.seq_cap > 0;
   R.seq_cap = R.seq ? o.seq_cap : 0;
-  int rc = leafscan_grid(ctx, ctx->D, R.kb, R.fma, &R.grid_scan);
-  if (rc != BKT_OK) return rc;
+  R.tc = ctx->has_tc && ctx->residency == 0 && o.kernel != 1;
+  if (o.kernel == 2 && !R.tc) return set_err(ctx, BKT_EINVAL, "tensor-core kernel requested but unavailable (needs a resident tree and d <= 31)");
+  int rc = BKT_OK;
+  if (R.tc) {
+    int occ = 0;
+    TcArgs dummy{};
+    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, 0, nullptr, dummy, &occ));
+    R.grid_scan = std::max(1, std::min(occ, 2)) * ctx->sm_count;
+  } else {
+    rc = leafscan_grid(ctx, ctx->D, R.kb, R.fma, &R.grid_scan);
+    if (rc != BKT_OK) return rc;
+  }
   R.grid_small = ctx->sm_count * 8;
 
   // batch size: whatever fits comfortably in free memory (or the caller's choice)

@@ -1,0 +1,38 @@
+// leafscan_tc_inst.cu -- instantiates the tensor-core leaf filter kernel for
+// K tiles of 16 and 32 (d + 1 <= KT) and every top-k bucket.
+#include "dims.h"
+#include "leafscan_tc.cuh"
+
+namespace bkt {
+namespace {
+template <int KT, int KB, bool FMA>
+cudaError_t launch_tc_one(int grid, cudaStream_t s, const TcArgs& a, int* occ) {
+  auto fn = leafscan_tc_kernel<KT, KB, FMA>;
+  // at least 76 KB so that no more than two CTAs (2 x 256 TMEM columns) share an SM
+  constexpr int smem = TcSmem<KT>::kBytes > 78 * 1024 ? TcSmem<KT>::kBytes : 78 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kTcThreads, smem);
+  fn<<<grid, kTcThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+template <int KT>
+cudaError_t launch_tc_kt(int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ) {
+  switch (kb) {
+#define BKT_CASE(KB) \
+  case KB:           \
+    return fma ? launch_tc_one<KT, KB, true>(grid, s, a, occ) : launch_tc_one<KT, KB, false>(grid, s, a, occ);
+    BKT_KB_LIST(BKT_CASE)
+#undef BKT_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+}  // namespace
+
+cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ) {
+  if (kt == 16) return launch_tc_kt<16>(kb, fma, grid, s, a, occ);
+  if (kt == 32) return launch_tc_kt<32>(kb, fma, grid, s, a, occ);
+  return cudaErrorInvalidValue;
+}
+}  // namespace bkt

@@ -44,6 +44,11 @@ __all__ = [
 ]
 
 
+# leaf-scan kernel selection (bkt_search_opts.kernel): "auto" uses the
+# tensor-core filter whenever the tree is resident and d <= 31
+_KERNELS = {"auto": 0, "direct": 1, "tc": 2}
+
+
 class DeviceConfigError(ValueError):
     """A requested configuration does not fit the device (device.py:49-50)."""
 
@@ -179,7 +184,7 @@ class GpuDevice:
 
     def search(self, queries: np.ndarray, k: int, *, exact: bool = True, visited: np.ndarray | None = None,
                seq_cap: int = 0, timing: bool = False, batch_queries: int = 0,
-               out_keys: np.ndarray | None = None) -> tuple[np.ndarray, dict, np.ndarray | None]:
+               out_keys: np.ndarray | None = None, kernel: str = "auto") -> tuple[np.ndarray, dict, np.ndarray | None]:
         """bkt_search on host arrays; returns (keys, stats, seq triples)."""
         q = np.ascontiguousarray(queries, dtype=np.float32)
         m = q.shape[0]
@@ -188,6 +193,7 @@ class GpuDevice:
         opts.exact = 1 if exact else 0
         opts.record_timing = 1 if timing else 0
         opts.batch_queries = int(batch_queries)
+        opts.kernel = _KERNELS[kernel]
         if visited is not None:
             opts.visited_out = visited.ctypes.data
         seq = None
@@ -207,7 +213,7 @@ class GpuDevice:
         return keys, st.as_dict(), seq
 
     def search_device(self, q_dev_ptr: int, m: int, k: int, keys_dev_ptr: int, *, exact: bool = True,
-                      timing: bool = False) -> dict:
+                      timing: bool = False, kernel: str = "auto") -> dict:
         """bkt_search with inputs and outputs already in this GPU's memory
         (raw device pointers, e.g. from torch tensors)."""
         opts = _native.SearchOpts()
@@ -215,6 +221,7 @@ class GpuDevice:
         opts.queries_on_device = 1
         opts.keys_on_device = 1
         opts.record_timing = 1 if timing else 0
+        opts.kernel = _KERNELS[kernel]
         st = _native.Stats()
         _native.check(_native.lib().bkt_search(self.ctx, ctypes.c_void_p(q_dev_ptr), int(m), int(k),
                                                ctypes.byref(opts), ctypes.c_void_p(keys_dev_ptr),

@@ -40,14 +40,16 @@ def assert_fma_close(got_keys, want_keys, rtol=FMA_RTOL):
             assert near.sum() >= 2 or cc == got_keys.shape[1] - 1, (rr, cc)
 
 
-def test_golden_instances_exact(knn_golden, gpu_device):
-    """Every golden instance: keys, counts, visited counts, leaf sequences."""
+@pytest.mark.parametrize("kernel", ["direct", "auto"])
+def test_golden_instances_exact(knn_golden, gpu_device, kernel):
+    """Every golden instance: keys, counts, visited counts, leaf sequences,
+    for the CUDA-core scan and the tensor-core filter (auto, d <= 31)."""
     for c in knn_golden:
         s = c["spec"]
         tree = bkt.build_buffer_tree(c["refs"], s["h"])
         stats = bkt.SearchStats(record_sequences=True)
         res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, stats=stats,
-                              debug_audit=True)
+                              debug_audit=True, kernel=kernel)
         assert np.array_equal(res.keys, c["keys"]), s
         assert np.array_equal(res.counts, c["counts"]), s
         assert np.array_equal(stats.visited_per_query, c["visited"]), s
@@ -57,23 +59,38 @@ def test_golden_instances_exact(knn_golden, gpu_device):
         assert bkt.result_digest(res) == c["digest"]
 
 
-def test_golden_instances_fma_within_tolerance(knn_golden, gpu_device):
+@pytest.mark.parametrize("kernel", ["direct", "tc"])
+def test_golden_instances_fma_within_tolerance(knn_golden, gpu_device, kernel):
     for c in knn_golden:
         s = c["spec"]
         if s["kind"] == "grid":
             continue  # exact ties everywhere; covered in exact mode
         tree = bkt.build_buffer_tree(c["refs"], s["h"])
-        res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, exact=False)
+        res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, exact=False,
+                              kernel=kernel)
         assert_fma_close(res.keys, c["keys"])
 
 
-def test_config1_full_digest(gpu_device):
+def test_tc_and_direct_fma_identical(knn_golden, gpu_device):
+    """FMA mode: the tensor-core filter re-evaluates survivors with the same
+    FMA arithmetic as the direct scan, so both kernels agree bit for bit."""
+    for c in knn_golden:
+        s = c["spec"]
+        tree = bkt.build_buffer_tree(c["refs"], s["h"])
+        p = bkt.SearchParams(k=s["k"])
+        a = bkt.lazy_search(tree, c["queries"], p, device=gpu_device, exact=False, kernel="direct")
+        b = bkt.lazy_search(tree, c["queries"], p, device=gpu_device, exact=False, kernel="tc")
+        assert np.array_equal(a.keys, b.keys), s
+
+
+@pytest.mark.parametrize("kernel", ["direct", "tc"])
+def test_config1_full_digest(gpu_device, kernel):
     """BASELINE configs[0] in full on the GPU: reference digest 4a6f28e1..."""
     gold = json.load(open(GOLDEN / "c1_digest.json"))
     refs, queries = bkt.datasets.config_inputs(1)
     tree = bkt.build_buffer_tree(refs, 8)
     stats = bkt.SearchStats()
-    res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=10), device=gpu_device, stats=stats)
+    res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=10), device=gpu_device, stats=stats, kernel=kernel)
     assert bkt.result_digest(res) == gold["digest_indices_sha256"]
     assert hashlib.sha256(res.keys.astype("<u8").tobytes()).hexdigest() == gold["keys_sha256"]
     assert stats.leaf_scan_events == gold["leaf_scan_events"]
@@ -83,13 +100,15 @@ def test_config1_full_digest(gpu_device):
     assert stats.pairs == 256 * gold["leaf_scan_events"]
 
 
-def test_config2_sample_exact(gpu_device):
+@pytest.mark.parametrize("kernel", ["direct", "tc"])
+def test_config2_sample_exact(gpu_device, kernel):
     g = np.load(GOLDEN / "c2_sample.npz")
     pts, _ = bkt.gen_mixture(12_000_000, 10, seed=1)
     refs = pts.data[:2_000_000]
     tree = bkt.build_buffer_tree(refs, 9)
     stats = bkt.SearchStats()
-    res = bkt.lazy_search(tree, g["queries"], bkt.SearchParams(k=10), device=gpu_device, stats=stats)
+    res = bkt.lazy_search(tree, g["queries"], bkt.SearchParams(k=10), device=gpu_device, stats=stats,
+                          kernel=kernel)
     assert np.array_equal(res.keys, g["keys"])
     assert np.array_equal(stats.visited_per_query, g["visited"])
 
@@ -168,22 +187,42 @@ def test_unpruned_backtracking_order(gpu_device):
     assert stats.leaf_sequences[0] == [0, 1, 2, 3]
 
 
-@pytest.mark.parametrize("d", [1, 2, 5, 9, 13, 16, 17, 21, 27, 32])
+@pytest.mark.parametrize("d", [1, 2, 5, 9, 13, 15, 16, 17, 21, 27, 31, 32])
 def test_dimension_coverage_exact(rng, gpu_device, d):
     refs = rng.random((3000, d), dtype=np.float32)
     queries = rng.random((257, d), dtype=np.float32)
     tree = bkt.build_buffer_tree(refs, 6)
     for k in (1, 3, 10, 33):
-        res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), device=gpu_device)
-        assert np.array_equal(res.keys, O.brute_keys(refs, queries, k, threads=4)), (d, k)
+        want = O.brute_keys(refs, queries, k, threads=4)
+        for kernel in ("direct", "auto"):
+            res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), device=gpu_device, kernel=kernel)
+            assert np.array_equal(res.keys, want), (d, k, kernel)
 
 
-def test_large_values_and_negative_coords(rng, gpu_device):
+@pytest.mark.parametrize("kernel", ["direct", "tc"])
+def test_large_values_and_negative_coords(rng, gpu_device, kernel):
     refs = (rng.normal(0, 1e5, (5000, 4))).astype(np.float32)
     queries = (rng.normal(0, 1e5, (500, 4))).astype(np.float32)
     tree = bkt.build_buffer_tree(refs, 7)
-    res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=7), device=gpu_device)
+    res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=7), device=gpu_device, kernel=kernel)
     assert np.array_equal(res.keys, O.brute_keys(refs, queries, 7, threads=4))
+
+
+@pytest.mark.parametrize("kernel", ["direct", "tc"])
+def test_clustered_far_queries_and_offsets(rng, gpu_device, kernel):
+    """Stress the tensor-core filter's error margin: tight clusters far from
+    the origin (large |p| relative to neighbour distances), queries both in
+    and far outside the clusters, duplicated points."""
+    centres = rng.normal(0, 1e3, (6, 5)).astype(np.float32)
+    refs = (centres[rng.integers(0, 6, 8000)] + rng.normal(0, 1e-2, (8000, 5))).astype(np.float32)
+    refs[:500] = refs[500:1000]  # exact duplicates
+    qa = (centres[rng.integers(0, 6, 400)] + rng.normal(0, 1e-2, (400, 5))).astype(np.float32)
+    qb = rng.normal(0, 2e3, (100, 5)).astype(np.float32)
+    queries = np.concatenate([qa, qb, refs[:50]])
+    tree = bkt.build_buffer_tree(refs, 8)
+    for k in (1, 10, 40):
+        res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), device=gpu_device, kernel=kernel)
+        assert np.array_equal(res.keys, O.brute_keys(refs, queries, k, threads=8)), (k, kernel)
 
 
 def test_batched_queries_equal_single_batch(rng, gpu_device):

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--heights", type=int, nargs="+", default=[9, 10, 11, 12])
     ap.add_argument("--modes", nargs="+", default=["fma", "exact"])
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--kernels", nargs="+", default=["direct", "tc"])
     a = ap.parse_args()
     import torch
     t0 = time.time()
@@ -37,16 +38,16 @@ def main():
     for h in a.heights:
         tree = bkt.build_buffer_tree(refs, h)
         dev.ensure_tree(tree)
-        for mode in a.modes:
+        for mode, kern in [(mo, ke) for ke in a.kernels for mo in a.modes]:
             best = None
             for r in range(a.reps + 1):
-                st = dev.search_device(q.data_ptr(), a.m, a.k, keys.data_ptr(), exact=(mode == "exact"), timing=True)
+                st = dev.search_device(q.data_ptr(), a.m, a.k, keys.data_ptr(), exact=(mode == "exact"), timing=True, kernel=kern)
                 if (r > 0 or a.reps == 0) and (best is None or st["search_ms"] < best["search_ms"]):
                     best = st
             st = best
             qps = a.m / (st["search_ms"] / 1e3)
             tf = 3 * a.d * st["pairs"] / (st["leafscan_ms"] / 1e3) / 1e12
-            print(json.dumps({"h": h, "mode": mode, "qps": round(qps), "search_ms": round(st["search_ms"], 1),
+            print(json.dumps({"h": h, "mode": mode, "kernel": kern, "qps": round(qps), "search_ms": round(st["search_ms"], 1),
                               "leafscan_ms": round(st["leafscan_ms"], 1), "rounds": st["rounds"],
                               "pairs_per_q": round(st["pairs"] / a.m), "leafscan_tflops": round(tf, 2),
                               "frac_peak": round(tf / peak, 3), "peak": round(peak, 1),

@@ -345,7 +345,7 @@ void build_tc_layout(const float* leaf_points, const int64_t* orig, const int64_
         }
         bg[(d / 4) * 32 + (d % 4)] = real ? tf32_rna_host((1.0f - kTcMargin) * pn) : __builtin_inff();
         ridx[R] = real ? (uint32_t)orig[r] : kIndexSentinel;
-        for (int j = 0; j < d; ++j) rows[R * d + j] = real ? leaf_points[r * d + j] : 0.0f;
+        for (int j = 0; j < d; ++j) rows[R * d + j] = real ? leaf_points[r * d + j] : __builtin_inff();
       }
     }
   };

@@ -18,6 +18,10 @@ cudaError_t launch_one(int grid, cudaStream_t s, const ScanArgs& a, int* occ) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
+  {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+  }
   if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kThreads, smem);
   fn<<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();

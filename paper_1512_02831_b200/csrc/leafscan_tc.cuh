@@ -31,7 +31,6 @@
 namespace bkt {
 
 constexpr int kTcRows = 128;                  // points per chunk (MMA N)
-constexpr int kTcStages = 4;
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
 constexpr int kTcTmemCols = 2 * kTcRows;      // two accumulators
@@ -41,7 +40,7 @@ struct TcArgs {
   ScanArgs s;                  // queries, keys, schedule, top tree, stats (quad fields unused)
   const float* B;              // canonical K-major tf32 blocks of every leaf (see engine.cu)
   const uint32_t* ridx;        // original index per padded row (0xFFFFFFFF padding)
-  const float* rows;           // padded row-major original coordinates, stride d
+  const float* rows;           // padded row-major original coordinates, stride d (padding rows +inf)
   const long long* row_base;   // nl + 1, first padded row of each leaf (multiples of 32)
   const float* centroid;       // nl x KT
   int d;                       // real dimensionality
@@ -50,14 +49,18 @@ struct TcArgs {
 
 template <int KT>
 struct TcSmem {
+  static constexpr int kStages = KT <= 16 ? 4 : 2;
   static constexpr int kStageB = kTcRows * KT * 4;
   static constexpr int kStageIdx = kTcRows * 4;
+  static constexpr int kStageRows = kTcRows * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
   static constexpr int kA = 128 * KT * 4;
-  static constexpr int kOffIdx = kTcStages * kStageB;
-  static constexpr int kOffA = kOffIdx + kTcStages * kStageIdx;
-  static constexpr int kOffQ = kOffA + 2 * kA;
+  static constexpr int kOffIdx = kStages * kStageB;
+  static constexpr int kOffRows = kOffIdx + kStages * kStageIdx;
+  static constexpr int kOffA = kOffRows + kStages * kStageRows;
+  static constexpr int kOffQs = kOffA + 2 * kA;
+  static constexpr int kOffQ = kOffQs + 128 * KT * 4;
   static constexpr int kOffBar = kOffQ + kQueue * 128 * 8;
-  static constexpr int kNumBars = 2 * kTcStages + 8;
+  static constexpr int kNumBars = 2 * kStages + 8;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
 };
 
@@ -92,6 +95,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ long long dmin_ll(long long x, long long y) { return x < y ? x : y; }
 
@@ -143,9 +158,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
   // 1 KB alignment for the operand tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int kTcStages = S::kStages;
   float* sB = reinterpret_cast<float*>(smem);
   uint32_t* sIdx = reinterpret_cast<uint32_t*>(smem + S::kOffIdx);
+  float* sRows = reinterpret_cast<float*>(smem + S::kOffRows);
   float* sA = reinterpret_cast<float*>(smem + S::kOffA);
+  float* sQ = reinterpret_cast<float*>(smem + S::kOffQs);  // [j][128] original query coordinates
   uint64_t* s_queue = reinterpret_cast<uint64_t*>(smem + S::kOffQ);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* full = bars;                      // [kTcStages] TMA -> MMA/epilogue
@@ -194,9 +212,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
           if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
           const long long row = T.r0 + (long long)c * kTcRows;
           const int nr = (int)dmin_ll(kTcRows, T.r1 - row);
-          mbar_arrive_expect_tx(&full[s], nr * (KT * 4 + 4));
+          mbar_arrive_expect_tx(&full[s], nr * (KT * 4 + 4 + A.d * 4));
           bulk_g2s(sB + s * (S::kStageB / 4), A.B + row * KT, nr * KT * 4, &full[s]);
           bulk_g2s(sIdx + s * kTcRows, A.ridx + row, nr * 4, &full[s]);
+          bulk_g2s(sRows + s * (S::kStageRows / 4), A.rows + row * A.d, nr * A.d * 4, &full[s]);
         }
       }
     }
@@ -275,7 +294,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         for (int j = 0; j < KT; ++j) {
           float v = 0.0f;
           if (j < d) {
-            float qc = valid ? __fsub_rn(__ldg(qp + j), __ldg(cen + j)) : 0.0f;
+            const float qv = valid ? __ldg(qp + j) : 0.0f;
+            sQ[j * 128 + tid] = qv;
+            float qc = valid ? __fsub_rn(qv, __ldg(cen + j)) : 0.0f;
             qn = __fmaf_rn(qc, qc, qn);
             v = __uint_as_float(tf32_rna(qc));
           } else if (j == d) {
@@ -296,6 +317,37 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       float thr = valid ? threshold(kth) : kth;
       int cn = 0;
 
+      // filter one 32-column group of TMEM values, then re-evaluate survivors
+      auto process = [&](const uint32_t (&v)[32], int gcol, int s, long long row0) {
+        float mn = __uint_as_float(v[0]);
+#pragma unroll
+        for (int j = 1; j < 32; ++j) mn = fminf(mn, __uint_as_float(v[j]));
+        if (!__any_sync(0xffffffffu, mn <= thr)) return;
+        uint32_t mask = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) <= thr ? 1u : 0u) << j;
+        const uint32_t* ids = sIdx + s * kTcRows + gcol;
+        const float* prow = sRows + s * (S::kStageRows / 4) + gcol * d;
+        while (__any_sync(0xffffffffu, mask != 0)) {
+          if (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float* pp = prow + j * d;
+            float acc = 0.0f;
+            for (int jj = 0; jj < d; ++jj) {
+              float df = __fsub_rn(sQ[jj * 128 + tid], pp[jj]);
+              if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
+              else acc = __fadd_rn(acc, __fmul_rn(df, df));
+            }
+            if (acc <= kth) qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
+          }
+          if (__any_sync(0xffffffffu, cn == kQueue)) {
+            merge_queue<KB>(arr, qslot, cn, kth);
+            if (valid) thr = threshold(kth);
+          }
+        }
+      };
+
       for (int c = 0; c < T.nchunks; ++c, ++g) {
         const int s = g % kTcStages;
         const uint32_t b = g & 1u;
@@ -304,27 +356,25 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         tc_fence_after();
         const long long row0 = T.r0 + (long long)c * kTcRows;
         const int ngrp = (int)dmin_ll(kTcRows, T.r1 - row0) / 32;
-        for (int gr = 0; gr < ngrp; ++gr) {
-          uint32_t v[32];
-          tmem_ld32(tmem + lane_base + b * kTcRows + gr * 32, v);
-          float mn = __uint_as_float(v[0]);
-#pragma unroll
-          for (int j = 1; j < 32; ++j) mn = fminf(mn, __uint_as_float(v[j]));
-          if (__any_sync(0xffffffffu, mn <= thr)) {
-            const uint32_t* ids = sIdx + s * kTcRows + gr * 32;
-#pragma unroll 1
-            for (int j = 0; j < 32; ++j) {
-              if (__uint_as_float(v[j]) <= thr) {
-                const long long row = row0 + gr * 32 + j;
-                const float dist = exact_dist<FMA>(qp, A.rows + row * d, d);
-                if (dist <= kth) qslot[(cn++) * kNT] = pack_key(dist, ids[j]);
-              }
-              if (__any_sync(0xffffffffu, cn == kQueue)) {
-                merge_queue<KB>(arr, qslot, cn, kth);
-                if (valid) thr = threshold(kth);
-              }
-            }
-          }
+        const uint32_t tbase = tmem + lane_base + b * kTcRows;
+        // two-deep TMEM load pipeline over the (up to four) 32-column groups
+        uint32_t va[32], vb[32];
+        tmem_ld32(tbase, va);
+        if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
+        process(va, 0, s, row0);
+        if (ngrp > 1) {
+          tmem_wait_ld();
+          if (ngrp > 2) tmem_ld32_async(tbase + 64, va);
+          process(vb, 32, s, row0);
+        }
+        if (ngrp > 2) {
+          tmem_wait_ld();
+          if (ngrp > 3) tmem_ld32_async(tbase + 96, vb);
+          process(va, 64, s, row0);
+        }
+        if (ngrp > 3) {
+          tmem_wait_ld();
+          process(vb, 96, s, row0);
         }
         tc_fence_before();
         __syncwarp();

@@ -12,6 +12,8 @@ cudaError_t launch_tc_one(int grid, cudaStream_t s, const TcArgs& a, int* occ) {
   constexpr int smem = TcSmem<KT>::kBytes > 78 * 1024 ? TcSmem<KT>::kBytes : 78 * 1024;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
   if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kTcThreads, smem);
   fn<<<grid, kTcThreads, smem, s>>>(a);
   return cudaGetLastError();

@@ -48,8 +48,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--mode", default="fma", choices=["fma", "exact"])
-    ap.add_argument("--height", type=int, default=11, help="tree height (results do not depend on it; 11 is fastest at n=2M)")
+    ap.add_argument("--mode", default="exact", choices=["fma", "exact"],
+                    help="exact: bit-identical to the reference (default); fma: fused multiply-add distances")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "tc"],
+                    help="leaf scan: tensor-core filter (auto/tc) or CUDA-core direct scan")
+    ap.add_argument("--height", type=int, default=9, help="tree height (results do not depend on it)")
     ap.add_argument("--m", type=int, default=M_QUERIES)
     ap.add_argument("--n", type=int, default=N_REFS)
     ap.add_argument("--no-e2e", action="store_true")
@@ -223,7 +226,8 @@ def main() -> None:
         torch.cuda.synchronize()
         barrier()
         w0 = time.perf_counter()
-        st = gpu.search_device(q_dev.data_ptr(), m, K, keys_dev.data_ptr(), exact=exact, timing=True)
+        st = gpu.search_device(q_dev.data_ptr(), m, K, keys_dev.data_ptr(), exact=exact, timing=True,
+                               kernel=a.kernel)
         torch.cuda.synchronize()
         w1 = time.perf_counter()
         barrier()
@@ -258,7 +262,7 @@ def main() -> None:
             torch.cuda.synchronize()
             barrier()
             w0 = time.perf_counter()
-            res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=K), device=gpu, exact=exact)
+            res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=K), device=gpu, exact=exact, kernel=a.kernel)
             w1 = time.perf_counter()
             barrier()
             if i > 0:  # first call is warm-up
@@ -289,6 +293,21 @@ def main() -> None:
     flops = 3.0 * DIM * pairs
     achieved = flops / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
     nominal = info["sm_count"] * 128 * 2 * 1965e6 / 1e12
+    tc_used = a.kernel in ("auto", "tc") and DIM <= 31
+    kernel_name = "leafscan_tc_kernel" if tc_used else "leafscan_kernel"
+    roofline_tensor = None
+    if tc_used and scan_ms > 0:
+        # tensor work actually issued: M=128 x N x K=16 TF32 MMAs over every (query slot, padded
+        # point) of a tile = 2 * 16 FLOP per pair (upper-bounded by padding); peak = TF32 dense
+        # = half the measured bf16 GEMM rate (MEASURED_PEAKS.json)
+        peaks = json.load(open(ROOT / "MEASURED_PEAKS.json")) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        tf32_peak = bf16 / 2
+        tc_ach = 2.0 * 16 * pairs / (scan_ms / 1e3) / 1e12
+        roofline_tensor = {"bound": "tensor", "achieved": tc_ach, "peak": tf32_peak, "unit": "TFLOP/s",
+                           "frac": tc_ach / tf32_peak, "kernel": kernel_name,
+                           "peak_source": "TF32 dense = measured bf16 / 2 (MEASURED_PEAKS.json)"
+                           if peaks else "fallback 1.59 PF bf16 / 2"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -312,7 +331,7 @@ def main() -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference gen_mixture recipe, seed 1; 8 gaussians, spread 0.05)",
             "config": {"workload": f"cfg2: mixture n={a.n} refs, m={m} queries per GPU, d={DIM}, k={K}, "
-                                   f"in-memory", "height": h, "mode": a.mode,
+                                   f"in-memory", "height": h, "mode": a.mode, "kernel": a.kernel,
                        "parallelism": f"query-sharded x{world} (tree replicated, no collective)",
                        "l2": "256 MiB write between steps; per-step inputs (1.2 GB) > L2",
                        "rounds": rounds, "pairs_per_query": pairs / (a.steps * m),
@@ -321,11 +340,12 @@ def main() -> None:
             "gpu_launches": launches,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_measured, "unit": "TFLOP/s",
                          "frac": (achieved / peak_measured) if achieved else None, "traffic": None,
-                         "kernel": "leafscan_kernel", "peak_source": "measured FFMA probe (bkt_fp32_peak); "
+                         "kernel": kernel_name, "peak_source": "measured FFMA probe (bkt_fp32_peak); "
                          f"nominal {nominal:.1f} at 1965 MHz", "flops_per_pair": 3 * DIM,
                          "leafscan_ms_per_step": scan_ms / a.steps,
                          "leafscan_share": scan_ms / dev_ms if dev_ms else None,
                          "leafscan_launches": scan_launches},
+            "roofline_tensor": roofline_tensor,
             "cpu_baseline": cpu,
             "clocks": clk,
         }

@@ -116,6 +116,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   } while (!ok);
 }
 
+// Spinning variant (no suspend): lowest wake-up latency for warps on the
+// critical path of a short producer/consumer loop.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
+  uint32_t a = smem_addr(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
 // ----------------------------------------------------------------------------
 // warp-aggregated atomics
 // ----------------------------------------------------------------------------

@@ -639,6 +639,29 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.centroid = ctx->tc_centroid;
     t.d = ctx->d;
     t.qstride = ctx->D;
+    t.spin = 1;
+    if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e) != 0;
+    if (std::getenv("BKT_TC_DEBUG") && R.leafscan_launches == 5) {
+      // per-chunk timestamps of CTA 0 in the 6th leafscan launch (a steady-state round)
+      static long long* dbg = nullptr;
+      const int cap = 4096;
+      if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 8 * cap);
+      cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * cap, ctx->stream);
+      t.dbg = dbg;
+      t.dbg_cap = cap;
+      CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr));
+      std::vector<long long> h(8 * cap);
+      CU(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * 8 * cap, cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      long long base = h[0];
+      for (int g = 0; g < cap && h[8 * g + 5]; ++g)
+        std::fprintf(stderr, "chunk %d tile %lld prod_wait %lld prod_issue %lld mma_ready %lld epi_start %lld epi_ready %lld epi_done %lld\n",
+                     g, h[8 * g + 6], h[8 * g] - base, h[8 * g + 1] - base, h[8 * g + 2] - base, h[8 * g + 3] - base,
+                     h[8 * g + 4] - base, h[8 * g + 5] - base);
+      R.launches++;
+      R.leafscan_launches++;
+      return BKT_OK;
+    }
     CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr));
   } else {
     CU(launch_leafscan(ctx->D, R.kb, R.fma, R.grid_scan, ctx->stream, a, nullptr));
@@ -807,10 +830,13 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   if (o.kernel == 2 && !R.tc) return set_err(ctx, BKT_EINVAL, "tensor-core kernel requested but unavailable (needs a resident tree and d <= 31)");
   int rc = BKT_OK;
   if (R.tc) {
+    // two CTAs per SM (2 x 256 TMEM columns); the attributes are set by the query
     int occ = 0;
     TcArgs dummy{};
     CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, 0, nullptr, dummy, &occ));
-    R.grid_scan = std::max(1, std::min(occ, 2)) * ctx->sm_count;
+    int per_sm = 2;
+    if (const char* e = std::getenv("BKT_TC_CTAS")) per_sm = std::max(1, std::min(2, std::atoi(e)));
+    R.grid_scan = per_sm * ctx->sm_count;
   } else {
     rc = leafscan_grid(ctx, ctx->D, R.kb, R.fma, &R.grid_scan);
     if (rc != BKT_OK) return rc;

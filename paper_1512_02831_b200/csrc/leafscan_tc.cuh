@@ -45,6 +45,9 @@ struct TcArgs {
   const float* centroid;       // nl x KT
   int d;                       // real dimensionality
   int qstride;                 // row stride of the query block (kernel D of the direct path)
+  int spin;                    // 1: MMA/epilogue warps spin on mbarriers instead of suspending
+  long long* dbg;              // diagnostics (BKT_TC_DEBUG): per-chunk timestamps of CTA 0
+  int dbg_cap;
 };
 
 template <int KT>
@@ -209,7 +212,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         for (int c = 0; c < T.nchunks; ++c, ++g) {
           const int s = g % kTcStages;
           const uint32_t use = g / kTcStages;
+          const long long tp0 = clock64();
           if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
+          if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) {
+            A.dbg[8 * g + 0] = tp0;
+            A.dbg[8 * g + 1] = clock64();
+          }
           const long long row = T.r0 + (long long)c * kTcRows;
           const int nr = (int)dmin_ll(kTcRows, T.r1 - row);
           mbar_arrive_expect_tx(&full[s], nr * (KT * 4 + 4 + A.d * 4));
@@ -227,14 +235,20 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x, ++tt) {
         const TcTile T = tc_tile_info(A, t);
         const uint32_t ab = tt & 1u;
-        mbar_wait(&afull[ab], (tt >> 1) & 1u);
+        if (A.spin) mbar_wait_spin(&afull[ab], (tt >> 1) & 1u); else mbar_wait(&afull[ab], (tt >> 1) & 1u);
         tc_fence_after();
         for (int c = 0; c < T.nchunks; ++c, ++g) {
           const int s = g % kTcStages;
-          mbar_wait(&full[s], (g / kTcStages) & 1u);
           const uint32_t b = g & 1u;
-          if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1u);
+          if (A.spin) {
+            mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
+            if (g >= 2) mbar_wait_spin(&tempty[b], ((g >> 1) - 1) & 1u);
+          } else {
+            mbar_wait(&full[s], (g / kTcStages) & 1u);
+            if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1u);
+          }
           tc_fence_after();
+          if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * g + 2] = clock64();
           const int nr = (int)dmin_ll(kTcRows, T.r1 - (T.r0 + (long long)c * kTcRows));
           const uint32_t idesc = idesc_tf32(nr);
 #pragma unroll
@@ -319,9 +333,15 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
 
       // filter one 32-column group of TMEM values, then re-evaluate survivors
       auto process = [&](const uint32_t (&v)[32], int gcol, int s, long long row0) {
-        float mn = __uint_as_float(v[0]);
+        // depth-4 tree of 3-input minima (FMNMX3) instead of a 31-long dependent chain
+        float m1[11];
 #pragma unroll
-        for (int j = 1; j < 32; ++j) mn = fminf(mn, __uint_as_float(v[j]));
+        for (int i = 0; i < 10; ++i)
+          m1[i] = fminf(fminf(__uint_as_float(v[3 * i]), __uint_as_float(v[3 * i + 1])), __uint_as_float(v[3 * i + 2]));
+        m1[10] = fminf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+        const float m2a = fminf(fminf(m1[0], m1[1]), m1[2]), m2b = fminf(fminf(m1[3], m1[4]), m1[5]);
+        const float m2c = fminf(fminf(m1[6], m1[7]), m1[8]), m2d = fminf(m1[9], m1[10]);
+        const float mn = fminf(fminf(m2a, m2b), fminf(m2c, m2d));
         if (!__any_sync(0xffffffffu, mn <= thr)) return;
         uint32_t mask = 0;
 #pragma unroll
@@ -351,16 +371,24 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       for (int c = 0; c < T.nchunks; ++c, ++g) {
         const int s = g % kTcStages;
         const uint32_t b = g & 1u;
-        mbar_wait(&tfull[b], (g >> 1) & 1u);
-        mbar_wait(&full[s], (g / kTcStages) & 1u);
+        const long long te0 = clock64();
+        if (A.spin) {
+          mbar_wait_spin(&tfull[b], (g >> 1) & 1u);
+          mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
+        } else {
+          mbar_wait(&tfull[b], (g >> 1) & 1u);
+          mbar_wait(&full[s], (g / kTcStages) & 1u);
+        }
         tc_fence_after();
+        const long long te1 = clock64();
         const long long row0 = T.r0 + (long long)c * kTcRows;
         const int ngrp = (int)dmin_ll(kTcRows, T.r1 - row0) / 32;
         const uint32_t tbase = tmem + lane_base + b * kTcRows;
         // two-deep TMEM load pipeline over the (up to four) 32-column groups
         uint32_t va[32], vb[32];
-        tmem_ld32(tbase, va);
+        tmem_ld32_async(tbase, va);
         if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
+        tmem_wait_ld();
         process(va, 0, s, row0);
         if (ngrp > 1) {
           tmem_wait_ld();
@@ -381,6 +409,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         if (lane == 0) {
           mbar_arrive(&tempty[b]);
           mbar_arrive(&empty[s]);
+        }
+        if (A.dbg && blockIdx.x == 0 && tid == 0 && (int)g < A.dbg_cap) {
+          A.dbg[8 * g + 3] = te0;
+          A.dbg[8 * g + 4] = te1;
+          A.dbg[8 * g + 5] = clock64();
+          A.dbg[8 * g + 6] = tt;
         }
       }
       if (__any_sync(0xffffffffu, cn > 0)) merge_queue<KB>(arr, qslot, cn, kth);

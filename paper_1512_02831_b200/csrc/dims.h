@@ -10,7 +10,7 @@
   X(20) X(24) X(27) X(28) X(32)
 
 // top-k register buckets: k is served by the smallest KB >= k
-#define BKT_KB_LIST(X) X(1) X(2) X(4) X(8) X(16) X(32) X(64)
+#define BKT_KB_LIST(X) X(1) X(2) X(4) X(8) X(10) X(16) X(32) X(64)
 
 namespace bkt {
 constexpr int kMaxKernelDim = 32;

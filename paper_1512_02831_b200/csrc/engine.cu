@@ -91,6 +91,7 @@ struct bkt_ctx {
   float* tc_rowsxyz = nullptr;
   long long* tc_row_base = nullptr;
   float* tc_centroid = nullptr;
+  float* tc_pnmax = nullptr;
 
   // ---- per-batch work buffers
   long long cap_m = 0;
@@ -107,6 +108,8 @@ struct bkt_ctx {
   int* cursor = nullptr;
   int* leaf_off = nullptr;
   int* tile_off = nullptr;
+  int4* tiles = nullptr;    // per-tile records (capacity tiles_cap)
+  long long tiles_cap = 0;
   RoundCtl* ctl = nullptr;
   unsigned long long* pairs = nullptr;
   unsigned long long* seq_pos = nullptr;
@@ -199,7 +202,7 @@ int leafscan_grid(bkt_ctx* ctx, int D, int kb, bool fma, int* grid) {
 }
 
 void free_tree(bkt_ctx* c) {
-  dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid);
+  dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid); dfree(c->tc_pnmax);
   c->has_tc = false;
   dfree(c->split); dfree(c->quad_base); dfree(c->leaf_size); dfree(c->pts); dfree(c->pidx);
   hfree(c->h_pts); hfree(c->h_pidx);
@@ -211,6 +214,8 @@ void free_tree(bkt_ctx* c) {
 }
 
 void free_work(bkt_ctx* c) {
+  dfree(c->tiles);
+  c->tiles_cap = 0;
   dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
   dfree(c->work[0]); dfree(c->work[1]);
   c->cap_m = 0; c->cap_k = 0;
@@ -248,6 +253,8 @@ int ensure_work(bkt_ctx* ctx, long long m, int k) {
   CU(cudaMalloc(&ctx->visits, sizeof(uint32_t) * M));
   CU(cudaMalloc(&ctx->work[0], sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[1], sizeof(int) * M));
+  ctx->tiles_cap = M / kNT + (1ll << ctx->h) + 1;
+  CU(cudaMalloc(&ctx->tiles, sizeof(int4) * ctx->tiles_cap));
   ctx->cap_m = M;
   ctx->cap_k = k;
   return BKT_OK;
@@ -319,7 +326,8 @@ inline float tf32_rna_host(float x) {
 // tf32((1 - C) |p'|^2) in column d, zeros after; padding rows carry +inf in
 // column d so they never pass the filter.
 void build_tc_layout(const float* leaf_points, const int64_t* orig, const int64_t* starts, int nl, int d, int KT,
-                     const std::vector<long long>& rb, float* B, uint32_t* ridx, float* rows, float* centroid) {
+                     const std::vector<long long>& rb, float* B, uint32_t* ridx, float* rows, float* centroid,
+                     float* pnmax) {
   auto work = [&](int l0, int l1) {
     std::vector<double> acc(d);
     for (int l = l0; l < l1; ++l) {
@@ -329,6 +337,7 @@ void build_tc_layout(const float* leaf_points, const int64_t* orig, const int64_
         for (int j = 0; j < d; ++j) acc[j] += leaf_points[r * d + j];
       float* cen = centroid + (long long)l * KT;
       for (int j = 0; j < KT; ++j) cen[j] = j < d ? (float)(acc[j] / (double)(e - s)) : 0.0f;
+      float pmax = 0.0f;
       for (long long R = rb[l]; R < rb[l + 1]; ++R) {
         long long r = s + (R - rb[l]);
         bool real = r < e;
@@ -344,9 +353,11 @@ void build_tc_layout(const float* leaf_points, const int64_t* orig, const int64_
           bg[(k / 4) * 32 + (k % 4)] = v;
         }
         bg[(d / 4) * 32 + (d % 4)] = real ? tf32_rna_host((1.0f - kTcMargin) * pn) : __builtin_inff();
+        if (real) pmax = std::max(pmax, pn);
         ridx[R] = real ? (uint32_t)orig[r] : kIndexSentinel;
         for (int j = 0; j < d; ++j) rows[R * d + j] = real ? leaf_points[r * d + j] : __builtin_inff();
       }
+      pnmax[l] = pmax * 1.0001f;
     }
   };
   int nt = std::max(1, std::min<int>(16, (int)std::thread::hardware_concurrency()));
@@ -506,10 +517,12 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       std::vector<long long> rb(nl + 1, 0);
       for (int l = 0; l < nl; ++l) rb[l + 1] = rb[l] + ((long long)ctx->h_leaf_size[l] + 31) / 32 * 32;
       const long long R = rb[nl];
-      std::vector<float> hB((size_t)R * KT), hrows((size_t)R * d), hcen((size_t)nl * KT);
+      std::vector<float> hB((size_t)R * KT), hrows((size_t)R * d), hcen((size_t)nl * KT), hpn((size_t)nl);
       std::vector<uint32_t> hidx((size_t)R);
       build_tc_layout(leaf_points, original_index, leaf_starts, nl, d, KT, rb, hB.data(), hidx.data(), hrows.data(),
-                      hcen.data());
+                      hcen.data(), hpn.data());
+      CU(cudaMalloc(&ctx->tc_pnmax, sizeof(float) * nl));
+      CU(cudaMemcpy(ctx->tc_pnmax, hpn.data(), sizeof(float) * nl, cudaMemcpyHostToDevice));
       CU(cudaMalloc(&ctx->tc_B, sizeof(float) * R * KT));
       CU(cudaMalloc(&ctx->tc_idx, sizeof(uint32_t) * R));
       CU(cudaMalloc(&ctx->tc_rowsxyz, sizeof(float) * R * d));
@@ -577,6 +590,7 @@ struct SearchRun {
   int kb = 0;
   bool fma = false;
   bool tc = false;
+  bool unfused = false;
   int grid_scan = 0;
   int grid_small = 0;
   bool timing = false;
@@ -603,6 +617,7 @@ ScanArgs make_scan_args(bkt_ctx* ctx, SearchRun& R, int cur) {
   a.num_tiles = &ctx->ctl->num_tiles;
   a.tile_lo = 0;
   a.tile_hi = -1;
+  a.tiles = ctx->tiles;
   a.counts = ctx->counts;
   a.pts = ctx->pts;
   a.pidx = ctx->pidx;
@@ -637,6 +652,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.rows = ctx->tc_rowsxyz;
     t.row_base = ctx->tc_row_base;
     t.centroid = ctx->tc_centroid;
+    t.pnmax = ctx->tc_pnmax;
     t.d = ctx->d;
     t.qstride = ctx->D;
     t.spin = 1;
@@ -759,7 +775,8 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   const bool ooc = ctx->residency == 1;
   for (;;) {
     plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl,
-                                                     ctx->nl, kNT, ctx->hist, kHistCap);
+                                                     ctx->nl, kNT, ctx->hist, kHistCap, ctx->tiles,
+                                                     (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
     CU(cudaGetLastError());
     R.launches++;
     const int slot = (int)(round % kRing);
@@ -779,8 +796,19 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       if (rc != BKT_OK) return rc;
     } else {
       ScanArgs a = make_scan_args(ctx, R, cur);
+      const bool unfused = R.tc && R.unfused;
+      if (unfused) a.fused = 0;
       int rc = launch_scan(ctx, R, a);
       if (rc != BKT_OK) return rc;
+      if (unfused) {
+        // FindLeaf as its own high-occupancy pass: its dependent top-tree loads
+        // then overlap across many warps instead of stalling the scan's epilogue
+        findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
+            ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys,
+            ctx->state, ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+        CU(cudaGetLastError());
+        R.launches++;
+      }
     }
     cur ^= 1;
     ++round;
@@ -827,6 +855,8 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   R.seq = o.seq_log != nullptr && o.seq_cap > 0;
   R.seq_cap = R.seq ? o.seq_cap : 0;
   R.tc = ctx->has_tc && ctx->residency == 0 && o.kernel != 1;
+  R.unfused = false;
+  if (const char* e = std::getenv("BKT_TC_UNFUSED")) R.unfused = std::atoi(e) != 0;
   if (o.kernel == 2 && !R.tc) return set_err(ctx, BKT_EINVAL, "tensor-core kernel requested but unavailable (needs a resident tree and d <= 31)");
   int rc = BKT_OK;
   if (R.tc) {

@@ -42,6 +42,7 @@ struct ScanArgs {
   const int* tile_off;   // nl + 1: first tile of each leaf
   const int* num_tiles;  // device scalar: tiles this round
   int tile_lo, tile_hi;  // chunk mode: tile sub-range; tile_hi < 0 = [0, *num_tiles)
+  const int4* tiles;     // per-tile {leaf, qbeg, qcnt} written by plan_kernel
   int* counts;           // nl: next-round histogram (fused epilogue)
   // leaf structure, quad-interleaved: quad g, dim j, point t at pts[(g - quad_origin)*4D + 4j + t]
   const float* pts;
@@ -99,21 +100,14 @@ struct TileInfo {
 };
 
 __device__ __forceinline__ TileInfo tile_info(const ScanArgs& a, int t) {
-  const int nl = 1 << a.top.h;
-  // last leaf with tile_off[leaf] <= t (empty leaves repeat the offset)
-  int lo = 0, hi = nl - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (__ldg(a.tile_off + mid) <= t) lo = mid; else hi = mid - 1;
-  }
+  const int4 rec = __ldg(a.tiles + t);
   TileInfo T;
-  T.leaf = lo;
-  const int j = t - __ldg(a.tile_off + lo);
-  T.qbeg = __ldg(a.leaf_off + lo) + j * kNT;
-  T.qcnt = min(kNT, __ldg(a.leaf_off + lo + 1) - T.qbeg);
-  T.lq0 = __ldg(a.quad_base + lo);
+  T.leaf = rec.x;
+  T.qbeg = rec.y;
+  T.qcnt = rec.z;
+  T.lq0 = __ldg(a.quad_base + rec.x);
   T.g0 = max(T.lq0, a.clip_lo);
-  T.g1 = min(__ldg(a.quad_base + lo + 1), a.clip_hi);
+  T.g1 = min(__ldg(a.quad_base + rec.x + 1), a.clip_hi);
   const int nq = (int)max(0ll, T.g1 - T.g0);
   T.nchunks = (nq + kChunkQuads - 1) / kChunkQuads;
   return T;

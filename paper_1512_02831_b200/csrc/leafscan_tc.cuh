@@ -30,10 +30,11 @@
 
 namespace bkt {
 
-constexpr int kTcRows = 128;                  // points per chunk (MMA N)
+constexpr int kTcRows = 64;                   // points per chunk (MMA N)
+constexpr int kTcBufs = 4;                    // TMEM accumulators (MMA runs kTcBufs-1 chunks ahead)
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
-constexpr int kTcTmemCols = 2 * kTcRows;      // two accumulators
+constexpr int kTcTmemCols = kTcBufs * kTcRows;  // 256 columns: two CTAs per SM
 constexpr float kTcMargin = 1.0f / 128.0f;    // C
 
 struct TcArgs {
@@ -43,6 +44,7 @@ struct TcArgs {
   const float* rows;           // padded row-major original coordinates, stride d (padding rows +inf)
   const long long* row_base;   // nl + 1, first padded row of each leaf (multiples of 32)
   const float* centroid;       // nl x KT
+  const float* pnmax;          // nl: max over the leaf of |p - c|^2 (upper-bound helper)
   int d;                       // real dimensionality
   int qstride;                 // row stride of the query block (kernel D of the direct path)
   int spin;                    // 1: MMA/epilogue warps spin on mbarriers instead of suspending
@@ -52,7 +54,7 @@ struct TcArgs {
 
 template <int KT>
 struct TcSmem {
-  static constexpr int kStages = KT <= 16 ? 4 : 2;
+  static constexpr int kStages = KT <= 16 ? 8 : 4;
   static constexpr int kStageB = kTcRows * KT * 4;
   static constexpr int kStageIdx = kTcRows * 4;
   static constexpr int kStageRows = kTcRows * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
@@ -61,9 +63,9 @@ struct TcSmem {
   static constexpr int kOffRows = kOffIdx + kStages * kStageIdx;
   static constexpr int kOffA = kOffRows + kStages * kStageRows;
   static constexpr int kOffQs = kOffA + 2 * kA;
-  static constexpr int kOffQ = kOffQs + 128 * KT * 4;
+  static constexpr int kOffQ = kOffQs + 2 * 128 * KT * 4;
   static constexpr int kOffBar = kOffQ + kQueue * 128 * 8;
-  static constexpr int kNumBars = 2 * kStages + 8;
+  static constexpr int kNumBars = 2 * kStages + 2 * kTcBufs + 4;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
 };
 
@@ -123,20 +125,13 @@ struct TcTile {
 };
 
 __device__ __forceinline__ TcTile tc_tile_info(const TcArgs& A, int t) {
-  const ScanArgs& a = A.s;
-  const int nl = 1 << a.top.h;
-  int lo = 0, hi = nl - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (__ldg(a.tile_off + mid) <= t) lo = mid; else hi = mid - 1;
-  }
+  const int4 rec = __ldg(A.s.tiles + t);
   TcTile T;
-  T.leaf = lo;
-  const int j = t - __ldg(a.tile_off + lo);
-  T.qbeg = __ldg(a.leaf_off + lo) + j * kNT;
-  T.qcnt = min(kNT, __ldg(a.leaf_off + lo + 1) - T.qbeg);
-  T.r0 = __ldg(A.row_base + lo);
-  T.r1 = __ldg(A.row_base + lo + 1);
+  T.leaf = rec.x;
+  T.qbeg = rec.y;
+  T.qcnt = rec.z;
+  T.r0 = __ldg(A.row_base + rec.x);
+  T.r1 = __ldg(A.row_base + rec.x + 1);
   T.nchunks = (int)((T.r1 - T.r0 + kTcRows - 1) / kTcRows);
   return T;
 }
@@ -171,9 +166,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* full = bars;                      // [kTcStages] TMA -> MMA/epilogue
   uint64_t* empty = bars + kTcStages;         // [kTcStages] epilogue -> TMA
-  uint64_t* tfull = bars + 2 * kTcStages;     // [2] MMA -> epilogue
-  uint64_t* tempty = tfull + 2;               // [2] epilogue -> MMA
-  uint64_t* afull = tempty + 2;               // [2] epilogue (A written) -> MMA
+  uint64_t* tfull = bars + 2 * kTcStages;     // [kTcBufs] MMA -> epilogue
+  uint64_t* tempty = tfull + kTcBufs;         // [kTcBufs] epilogue -> MMA
+  uint64_t* afull = tempty + kTcBufs;         // [2] epilogue (A written) -> MMA
   uint64_t* aempty = afull + 2;               // [2] MMA (tile done) -> epilogue
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + S::kNumBars);
 
@@ -184,9 +179,11 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kTcEpiWarps);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kTcBufs; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kTcEpiWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&afull[b], kTcEpiWarps);
       mbar_init(&aempty[b], 1);
     }
@@ -239,13 +236,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         tc_fence_after();
         for (int c = 0; c < T.nchunks; ++c, ++g) {
           const int s = g % kTcStages;
-          const uint32_t b = g & 1u;
+          const uint32_t b = g % kTcBufs, use = g / kTcBufs;
           if (A.spin) {
             mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
-            if (g >= 2) mbar_wait_spin(&tempty[b], ((g >> 1) - 1) & 1u);
+            if (use > 0) mbar_wait_spin(&tempty[b], (use - 1) & 1u);
           } else {
             mbar_wait(&full[s], (g / kTcStages) & 1u);
-            if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1u);
+            if (use > 0) mbar_wait(&tempty[b], (use - 1) & 1u);
           }
           tc_fence_after();
           if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * g + 2] = clock64();
@@ -276,18 +273,60 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
     uint64_t* qslot = s_queue + tid;
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
     const int d = A.d;
+    // Stage tile T's A rows and query coordinates into buffer `buf` (the
+    // tile's parity); called one tile ahead so the MMA warp can start the
+    // next tile while this warp finishes the current one.
+    auto stage = [&](const TcTile& T, uint32_t buf, uint32_t tidx, int& qi_out, float& qn_out) {
+      const bool v_ok = tid < T.qcnt;
+      qi_out = v_ok ? __ldg(a.work + T.qbeg + tid) : 0;
+      const float* qsrc = a.q + (long long)qi_out * A.qstride;
+      if (tidx >= 2) mbar_wait(&aempty[buf], ((tidx >> 1) - 1) & 1u);
+      const float* cen = A.centroid + (long long)T.leaf * KT;
+      float qn = 0.0f;
+      float* arow = sA + buf * (S::kA / 4);
+      float* sq = sQ + buf * (128 * KT);
+      // canonical layout: row r -> group r/8 (KT*32 B), chunk k/4 (128 B), row r%8 (16 B)
+      float* base = arow + (tid >> 3) * (KT * 8) + (tid & 7) * 4;
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        float v = 0.0f;
+        if (j < d) {
+          const float qv = v_ok ? __ldg(qsrc + j) : 0.0f;
+          sq[j * 128 + tid] = qv;
+          float qc = v_ok ? __fsub_rn(qv, __ldg(cen + j)) : 0.0f;
+          qn = __fmaf_rn(qc, qc, qn);
+          v = __uint_as_float(tf32_rna(qc));
+        } else if (j == d) {
+          v = 1.0f;
+        }
+        base[(j >> 2) * 32 + (j & 3)] = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[buf]);
+      qn_out = qn;
+    };
+
     uint32_t g = 0, tt = 0;
-    for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x, ++tt) {
-      const TcTile T = tc_tile_info(A, t);
+    int t = a.tile_lo + blockIdx.x;
+    TcTile Tn{};
+    int qi_n = 0;
+    float qn_n = 0.0f;
+    if (t < tiles_end) {
+      Tn = tc_tile_info(A, t);
+      stage(Tn, 0, 0, qi_n, qn_n);
+    }
+    for (; t < tiles_end; t += gridDim.x, ++tt) {
+      const TcTile T = Tn;
+      const int qi = qi_n;
+      const float qn = qn_n;
       const uint32_t ab = tt & 1u;
       const bool valid = tid < T.qcnt;
-      int qi = 0;
+      const float* sQc = sQ + ab * (128 * KT);  // this tile's query coordinates [j][128]
       uint64_t arr[KB];
       float kth = -__int_as_float(0x7f800000);  // invalid rows never take candidates
-      const float* qp = a.q;
+      const float* qp = a.q + (long long)qi * A.qstride;
       if (valid) {
-        qi = __ldg(a.work + T.qbeg + tid);
-        qp = a.q + (long long)qi * A.qstride;
         const uint64_t* kp = a.keys + (long long)qi * a.k;
 #pragma unroll
         for (int j = 0; j < KB; ++j) arr[j] = (j < a.k) ? kp[a.k - 1 - j] : 0ull;
@@ -296,40 +335,28 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
 #pragma unroll
         for (int j = 0; j < KB; ++j) arr[j] = 0;
       }
-      // A row: tf32(q - c) in dims < d, 1.0 in column d, zeros after
-      if (tt >= 2) mbar_wait(&aempty[ab], ((tt >> 1) - 1) & 1u);
-      const float* cen = A.centroid + (long long)T.leaf * KT;
-      float qn = 0.0f;
-      {
-        float* arow = sA + ab * (S::kA / 4);
-        // canonical layout: row r -> group r/8 (KT*32 B), chunk k/4 (128 B), row r%8 (16 B)
-        float* base = arow + (tid >> 3) * (KT * 8) + (tid & 7) * 4;
-#pragma unroll
-        for (int j = 0; j < KT; ++j) {
-          float v = 0.0f;
-          if (j < d) {
-            const float qv = valid ? __ldg(qp + j) : 0.0f;
-            sQ[j * 128 + tid] = qv;
-            float qc = valid ? __fsub_rn(qv, __ldg(cen + j)) : 0.0f;
-            qn = __fmaf_rn(qc, qc, qn);
-            v = __uint_as_float(tf32_rna(qc));
-          } else if (j == d) {
-            v = 1.0f;
-          }
-          base[(j >> 2) * 32 + (j & 3)] = v;
+      bool staged_next = false;
+      auto stage_next = [&]() {
+        if (staged_next) return;
+        staged_next = true;
+        const int tn = t + (int)gridDim.x;
+        if (tn < tiles_end) {
+          Tn = tc_tile_info(A, tn);
+          stage(Tn, ab ^ 1u, tt + 1, qi_n, qn_n);
         }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[ab]);
+      };
       const float qnc = (1.0f - kTcMargin) * qn;
       auto threshold = [&](float kk) {
         // kth - (1 - C) qn, rounded up by a hair so the fp32 subtraction cannot cut a candidate
         float t0 = __fsub_ru(kk, qnc);
         return t0 + 1e-6f * (fabsf(kk) + qnc);
       };
-      float thr = valid ? threshold(kth) : kth;
+      // kflt: the radius the filter and the queue test against = min(kth, kub)
+      // where kub is a proven upper bound of the k-th distance (below)
+      float kflt = kth;
+      float thr = valid ? threshold(kflt) : kth;
       int cn = 0;
+      const float leaf_pnmax = __ldg(A.pnmax + T.leaf);
 
       // filter one 32-column group of TMEM values, then re-evaluate survivors
       auto process = [&](const uint32_t (&v)[32], int gcol, int s, long long row0) {
@@ -355,28 +382,29 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
             const float* pp = prow + j * d;
             float acc = 0.0f;
             for (int jj = 0; jj < d; ++jj) {
-              float df = __fsub_rn(sQ[jj * 128 + tid], pp[jj]);
+              float df = __fsub_rn(sQc[jj * 128 + tid], pp[jj]);
               if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
               else acc = __fadd_rn(acc, __fmul_rn(df, df));
             }
-            if (acc <= kth) qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
+            if (acc <= kflt) qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
           }
           if (__any_sync(0xffffffffu, cn == kQueue)) {
             merge_queue<KB>(arr, qslot, cn, kth);
-            if (valid) thr = threshold(kth);
+            kflt = fminf(kflt, kth);
+            if (valid) thr = threshold(kflt);
           }
         }
       };
 
       for (int c = 0; c < T.nchunks; ++c, ++g) {
         const int s = g % kTcStages;
-        const uint32_t b = g & 1u;
+        const uint32_t b = g % kTcBufs;
         const long long te0 = clock64();
         if (A.spin) {
-          mbar_wait_spin(&tfull[b], (g >> 1) & 1u);
+          mbar_wait_spin(&tfull[b], (g / kTcBufs) & 1u);
           mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
         } else {
-          mbar_wait(&tfull[b], (g >> 1) & 1u);
+          mbar_wait(&tfull[b], (g / kTcBufs) & 1u);
           mbar_wait(&full[s], (g / kTcStages) & 1u);
         }
         tc_fence_after();
@@ -384,26 +412,36 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         const long long row0 = T.r0 + (long long)c * kTcRows;
         const int ngrp = (int)dmin_ll(kTcRows, T.r1 - row0) / 32;
         const uint32_t tbase = tmem + lane_base + b * kTcRows;
-        // two-deep TMEM load pipeline over the (up to four) 32-column groups
+        // both 32-column groups of the chunk in flight, one wait
         uint32_t va[32], vb[32];
         tmem_ld32_async(tbase, va);
         if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
         tmem_wait_ld();
+        if constexpr (KB <= 32) {
+          if (c == 0 && valid && kth == __int_as_float(0x7f800000)) {
+            // No k-th neighbour yet (first leaf): bound it from this chunk's first
+            // 32 points.  With U_j = T_j + qn + 2C (qn + pnmax_leaf) >= D_ref(q, p_j)
+            // (the filter's error analysis), the KB >= k disjoint column groups
+            // j = g (mod KB) each contain a point with D_ref <= min_g U, so the
+            // k-th distance is <= max_g min_{j in g} U_j.  Filtering against it
+            // drops only points that cannot enter the top-k.
+            float gmax = -__int_as_float(0x7f800000);
+#pragma unroll
+            for (int gi = 0; gi < KB; ++gi) {
+              float gm = __uint_as_float(va[gi]);
+#pragma unroll
+              for (int j = gi + KB; j < 32; j += KB) gm = fminf(gm, __uint_as_float(va[j]));
+              gmax = fmaxf(gmax, gm);
+            }
+            const float kub = __fadd_ru(__fadd_ru(gmax, qn), 2.0f * kTcMargin * (qn + leaf_pnmax) * 1.0001f);
+            if (kub < kflt) {
+              kflt = kub;
+              thr = threshold(kflt);
+            }
+          }
+        }
         process(va, 0, s, row0);
-        if (ngrp > 1) {
-          tmem_wait_ld();
-          if (ngrp > 2) tmem_ld32_async(tbase + 64, va);
-          process(vb, 32, s, row0);
-        }
-        if (ngrp > 2) {
-          tmem_wait_ld();
-          if (ngrp > 3) tmem_ld32_async(tbase + 96, vb);
-          process(va, 64, s, row0);
-        }
-        if (ngrp > 3) {
-          tmem_wait_ld();
-          process(vb, 96, s, row0);
-        }
+        if (ngrp > 1) process(vb, 32, s, row0);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -416,7 +454,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
           A.dbg[8 * g + 5] = clock64();
           A.dbg[8 * g + 6] = tt;
         }
+        if (c == 0) stage_next();
       }
+      stage_next();
       if (__any_sync(0xffffffffu, cn > 0)) merge_queue<KB>(arr, qslot, cn, kth);
 
       if (tid == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)(__ldg(a.leaf_size + T.leaf)) * T.qcnt);

@@ -90,7 +90,7 @@ __device__ __forceinline__ void block_scan2(long long& a, long long& b, long lon
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ counts, int* __restrict__ leaf_off,
                                                             int* __restrict__ tile_off, int* __restrict__ cursor,
                                                             RoundCtl* ctl, int nl, int tile_q, int* hist,
-                                                            int hist_cap) {
+                                                            int hist_cap, int4* tiles, int tiles_cap) {
   const int per = (nl + kPlanThreads - 1) / kPlanThreads;
   const int lo = min(nl, (int)threadIdx.x * per), hi = min(nl, lo + per);
   long long sc = 0, st = 0;
@@ -106,8 +106,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
     int c = counts[l];
     leaf_off[l] = (int)ec;
     tile_off[l] = (int)et;
+    // per-tile records {leaf, first work-list slot, query count}: one load per tile
+    // in the scan kernels instead of a binary search over tile_off
+    const int nt = (c + tile_q - 1) / tile_q;
+    for (int j = 0; j < nt && et + j < tiles_cap; ++j)
+      tiles[et + j] = make_int4(l, (int)ec + j * tile_q, min(tile_q, c - j * tile_q), 0);
     ec += c;
-    et += (c + tile_q - 1) / tile_q;
+    et += nt;
     counts[l] = 0;
     cursor[l] = 0;
   }

@@ -102,6 +102,7 @@ struct bkt_ctx {
   uint32_t* state = nullptr;
   int* next = nullptr;
   uint32_t* visits = nullptr;
+  float* kthv = nullptr;    // per query k-th distance (TC kernel's lazy top-k)
   int* work[2] = {nullptr, nullptr};
   int cap_nl = 0;
   int* counts = nullptr;
@@ -216,6 +217,7 @@ void free_tree(bkt_ctx* c) {
 void free_work(bkt_ctx* c) {
   dfree(c->tiles);
   c->tiles_cap = 0;
+  dfree(c->kthv);
   dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
   dfree(c->work[0]); dfree(c->work[1]);
   c->cap_m = 0; c->cap_k = 0;
@@ -251,6 +253,7 @@ int ensure_work(bkt_ctx* ctx, long long m, int k) {
   CU(cudaMalloc(&ctx->state, sizeof(uint32_t) * M));
   CU(cudaMalloc(&ctx->next, sizeof(int) * M));
   CU(cudaMalloc(&ctx->visits, sizeof(uint32_t) * M));
+  CU(cudaMalloc(&ctx->kthv, sizeof(float) * M));
   CU(cudaMalloc(&ctx->work[0], sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[1], sizeof(int) * M));
   ctx->tiles_cap = M / kNT + (1ll << ctx->h) + 1;
@@ -653,6 +656,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.row_base = ctx->tc_row_base;
     t.centroid = ctx->tc_centroid;
     t.pnmax = ctx->tc_pnmax;
+    t.kth = ctx->kthv;
     t.d = ctx->d;
     t.qstride = ctx->D;
     t.spin = 1;
@@ -763,7 +767,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   CU(cudaMemsetAsync(ctx->cursor, 0, sizeof(int) * ctx->nl, ctx->stream));
   start_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
                                                        ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr,
-                                                       ctx->seq_pos, R.seq_cap);
+                                                       ctx->seq_pos, R.seq_cap, ctx->kthv);
   CU(cudaGetLastError());
   R.launches++;
 

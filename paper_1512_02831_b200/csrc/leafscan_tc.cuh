@@ -45,6 +45,7 @@ struct TcArgs {
   const long long* row_base;   // nl + 1, first padded row of each leaf (multiples of 32)
   const float* centroid;       // nl x KT
   const float* pnmax;          // nl: max over the leaf of |p - c|^2 (upper-bound helper)
+  float* kth;                  // per query: current k-th distance (== key_dist(keys[k-1]))
   int d;                       // real dimensionality
   int qstride;                 // row stride of the query block (kernel D of the direct path)
   int spin;                    // 1: MMA/epilogue warps spin on mbarriers instead of suspending
@@ -63,7 +64,7 @@ struct TcSmem {
   static constexpr int kOffRows = kOffIdx + kStages * kStageIdx;
   static constexpr int kOffA = kOffRows + kStages * kStageRows;
   static constexpr int kOffQs = kOffA + 2 * kA;
-  static constexpr int kOffQ = kOffQs + 2 * 128 * KT * 4;
+  static constexpr int kOffQ = kOffQs + 128 * KT * 4;
   static constexpr int kOffBar = kOffQ + kQueue * 128 * 8;
   static constexpr int kNumBars = 2 * kStages + 2 * kTcBufs + 4;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
@@ -273,78 +274,47 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
     uint64_t* qslot = s_queue + tid;
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
     const int d = A.d;
-    // Stage tile T's A rows and query coordinates into buffer `buf` (the
-    // tile's parity); called one tile ahead so the MMA warp can start the
-    // next tile while this warp finishes the current one.
-    auto stage = [&](const TcTile& T, uint32_t buf, uint32_t tidx, int& qi_out, float& qn_out) {
-      const bool v_ok = tid < T.qcnt;
-      qi_out = v_ok ? __ldg(a.work + T.qbeg + tid) : 0;
-      const float* qsrc = a.q + (long long)qi_out * A.qstride;
-      if (tidx >= 2) mbar_wait(&aempty[buf], ((tidx >> 1) - 1) & 1u);
+    uint32_t g = 0, tt = 0;
+    for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x, ++tt) {
+      const TcTile T = tc_tile_info(A, t);
+      const uint32_t ab = tt & 1u;
+      const bool valid = tid < T.qcnt;
+      const int qi = valid ? __ldg(a.work + T.qbeg + tid) : 0;
+      const float* qp = a.q + (long long)qi * A.qstride;
+      // The full top-k list is only needed when a candidate enters it; a tile
+      // starts from the query's k-th distance alone (kth array) and loads the
+      // list lazily at the first merge.
+      uint64_t arr[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) arr[j] = 0;
+      bool have_list = false;
+      float kth = valid ? __ldg(A.kth + qi) : -__int_as_float(0x7f800000);  // invalid rows never take candidates
+      // A row: tf32(q - c) in dims < d, 1.0 in column d, zeros after
+      if (tt >= 2) mbar_wait(&aempty[ab], ((tt >> 1) - 1) & 1u);
       const float* cen = A.centroid + (long long)T.leaf * KT;
       float qn = 0.0f;
-      float* arow = sA + buf * (S::kA / 4);
-      float* sq = sQ + buf * (128 * KT);
-      // canonical layout: row r -> group r/8 (KT*32 B), chunk k/4 (128 B), row r%8 (16 B)
-      float* base = arow + (tid >> 3) * (KT * 8) + (tid & 7) * 4;
+      {
+        float* arow = sA + ab * (S::kA / 4);
+        // canonical layout: row r -> group r/8 (KT*32 B), chunk k/4 (128 B), row r%8 (16 B)
+        float* base = arow + (tid >> 3) * (KT * 8) + (tid & 7) * 4;
 #pragma unroll
-      for (int j = 0; j < KT; ++j) {
-        float v = 0.0f;
-        if (j < d) {
-          const float qv = v_ok ? __ldg(qsrc + j) : 0.0f;
-          sq[j * 128 + tid] = qv;
-          float qc = v_ok ? __fsub_rn(qv, __ldg(cen + j)) : 0.0f;
-          qn = __fmaf_rn(qc, qc, qn);
-          v = __uint_as_float(tf32_rna(qc));
-        } else if (j == d) {
-          v = 1.0f;
+        for (int j = 0; j < KT; ++j) {
+          float v = 0.0f;
+          if (j < d) {
+            const float qv = valid ? __ldg(qp + j) : 0.0f;
+            sQ[j * 128 + tid] = qv;
+            float qc = valid ? __fsub_rn(qv, __ldg(cen + j)) : 0.0f;
+            qn = __fmaf_rn(qc, qc, qn);
+            v = __uint_as_float(tf32_rna(qc));
+          } else if (j == d) {
+            v = 1.0f;
+          }
+          base[(j >> 2) * 32 + (j & 3)] = v;
         }
-        base[(j >> 2) * 32 + (j & 3)] = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[buf]);
-      qn_out = qn;
-    };
-
-    uint32_t g = 0, tt = 0;
-    int t = a.tile_lo + blockIdx.x;
-    TcTile Tn{};
-    int qi_n = 0;
-    float qn_n = 0.0f;
-    if (t < tiles_end) {
-      Tn = tc_tile_info(A, t);
-      stage(Tn, 0, 0, qi_n, qn_n);
-    }
-    for (; t < tiles_end; t += gridDim.x, ++tt) {
-      const TcTile T = Tn;
-      const int qi = qi_n;
-      const float qn = qn_n;
-      const uint32_t ab = tt & 1u;
-      const bool valid = tid < T.qcnt;
-      const float* sQc = sQ + ab * (128 * KT);  // this tile's query coordinates [j][128]
-      uint64_t arr[KB];
-      float kth = -__int_as_float(0x7f800000);  // invalid rows never take candidates
-      const float* qp = a.q + (long long)qi * A.qstride;
-      if (valid) {
-        const uint64_t* kp = a.keys + (long long)qi * a.k;
-#pragma unroll
-        for (int j = 0; j < KB; ++j) arr[j] = (j < a.k) ? kp[a.k - 1 - j] : 0ull;
-        kth = key_dist(arr[0]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < KB; ++j) arr[j] = 0;
-      }
-      bool staged_next = false;
-      auto stage_next = [&]() {
-        if (staged_next) return;
-        staged_next = true;
-        const int tn = t + (int)gridDim.x;
-        if (tn < tiles_end) {
-          Tn = tc_tile_info(A, tn);
-          stage(Tn, ab ^ 1u, tt + 1, qi_n, qn_n);
-        }
-      };
+      if (lane == 0) mbar_arrive(&afull[ab]);
       const float qnc = (1.0f - kTcMargin) * qn;
       auto threshold = [&](float kk) {
         // kth - (1 - C) qn, rounded up by a hair so the fp32 subtraction cannot cut a candidate
@@ -357,6 +327,19 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       float thr = valid ? threshold(kflt) : kth;
       int cn = 0;
       const float leaf_pnmax = __ldg(A.pnmax + T.leaf);
+
+      // insert this lane's queued candidates; the list is fetched on first use
+      auto merge = [&]() {
+        if (cn > 0) {
+          if (!have_list) {
+            const uint64_t* kp = a.keys + (long long)qi * a.k;
+#pragma unroll
+            for (int j = 0; j < KB; ++j) arr[j] = (j < a.k) ? kp[a.k - 1 - j] : 0ull;
+            have_list = true;
+          }
+          merge_queue<KB>(arr, qslot, cn, kth);
+        }
+      };
 
       // filter one 32-column group of TMEM values, then re-evaluate survivors
       auto process = [&](const uint32_t (&v)[32], int gcol, int s, long long row0) {
@@ -382,14 +365,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
             const float* pp = prow + j * d;
             float acc = 0.0f;
             for (int jj = 0; jj < d; ++jj) {
-              float df = __fsub_rn(sQc[jj * 128 + tid], pp[jj]);
+              float df = __fsub_rn(sQ[jj * 128 + tid], pp[jj]);
               if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
               else acc = __fadd_rn(acc, __fmul_rn(df, df));
             }
             if (acc <= kflt) qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
           }
           if (__any_sync(0xffffffffu, cn == kQueue)) {
-            merge_queue<KB>(arr, qslot, cn, kth);
+            merge();
             kflt = fminf(kflt, kth);
             if (valid) thr = threshold(kflt);
           }
@@ -454,23 +437,24 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
           A.dbg[8 * g + 5] = clock64();
           A.dbg[8 * g + 6] = tt;
         }
-        if (c == 0) stage_next();
       }
-      stage_next();
-      if (__any_sync(0xffffffffu, cn > 0)) merge_queue<KB>(arr, qslot, cn, kth);
+      if (__any_sync(0xffffffffu, cn > 0)) merge();
 
       if (tid == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)(__ldg(a.leaf_size + T.leaf)) * T.qcnt);
 
       if (valid) {
-        uint64_t* kp = a.keys + (long long)qi * a.k;
+        if (have_list) {
+          uint64_t* kp = a.keys + (long long)qi * a.k;
 #pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (j < a.k) kp[a.k - 1 - j] = arr[j];
+          for (int j = 0; j < KB; ++j)
+            if (j < a.k) kp[a.k - 1 - j] = arr[j];
+          A.kth[qi] = kth;
+        }
         if (a.fused) {
           auto qget = [qp](int j) { return __ldg(qp + j); };
           uint32_t st = a.state[qi];
           uint32_t lf = st & 0xFFFFu, pend = st >> 16;
-          int nxt = find_next_leaf(a.top, qget, key_dist(arr[0]), lf, pend);
+          int nxt = find_next_leaf(a.top, qget, kth, lf, pend);
           a.state[qi] = (pend << 16) | lf;
           a.next[qi] = nxt;
           if (nxt >= 0) {

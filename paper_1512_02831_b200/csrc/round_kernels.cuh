@@ -32,10 +32,11 @@ constexpr int kPlanThreads = 1024;
 __global__ void start_kernel(const float* __restrict__ q, int D, long long m, int k, TopTreeView top,
                              uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next,
                              uint32_t* __restrict__ visits, int* __restrict__ counts, int* seq_log,
-                             unsigned long long* seq_pos, long long seq_cap) {
+                             unsigned long long* seq_pos, long long seq_cap, float* __restrict__ kth) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
     uint64_t* kp = keys + i * k;
     for (int t = 0; t < k; ++t) kp[t] = kEmptyKey;
+    kth[i] = __int_as_float(0x7f800000);
     const float* qp = q + i * D;
     auto qget = [qp](int j) { return __ldg(qp + j); };
     uint32_t leaf = 0, pend = 0;

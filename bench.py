@@ -194,10 +194,12 @@ def main() -> None:
     world, rank, local = dist_env()
     import torch
     import torch.distributed as dist
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # one process per GPU; on a box with fewer GPUs than ranks (smoke-testing the
+    # multi-rank flow) ranks share devices round-robin
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev_t = torch.device("cuda", local)
 
     import paper_1512_02831_b200 as bkt

@@ -1,0 +1,150 @@
+"""Measure BASELINE.json's configs beyond the headline (bench.py measures configs[1]).
+
+    python tools/configs.py cfg1                 # uniform n=m=2^16, d=10, k=10, h=8 (+ reference digest)
+    python tools/configs.py cfg3 [--m 2e8]       # n=2M refs, query stream of m queries in 10M chunks
+    python tools/configs.py cfg4 [--m 10e6]      # d = 5 / 15 / 27 mixture, n=2M
+    python tools/configs.py cfg5 [--m 1e6]       # n=8M host-resident leaf streaming, k in {1,10,50}, h in {8,11,14}
+
+One JSON line per measurement on stdout.  Every run checks a sample of rows
+against the CPU oracle (exact mode: bit-identical keys).
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_1512_02831_b200 as bkt  # noqa: E402
+from paper_1512_02831_b200.datasets import gen_mixture, gen_query_chunk  # noqa: E402
+
+
+def oracle_check(tree, queries, keys, k, rows=512):
+    from oracle import oracle as O
+    ot = O.OracleTree(tree.top.height, tree.d, tree.top.split_values, np.ascontiguousarray(np.asarray(tree.leaves.points)),
+                      tree.leaves.original_index, tree.leaves.leaf_starts)
+    r = O.knn_tree(ot, np.ascontiguousarray(queries[:rows]), k, threads=os.cpu_count() or 1)
+    return bool(np.array_equal(r["keys"], keys[:rows]))
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def cfg1(a):
+    refs, queries = bkt.datasets.config_inputs(1)
+    tree = bkt.build_buffer_tree(refs, 8)
+    dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
+    dev.ensure_tree(tree)
+    for kern in ("auto", "direct"):
+        dev.search(queries, 10, kernel=kern)  # warm-up
+        t0 = time.perf_counter()
+        keys, st, _ = dev.search(queries, 10, kernel=kern)
+        wall = time.perf_counter() - t0
+        dig = hashlib.sha256((keys & np.uint64(0xFFFFFFFF)).astype("<i8").tobytes()).hexdigest()
+        gold = json.load(open(ROOT / "tests" / "golden" / "c1_digest.json"))["digest_indices_sha256"]
+        emit({"config": "cfg1 uniform n=m=65536 d=10 k=10 h=8", "kernel": kern, "qps_device": 65536 / (st["search_ms"] / 1e3),
+              "qps_e2e": 65536 / wall, "rounds": st["rounds"], "digest_matches_reference": dig == gold})
+    dev.close()
+
+
+def _gen(args):
+    c, size = args
+    return gen_query_chunk(c, size, 10)
+
+
+def cfg3(a):
+    n, m, chunk = 2_000_000, int(a.m), 10_000_000
+    pts, _ = gen_mixture(n + 10_000_000, 10, seed=1)
+    refs = pts.data[:n]
+    tree = bkt.build_buffer_tree(refs, 9)
+    dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
+    dev.ensure_tree(tree)
+    nchunks = (m + chunk - 1) // chunk
+    h = hashlib.sha256()
+    first_q = first_k = None
+    t_search = 0.0
+    with ProcessPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        futs = [ex.submit(_gen, (c, min(chunk, m - c * chunk))) for c in range(min(nchunks, 10))]
+        t0 = time.perf_counter()
+        done = 0
+        for c in range(nchunks):
+            q = futs[c].result()
+            if c + 10 < nchunks:
+                futs.append(ex.submit(_gen, (c + 10, min(chunk, m - (c + 10) * chunk))))
+            s0 = time.perf_counter()
+            keys, st, _ = dev.search(q, 10)  # public API call: H2D, search, D2H
+            t_search += time.perf_counter() - s0
+            h.update((keys & np.uint64(0xFFFFFFFF)).astype("<i8").tobytes())
+            if c == 0:
+                first_q, first_k = q, keys
+            done += q.shape[0]
+        wall = time.perf_counter() - t0
+    ok = oracle_check(tree, first_q, first_k, 10)
+    emit({"config": f"cfg3 stream: n=2M refs, m={m} queries in {nchunks} chunks of {chunk} (config-3 recipe, "
+                    f"default_rng(1000+c)), d=10, k=10, h=9, 1 GPU", "qps_search_api": done / t_search,
+          "qps_wall_incl_host_generation": done / wall, "digest_sha256": h.hexdigest(), "sample_rows_match_oracle": ok})
+    dev.close()
+
+
+def cfg4(a):
+    n, m = 2_000_000, int(a.m)
+    for d in (5, 15, 27):
+        pts, _ = gen_mixture(n + m, d, seed=1)
+        refs, queries = pts.data[:n], pts.data[n:]
+        tree = bkt.build_buffer_tree(refs, 9)
+        dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
+        dev.ensure_tree(tree)
+        for kern in ("auto", "direct"):
+            dev.search(queries[:100000], 10, kernel=kern)
+            keys, st, _ = dev.search(queries, 10, kernel=kern, timing=True)
+            ok = oracle_check(tree, queries, keys, 10, rows=256)
+            emit({"config": f"cfg4 mixture n=2M m={m} d={d} k=10 h=9", "kernel": kern, "qps_device": m / (st["search_ms"] / 1e3),
+                  "pairs_per_query": st["pairs"] / m, "leafscan_tflops_fp32_equiv": 3 * d * st["pairs"] / (st["leafscan_ms"] / 1e3) / 1e12,
+                  "rounds": st["rounds"], "sample_rows_match_oracle": ok})
+        dev.close()
+
+
+def cfg5(a):
+    n, m = 8_000_000, int(a.m)
+    pts, _ = gen_mixture(n + m, 10, seed=1)
+    refs, queries = pts.data[:n], pts.data[n:]
+    for h in (8, 11, 14):
+        tree = bkt.build_buffer_tree(refs, h)
+        for num_chunks in (1, 4):
+            plan = bkt.ChunkPlan.build(n, num_chunks)
+            dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
+            dev.ensure_tree(tree, plan if num_chunks > 1 else None)
+            for k in (1, 10, 50):
+                t0 = time.perf_counter()
+                keys, st, _ = dev.search(queries, k, timing=True)
+                wall = time.perf_counter() - t0
+                ok = oracle_check(tree, queries, keys, k, rows=128)
+                emit({"config": f"cfg5 mixture n=8M m={m} d=10 h={h} k={k} "
+                                f"{'host-resident, ' + str(num_chunks) + ' chunks streamed' if num_chunks > 1 else 'HBM-resident'}",
+                      "qps_device": m / (st["search_ms"] / 1e3), "qps_wall": m / wall, "rounds": st["rounds"],
+                      "pairs_per_query": st["pairs"] / m, "sample_rows_match_oracle": ok})
+            dev.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", choices=["cfg1", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--m", type=float, default=None)
+    a = ap.parse_args()
+    if a.m is None:
+        a.m = {"cfg1": 65536, "cfg3": 2e8, "cfg4": 10e6, "cfg5": 1e6}[a.which]
+    globals()[a.which](a)
+
+
+if __name__ == "__main__":
+    main()

@@ -196,11 +196,17 @@ def main() -> None:
     import torch.distributed as dist
     # one process per GPU; on a box with fewer GPUs than ranks (smoke-testing the
     # multi-rank flow) ranks share devices round-robin
-    local = local % max(1, torch.cuda.device_count())
+    ngpu = max(1, torch.cuda.device_count())
+    local = local % ngpu
     torch.cuda.set_device(local)
+    shared = world > ngpu  # NCCL refuses two ranks on one GPU: use gloo for the control collectives
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev_t = torch.device("cuda", local)
+    red_t = torch.device("cpu") if shared else dev_t
 
     import paper_1512_02831_b200 as bkt
     refs, queries = workload(rank, a.n, a.m)
@@ -280,7 +286,7 @@ def main() -> None:
     def allmax(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev_t)
+        t = torch.tensor([x], dtype=torch.float64, device=red_t)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -333,6 +339,8 @@ def main() -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference gen_mixture recipe, seed 1; 8 gaussians, spread 0.05)",
             "config": {"workload": f"cfg2: mixture n={a.n} refs, m={m} queries per GPU, d={DIM}, k={K}, "
+                                   + ("ranks sharing GPUs (smoke test), " if shared else "")
+                                   + 
                                    f"in-memory", "height": h, "mode": a.mode, "kernel": a.kernel,
                        "parallelism": f"query-sharded x{world} (tree replicated, no collective)",
                        "l2": "256 MiB write between steps; per-step inputs (1.2 GB) > L2",

@@ -123,6 +123,8 @@ struct bkt_ctx {
   int h_tile_off_cap = 0;
   uint64_t* h_stage = nullptr;  // pinned staging for D2H / H2D
   size_t h_stage_bytes = 0;
+  char* stage_slot[2] = {nullptr, nullptr};  // pinned staging slots for host <-> device streaming
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 
   std::vector<cudaEvent_t> ev_pool;   // leafscan timing events
   cudaEvent_t ring_ev[4] = {};        // round-check ring (kRing)
@@ -281,6 +283,75 @@ cudaEvent_t get_event(bkt_ctx* c, size_t i) {
   return c->ev_pool[i];
 }
 
+constexpr size_t kStageSlot = 32ull << 20;
+
+// memcpy with a few host threads (host <-> pinned staging is the e2e bottleneck)
+void par_memcpy(void* dst, const void* src, size_t n) {
+  const int nt = (int)std::min<size_t>(8, std::max<size_t>(1, n >> 22));
+  if (nt <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    size_t a = t * per, b = std::min(n, a + per);
+    if (a >= b) break;
+    th.emplace_back([=]() { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
+  }
+  for (auto& x : th) x.join();
+}
+
+int ensure_stage_slots(bkt_ctx* ctx) {
+  for (int i = 0; i < 2; ++i) {
+    if (!ctx->stage_slot[i]) CU(cudaHostAlloc(&ctx->stage_slot[i], kStageSlot, cudaHostAllocDefault));
+    if (!ctx->stage_ev[i]) CU(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+  }
+  return BKT_OK;
+}
+
+// pageable host -> device: host threads fill one pinned slot while the other DMAs
+int h2d_staged(bkt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  int rc = ensure_stage_slots(ctx);
+  if (rc != BKT_OK) return rc;
+  size_t off = 0;
+  for (int i = 0; off < bytes; ++i) {
+    const int s = i & 1;
+    const size_t n = std::min(kStageSlot, bytes - off);
+    CU(cudaEventSynchronize(ctx->stage_ev[s]));  // slot's previous DMA done (never-recorded events return at once)
+    par_memcpy(ctx->stage_slot[s], (const char*)src + off, n);
+    CU(cudaMemcpyAsync((char*)dst + off, ctx->stage_slot[s], n, cudaMemcpyHostToDevice, ctx->copy_stream));
+    CU(cudaEventRecord(ctx->stage_ev[s], ctx->copy_stream));
+    off += n;
+  }
+  CU(cudaStreamSynchronize(ctx->copy_stream));
+  return BKT_OK;
+}
+
+// device -> pageable host: DMA chunk i+1 into one slot while host threads drain the other
+int d2h_staged(bkt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  int rc = ensure_stage_slots(ctx);
+  if (rc != BKT_OK) return rc;
+  const size_t nchunks = (bytes + kStageSlot - 1) / kStageSlot;
+  auto issue = [&](size_t i) -> int {
+    const int s = (int)(i & 1);
+    const size_t off = i * kStageSlot, n = std::min(kStageSlot, bytes - off);
+    CU(cudaMemcpyAsync(ctx->stage_slot[s], (const char*)src + off, n, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    CU(cudaEventRecord(ctx->stage_ev[s], ctx->copy_stream));
+    return BKT_OK;
+  };
+  if (nchunks == 0) return BKT_OK;
+  if ((rc = issue(0)) != BKT_OK) return rc;
+  for (size_t i = 0; i < nchunks; ++i) {
+    const int s = (int)(i & 1);
+    CU(cudaEventSynchronize(ctx->stage_ev[s]));
+    if (i + 1 < nchunks && (rc = issue(i + 1)) != BKT_OK) return rc;
+    const size_t off = i * kStageSlot, n = std::min(kStageSlot, bytes - off);
+    par_memcpy((char*)dst + off, ctx->stage_slot[s], n);
+  }
+  return BKT_OK;
+}
+
 // host quad-interleaved layout of the leaf structure
 void build_quad_layout(const float* leaf_points, const int64_t* orig, const int64_t* starts, int nl, int d, int D,
                        const std::vector<long long>& qb, float* out_pts, uint32_t* out_idx) {
@@ -431,6 +502,10 @@ void bkt_close(bkt_ctx* ctx) {
   free_leafbufs(ctx);
   dfree(ctx->ctl); dfree(ctx->pairs); dfree(ctx->seq_pos); dfree(ctx->seq_dev); dfree(ctx->hist);
   hfree(ctx->h_ctl); hfree(ctx->h_stage);
+  for (int i = 0; i < 2; ++i) {
+    hfree(ctx->stage_slot[i]);
+    if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+  }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < kRing; ++i)
     if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
@@ -858,7 +933,9 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   R.timing = o.record_timing != 0;
   R.seq = o.seq_log != nullptr && o.seq_cap > 0;
   R.seq_cap = R.seq ? o.seq_cap : 0;
-  R.tc = ctx->has_tc && ctx->residency == 0 && o.kernel != 1;
+  // auto: the tensor-core filter from d >= 8 (below that the CUDA-core scan is
+  // as fast: few pairs per query and a mostly empty K=16 MMA; tools/configs.py cfg4)
+  R.tc = ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
   R.unfused = false;
   if (const char* e = std::getenv("BKT_TC_UNFUSED")) R.unfused = std::atoi(e) != 0;
   if (o.kernel == 2 && !R.tc) return set_err(ctx, BKT_EINVAL, "tensor-core kernel requested but unavailable (needs a resident tree and d <= 31)");
@@ -918,8 +995,9 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
       else raw = const_cast<float*>(src);
     } else {
       auto c0 = std::chrono::steady_clock::now();
-      CU(cudaMemcpyAsync(raw, src, qbytes, cudaMemcpyHostToDevice, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
+      rc = h2d_staged(ctx, raw, src, qbytes);
+      if (rc != BKT_OK) return rc;
       st.h2d_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
       st.h2d_bytes += qbytes;
     }
@@ -936,8 +1014,9 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
       CU(cudaMemcpyAsync(out_keys + b0 * k, ctx->keys, kbytes, cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
       auto c0 = std::chrono::steady_clock::now();
-      CU(cudaMemcpyAsync(out_keys + b0 * k, ctx->keys, kbytes, cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
+      rc = d2h_staged(ctx, out_keys + b0 * k, ctx->keys, kbytes);
+      if (rc != BKT_OK) return rc;
       st.d2h_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
       st.d2h_bytes += kbytes;
     }

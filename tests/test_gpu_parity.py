@@ -40,7 +40,7 @@ def assert_fma_close(got_keys, want_keys, rtol=FMA_RTOL):
             assert near.sum() >= 2 or cc == got_keys.shape[1] - 1, (rr, cc)
 
 
-@pytest.mark.parametrize("kernel", ["direct", "auto"])
+@pytest.mark.parametrize("kernel", ["direct", "tc"])
 def test_golden_instances_exact(knn_golden, gpu_device, kernel):
     """Every golden instance: keys, counts, visited counts, leaf sequences,
     for the CUDA-core scan and the tensor-core filter (auto, d <= 31)."""
@@ -194,7 +194,7 @@ def test_dimension_coverage_exact(rng, gpu_device, d):
     tree = bkt.build_buffer_tree(refs, 6)
     for k in (1, 3, 10, 33):
         want = O.brute_keys(refs, queries, k, threads=4)
-        for kernel in ("direct", "auto"):
+        for kernel in ("direct", "tc") if d <= 31 else ("direct", "auto"):
             res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), device=gpu_device, kernel=kernel)
             assert np.array_equal(res.keys, want), (d, k, kernel)
 

@@ -379,57 +379,29 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         }
       };
 
-      // The tile's TMEM rows are consumed as one stream of 32-column groups
-      // (two per 64-column chunk).  The load of group i+1 -- across chunk
-      // boundaries -- is issued before group i is filtered, and each TMEM
-      // accumulator is handed back to the MMA warp as soon as its columns are
-      // in registers; the smem stage (ids, coordinates) is released after the
-      // chunk's survivors are re-evaluated.
-      const uint32_t g0 = g;
-      const int ngroups = (int)((T.r1 - T.r0) / 32);
-      auto chunk_ready = [&](int c) {
-        const uint32_t gc = g0 + c;
+      for (int c = 0; c < T.nchunks; ++c, ++g) {
+        const int s = g % kTcStages;
+        const uint32_t b = g % kTcBufs;
+        const long long te0 = clock64();
         if (A.spin) {
-          mbar_wait_spin(&tfull[gc % kTcBufs], (gc / kTcBufs) & 1u);
-          mbar_wait_spin(&full[gc % kTcStages], (gc / kTcStages) & 1u);
+          mbar_wait_spin(&tfull[b], (g / kTcBufs) & 1u);
+          mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
         } else {
-          mbar_wait(&tfull[gc % kTcBufs], (gc / kTcBufs) & 1u);
-          mbar_wait(&full[gc % kTcStages], (gc / kTcStages) & 1u);
+          mbar_wait(&tfull[b], (g / kTcBufs) & 1u);
+          mbar_wait(&full[s], (g / kTcStages) & 1u);
         }
         tc_fence_after();
-      };
-      auto taddr = [&](int i) {
-        return tmem + lane_base + ((g0 + (i >> 1)) % kTcBufs) * kTcRows + (i & 1) * 32;
-      };
-      auto release_tmem = [&](int c) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[(g0 + c) % kTcBufs]);
-      };
-      auto release_stage = [&](int c) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[(g0 + c) % kTcStages]);
-        if (A.dbg && blockIdx.x == 0 && tid == 0 && (int)(g0 + c) < A.dbg_cap) {
-          A.dbg[8 * (g0 + c) + 5] = clock64();
-          A.dbg[8 * (g0 + c) + 6] = tt;
-        }
-      };
-      auto stage_of = [&](int i) { return (int)((g0 + (i >> 1)) % kTcStages); };
-      auto row0_of = [&](int i) { return T.r0 + (long long)(i >> 1) * kTcRows; };
-
-      uint32_t va[32], vb[32];
-      if (ngroups > 0) {
-        chunk_ready(0);
-        tmem_ld32_async(taddr(0), va);
-      }
-      for (int i = 0; i < ngroups; i += 2) {
-        // ---- group i (even: first group of chunk i/2), data in va
+        const long long te1 = clock64();
+        const long long row0 = T.r0 + (long long)c * kTcRows;
+        const int ngrp = (int)dmin_ll(kTcRows, T.r1 - row0) / 32;
+        const uint32_t tbase = tmem + lane_base + b * kTcRows;
+        // both 32-column groups of the chunk in flight, one wait
+        uint32_t va[32], vb[32];
+        tmem_ld32_async(tbase, va);
+        if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
         tmem_wait_ld();
-        const bool pair = i + 1 < ngroups;
-        if (pair) tmem_ld32_async(taddr(i + 1), vb);
-        else release_tmem(i >> 1);
         if constexpr (KB <= 32) {
-          if (i == 0 && valid && kth == __int_as_float(0x7f800000)) {
+          if (c == 0 && valid && kth == __int_as_float(0x7f800000)) {
             // No k-th neighbour yet (first leaf): bound it from this chunk's first
             // 32 points.  With U_j = T_j + qn + 2C (qn + pnmax_leaf) >= D_ref(q, p_j)
             // (the filter's error analysis), the KB >= k disjoint column groups
@@ -451,22 +423,21 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
             }
           }
         }
-        process(va, 0, stage_of(i), row0_of(i));
-        if (!pair) {
-          release_stage(i >> 1);
-          break;
+        process(va, 0, s, row0);
+        if (ngrp > 1) process(vb, 32, s, row0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&tempty[b]);
+          mbar_arrive(&empty[s]);
         }
-        // ---- group i+1 (second group of chunk i/2), data in vb
-        tmem_wait_ld();
-        release_tmem(i >> 1);
-        if (i + 2 < ngroups) {
-          chunk_ready((i + 2) >> 1);
-          tmem_ld32_async(taddr(i + 2), va);
+        if (A.dbg && blockIdx.x == 0 && tid == 0 && (int)g < A.dbg_cap) {
+          A.dbg[8 * g + 3] = te0;
+          A.dbg[8 * g + 4] = te1;
+          A.dbg[8 * g + 5] = clock64();
+          A.dbg[8 * g + 6] = tt;
         }
-        process(vb, 32, stage_of(i), row0_of(i));
-        release_stage(i >> 1);
       }
-      g = g0 + T.nchunks;
       if (__any_sync(0xffffffffu, cn > 0)) merge();
 
       if (tid == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)(__ldg(a.leaf_size + T.leaf)) * T.qcnt);

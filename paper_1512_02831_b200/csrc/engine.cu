@@ -34,7 +34,8 @@
 using namespace bkt;
 
 namespace bkt {
-cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ);
+cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ,
+                               int nr);
 }
 
 namespace {
@@ -669,6 +670,7 @@ struct SearchRun {
   bool fma = false;
   bool tc = false;
   bool unfused = false;
+  int tc_rows = 128;  // TC chunk width (BKT_TC_N)
   int grid_scan = 0;
   int grid_small = 0;
   bool timing = false;
@@ -744,7 +746,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
       cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * cap, ctx->stream);
       t.dbg = dbg;
       t.dbg_cap = cap;
-      CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr));
+      CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows));
       std::vector<long long> h(8 * cap);
       CU(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * 8 * cap, cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
@@ -757,7 +759,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
       R.leafscan_launches++;
       return BKT_OK;
     }
-    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr));
+    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows));
   } else {
     CU(launch_leafscan(ctx->D, R.kb, R.fma, R.grid_scan, ctx->stream, a, nullptr));
   }
@@ -785,6 +787,12 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
     int t0 = ctx->h_tile_off[ctx->chunk_leaf_lo[j]], t1 = ctx->h_tile_off[ctx->chunk_leaf_hi[j] + 1];
     if (t1 > t0) need.push_back(j);
   }
+  // Chunks still resident from the previous round go first, so a round copies
+  // only (chunks with work - 2) chunks and leaves its last two resident for the
+  // next round (the reference re-streams every chunk every round,
+  // device.py:432-446; results do not depend on the order).
+  std::stable_partition(need.begin(), need.end(),
+                        [&](int j) { return ctx->slot_chunk[0] == j || ctx->slot_chunk[1] == j; });
   const int D = ctx->D;
   auto ensure_resident = [&](int j, int avoid_slot) -> int {
     for (int s = 0; s < 2; ++s)
@@ -937,6 +945,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // as fast: few pairs per query and a mostly empty K=16 MMA; tools/configs.py cfg4)
   R.tc = ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
   R.unfused = false;
+  if (const char* e = std::getenv("BKT_TC_N")) R.tc_rows = std::atoi(e) == 64 ? 64 : 128;
   if (const char* e = std::getenv("BKT_TC_UNFUSED")) R.unfused = std::atoi(e) != 0;
   if (o.kernel == 2 && !R.tc) return set_err(ctx, BKT_EINVAL, "tensor-core kernel requested but unavailable (needs a resident tree and d <= 31)");
   int rc = BKT_OK;
@@ -944,7 +953,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     // two CTAs per SM (2 x 256 TMEM columns); the attributes are set by the query
     int occ = 0;
     TcArgs dummy{};
-    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, 0, nullptr, dummy, &occ));
+    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, 0, nullptr, dummy, &occ, R.tc_rows));
     int per_sm = 2;
     if (const char* e = std::getenv("BKT_TC_CTAS")) per_sm = std::max(1, std::min(2, std::atoi(e)));
     R.grid_scan = per_sm * ctx->sm_count;

@@ -30,11 +30,11 @@
 
 namespace bkt {
 
-constexpr int kTcRows = 64;                   // points per chunk (MMA N)
-constexpr int kTcBufs = 4;                    // TMEM accumulators (MMA runs kTcBufs-1 chunks ahead)
+// chunk width NR (MMA N) is a template parameter: NR = 64 with 4 TMEM
+// accumulators or NR = 128 with 2; both use 256 TMEM columns (two CTAs/SM)
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
-constexpr int kTcTmemCols = kTcBufs * kTcRows;  // 256 columns: two CTAs per SM
+constexpr int kTcTmemCols = 256;
 constexpr float kTcMargin = 1.0f / 128.0f;    // C
 
 struct TcArgs {
@@ -53,12 +53,14 @@ struct TcArgs {
   int dbg_cap;
 };
 
-template <int KT>
+template <int KT, int NR>
 struct TcSmem {
-  static constexpr int kStages = KT <= 16 ? 8 : 4;
-  static constexpr int kStageB = kTcRows * KT * 4;
-  static constexpr int kStageIdx = kTcRows * 4;
-  static constexpr int kStageRows = kTcRows * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
+  static constexpr int kRows = NR;
+  static constexpr int kBufs = kTcTmemCols / NR;
+  static constexpr int kStages = (KT <= 16 ? 8 : 4) * 64 / NR;
+  static constexpr int kStageB = NR * KT * 4;
+  static constexpr int kStageIdx = NR * 4;
+  static constexpr int kStageRows = NR * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
   static constexpr int kA = 128 * KT * 4;
   static constexpr int kOffIdx = kStages * kStageB;
   static constexpr int kOffRows = kOffIdx + kStages * kStageIdx;
@@ -66,7 +68,7 @@ struct TcSmem {
   static constexpr int kOffQs = kOffA + 2 * kA;
   static constexpr int kOffQ = kOffQs + 128 * KT * 4;
   static constexpr int kOffBar = kOffQ + kQueue * 128 * 8;
-  static constexpr int kNumBars = 2 * kStages + 2 * kTcBufs + 4;
+  static constexpr int kNumBars = 2 * kStages + 2 * kBufs + 4;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
 };
 
@@ -125,6 +127,7 @@ struct TcTile {
   int nchunks;
 };
 
+template <int kTcRows>
 __device__ __forceinline__ TcTile tc_tile_info(const TcArgs& A, int t) {
   const int4 rec = __ldg(A.s.tiles + t);
   TcTile T;
@@ -149,9 +152,11 @@ __device__ __forceinline__ float exact_dist(const float* __restrict__ qp, const 
   return acc;
 }
 
-template <int KT, int KB, bool FMA>
+template <int KT, int KB, bool FMA, int NR>
 __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs A) {
-  using S = TcSmem<KT>;
+  using S = TcSmem<KT, NR>;
+  constexpr int kTcRows = NR;
+  constexpr int kTcBufs = S::kBufs;
   const ScanArgs& a = A.s;
   extern __shared__ unsigned char smem_raw[];
   // 1 KB alignment for the operand tiles
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
     if (lane == 0) {
       uint32_t g = 0;
       for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x) {
-        const TcTile T = tc_tile_info(A, t);
+        const TcTile T = tc_tile_info<kTcRows>(A, t);
         for (int c = 0; c < T.nchunks; ++c, ++g) {
           const int s = g % kTcStages;
           const uint32_t use = g / kTcStages;
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       uint32_t g = 0, tt = 0;
       const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
       for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x, ++tt) {
-        const TcTile T = tc_tile_info(A, t);
+        const TcTile T = tc_tile_info<kTcRows>(A, t);
         const uint32_t ab = tt & 1u;
         if (A.spin) mbar_wait_spin(&afull[ab], (tt >> 1) & 1u); else mbar_wait(&afull[ab], (tt >> 1) & 1u);
         tc_fence_after();
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
     const int d = A.d;
     uint32_t g = 0, tt = 0;
     for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x, ++tt) {
-      const TcTile T = tc_tile_info(A, t);
+      const TcTile T = tc_tile_info<kTcRows>(A, t);
       const uint32_t ab = tt & 1u;
       const bool valid = tid < T.qcnt;
       const int qi = valid ? __ldg(a.work + T.qbeg + tid) : 0;
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         const long long row0 = T.r0 + (long long)c * kTcRows;
         const int ngrp = (int)dmin_ll(kTcRows, T.r1 - row0) / 32;
         const uint32_t tbase = tmem + lane_base + b * kTcRows;
-        // both 32-column groups of the chunk in flight, one wait
+        // two 32-column groups in flight, one wait (NR = 128: second pair below)
         uint32_t va[32], vb[32];
         tmem_ld32_async(tbase, va);
         if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
@@ -425,6 +430,15 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         }
         process(va, 0, s, row0);
         if (ngrp > 1) process(vb, 32, s, row0);
+        if constexpr (NR > 64) {
+          if (ngrp > 2) {
+            tmem_ld32_async(tbase + 64, va);
+            if (ngrp > 3) tmem_ld32_async(tbase + 96, vb);
+            tmem_wait_ld();
+            process(va, 64, s, row0);
+            if (ngrp > 3) process(vb, 96, s, row0);
+          }
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {

@@ -5,11 +5,11 @@
 
 namespace bkt {
 namespace {
-template <int KT, int KB, bool FMA>
+template <int KT, int KB, bool FMA, int NR>
 cudaError_t launch_tc_one(int grid, cudaStream_t s, const TcArgs& a, int* occ) {
-  auto fn = leafscan_tc_kernel<KT, KB, FMA>;
+  auto fn = leafscan_tc_kernel<KT, KB, FMA, NR>;
   // at least 76 KB so that no more than two CTAs (2 x 256 TMEM columns) share an SM
-  constexpr int smem = TcSmem<KT>::kBytes > 78 * 1024 ? TcSmem<KT>::kBytes : 78 * 1024;
+  constexpr int smem = TcSmem<KT, NR>::kBytes > 78 * 1024 ? TcSmem<KT, NR>::kBytes : 78 * 1024;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -18,12 +18,12 @@ cudaError_t launch_tc_one(int grid, cudaStream_t s, const TcArgs& a, int* occ) {
   fn<<<grid, kTcThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
-template <int KT>
+template <int KT, int NR>
 cudaError_t launch_tc_kt(int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ) {
   switch (kb) {
 #define BKT_CASE(KB) \
   case KB:           \
-    return fma ? launch_tc_one<KT, KB, true>(grid, s, a, occ) : launch_tc_one<KT, KB, false>(grid, s, a, occ);
+    return fma ? launch_tc_one<KT, KB, true, NR>(grid, s, a, occ) : launch_tc_one<KT, KB, false, NR>(grid, s, a, occ);
     BKT_KB_LIST(BKT_CASE)
 #undef BKT_CASE
     default:
@@ -32,9 +32,15 @@ cudaError_t launch_tc_kt(int kb, bool fma, int grid, cudaStream_t s, const TcArg
 }
 }  // namespace
 
-cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ) {
-  if (kt == 16) return launch_tc_kt<16>(kb, fma, grid, s, a, occ);
-  if (kt == 32) return launch_tc_kt<32>(kb, fma, grid, s, a, occ);
+cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ,
+                               int nr) {
+  if (nr == 128) {
+    if (kt == 16) return launch_tc_kt<16, 128>(kb, fma, grid, s, a, occ);
+    if (kt == 32) return launch_tc_kt<32, 128>(kb, fma, grid, s, a, occ);
+  } else {
+    if (kt == 16) return launch_tc_kt<16, 64>(kb, fma, grid, s, a, occ);
+    if (kt == 32) return launch_tc_kt<32, 64>(kb, fma, grid, s, a, occ);
+  }
   return cudaErrorInvalidValue;
 }
 }  // namespace bkt

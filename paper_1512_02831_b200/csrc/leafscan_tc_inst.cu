@@ -1,5 +1,7 @@
 // leafscan_tc_inst.cu -- instantiates the tensor-core leaf filter kernel for
 // K tiles of 16 and 32 (d + 1 <= KT) and every top-k bucket.
+#include <atomic>
+
 #include "dims.h"
 #include "leafscan_tc.cuh"
 
@@ -10,10 +12,19 @@ cudaError_t launch_tc_one(int grid, cudaStream_t s, const TcArgs& a, int* occ) {
   auto fn = leafscan_tc_kernel<KT, KB, FMA, NR>;
   // at least 76 KB so that no more than two CTAs (2 x 256 TMEM columns) share an SM
   constexpr int smem = TcSmem<KT, NR>::kBytes > 78 * 1024 ? TcSmem<KT, NR>::kBytes : 78 * 1024;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // function attributes are per device: set them once per (instantiation, device)
+  static std::atomic<unsigned long long> configured{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(bit, std::memory_order_release);
+  }
   if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kTcThreads, smem);
   fn<<<grid, kTcThreads, smem, s>>>(a);
   return cudaGetLastError();

@@ -54,27 +54,75 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
 
 
+def _deps(src: Path, seen: set | None = None) -> set:
+    """src plus every local header it includes (transitively)."""
+    seen = set() if seen is None else seen
+    if src in seen or not src.exists():
+        return seen
+    seen.add(src)
+    for inc in re.findall(r'#include\s+"([^"]+)"', src.read_text()):
+        for base in (src.parent, CSRC, INCLUDE):
+            cand = (base / inc).resolve()
+            if cand.exists():
+                _deps(cand, seen)
+                break
+    return seen
+
+
+def _unit_hash(cmd: list[str], src: Path) -> str:
+    h = hashlib.sha256(" ".join(cmd).encode())
+    for p in sorted(_deps(src)):
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()[:16]
+
+
+def _compile(cmd: list[str], src: Path, obj: Path, force: bool) -> bool:
+    """Compile one unit unless its object is up to date; True if it ran."""
+    stamp = obj.with_suffix(".stamp")
+    tag = _unit_hash(cmd, src)
+    if not force and obj.exists() and stamp.exists() and stamp.read_text() == tag:
+        return False
+    _run(cmd)
+    stamp.write_text(tag)
+    return True
+
+
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> Path:
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
-    tag = _sources_hash("v1")
+    tag = _sources_hash("v1" + os.environ.get("BKT_BUILD_DIAG", ""))
     stamp = LIB_DIR / "libbkt.stamp"
     if LIB.exists() and stamp.exists() and stamp.read_text() == tag and not force:
         return LIB
-    units: list[tuple[list[str], Path]] = []
+    units: list[tuple[list[str], Path, Path]] = []
     for d in _dims():
         obj = OBJ_DIR / f"leafscan_d{d}.o"
-        units.append(([NVCC, *NVFLAGS, f"-DBKT_D={d}", "-c", str(CSRC / "leafscan_inst.cu"), "-o", str(obj)], obj))
-    for src in ("engine.cu", "misc.cu", "leafscan_tc_inst.cu"):
-        obj = OBJ_DIR / (Path(src).stem + ".o")
-        units.append(([NVCC, *NVFLAGS, "-c", str(CSRC / src), "-o", str(obj)], obj))
+        src = CSRC / "leafscan_inst.cu"
+        units.append(([NVCC, *NVFLAGS, f"-DBKT_D={d}", "-c", str(src), "-o", str(obj)], src, obj))
+    diag = ["-DBKT_TC_DIAG=1"] if os.environ.get("BKT_BUILD_DIAG") == "1" else []
+    for kt, nr, cps in ((16, 64, 2), (16, 128, 2), (32, 64, 2)):
+        for fma in (0, 1):
+            obj = OBJ_DIR / f"leafscan_tc_{kt}_{nr}_{cps}_{fma}.o"
+            src = CSRC / "leafscan_tc_inst.cu"
+            flags = [f"-DBKT_TC_KT={kt}", f"-DBKT_TC_NR={nr}", f"-DBKT_TC_CPS={cps}", f"-DBKT_TC_FMA={fma}", *diag]
+            if (kt, nr, cps, fma) == (16, 128, 2, 0):
+                flags.append("-DBKT_TC_DISPATCH")
+            units.append(([NVCC, *NVFLAGS, *flags, "-c", str(src), "-o", str(obj)], src, obj))
+    for name in ("engine.cu", "misc.cu"):
+        obj = OBJ_DIR / (Path(name).stem + ".o")
+        src = CSRC / name
+        units.append(([NVCC, *NVFLAGS, "-c", str(src), "-o", str(obj)], src, obj))
     obj = OBJ_DIR / "build_tree.o"
+    src = CSRC / "build_tree.cpp"
     units.append((["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-I", str(INCLUDE), "-c",
-                   str(CSRC / "build_tree.cpp"), "-o", str(obj)], obj))
+                   str(src), "-o", str(obj)], src, obj))
     jobs = jobs or max(1, os.cpu_count() or 1)
     with ThreadPoolExecutor(max_workers=jobs) as ex:
-        list(ex.map(lambda u: _run(u[0]), units))
+        ran = list(ex.map(lambda u: _compile(u[0], u[1], u[2], force), units))
+    if verbose:
+        print(f"compiled {sum(ran)} of {len(units)} units")
     tmp = LIB.with_suffix(".so.tmp")
-    _run([NVCC, *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *[str(u[1]) for u in units], "-lpthread"])
+    _run([NVCC, *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *[str(u[2]) for u in units], "-lpthread"])
     os.replace(tmp, LIB)
     stamp.write_text(tag)
     if verbose:

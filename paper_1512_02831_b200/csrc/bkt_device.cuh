@@ -169,14 +169,15 @@ struct TopTreeView {
 
 // Descend from depth `from` to a leaf along q, pushing every far child
 // (buffer_tree.py:365-376: go_left = q[sd] < split, strict; equal goes right).
-template <typename QFn>
-__device__ __forceinline__ void descend(const TopTreeView& T, QFn qget, uint32_t& leaf, uint32_t& pend,
-                                        int from) {
-  for (int j = from; j < T.h; ++j) {
-    uint32_t node = (1u << j) - 1u + (leaf >> (T.h - j));
-    float qv = qget(j % T.d);
-    uint32_t right = (qv < __ldg(T.split + node)) ? 0u : 1u;
-    uint32_t bit = 1u << (T.h - 1 - j);
+// SFn(node) returns split value `node` (global or shared memory).
+template <typename QFn, typename SFn>
+__device__ __forceinline__ void descend_with(int h, int d, SFn sget, QFn qget, uint32_t& leaf, uint32_t& pend,
+                                             int from) {
+  for (int j = from; j < h; ++j) {
+    uint32_t node = (1u << j) - 1u + (leaf >> (h - j));
+    float qv = qget(j % d);
+    uint32_t right = (qv < sget(node)) ? 0u : 1u;
+    uint32_t bit = 1u << (h - 1 - j);
     leaf = (leaf & ~bit) | (right ? bit : 0u);
     pend |= 1u << j;
   }
@@ -185,21 +186,35 @@ __device__ __forceinline__ void descend(const TopTreeView& T, QFn qget, uint32_t
 // FindLeaf for a resumed query (buffer_tree.py:330-349): pop the deepest
 // pending far child, prune while (q[sd]-split)^2 > kth in float32 (ties are
 // visited), descend into the first survivor.  Returns the leaf id or -1 (DONE).
-template <typename QFn>
-__device__ __forceinline__ int find_next_leaf(const TopTreeView& T, QFn qget, float kth, uint32_t& leaf,
-                                              uint32_t& pend) {
+template <typename QFn, typename SFn>
+__device__ __forceinline__ int find_next_leaf_with(int h, int d, SFn sget, QFn qget, float kth, uint32_t& leaf,
+                                                   uint32_t& pend) {
   while (pend) {
     int di = 31 - __clz(pend);
     pend &= ~(1u << di);
-    uint32_t parent = (1u << di) - 1u + (leaf >> (T.h - di));
-    float hp = __fsub_rn(qget(di % T.d), __ldg(T.split + parent));
+    uint32_t parent = (1u << di) - 1u + (leaf >> (h - di));
+    float hp = __fsub_rn(qget(di % d), sget(parent));
     if (!(__fmul_rn(hp, hp) > kth)) {
-      leaf ^= 1u << (T.h - 1 - di);
-      descend(T, qget, leaf, pend, di + 1);
+      leaf ^= 1u << (h - 1 - di);
+      descend_with(h, d, sget, qget, leaf, pend, di + 1);
       return (int)leaf;
     }
   }
   return -1;
+}
+
+template <typename QFn>
+__device__ __forceinline__ void descend(const TopTreeView& T, QFn qget, uint32_t& leaf, uint32_t& pend,
+                                        int from) {
+  const float* sp = T.split;
+  descend_with(T.h, T.d, [sp](uint32_t node) { return __ldg(sp + node); }, qget, leaf, pend, from);
+}
+
+template <typename QFn>
+__device__ __forceinline__ int find_next_leaf(const TopTreeView& T, QFn qget, float kth, uint32_t& leaf,
+                                              uint32_t& pend) {
+  const float* sp = T.split;
+  return find_next_leaf_with(T.h, T.d, [sp](uint32_t node) { return __ldg(sp + node); }, qget, kth, leaf, pend);
 }
 
 }  // namespace bkt

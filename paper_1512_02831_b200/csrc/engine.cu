@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -93,6 +94,17 @@ struct bkt_ctx {
   long long* tc_row_base = nullptr;
   float* tc_centroid = nullptr;
   float* tc_pnmax = nullptr;
+  unsigned long long* tc_ctr = nullptr;  // BKT_TC_COUNTERS diagnostics (8 counters)
+  // leaf-internal blocks: each leaf of the tensor-core layout is ordered as
+  // kBlockRows-point blocks along a small k-d split tree.  Queries are
+  // bucketed per (leaf, block) so that a warp's queries are neighbours, and
+  // the leaf scan skips blocks no query of a warp can reach.  Without the TC
+  // layout every leaf is one block.
+  int nkeys = 0;              // total blocks
+  int sub_w = 1;              // bucket keys per leaf (power of two): key = leaf * sub_w + sub
+  int nbuckets = 0;           // nl * sub_w
+  int* blk_base = nullptr;    // nl + 1: first block of each leaf
+  int4* nodes = nullptr;      // {split value bits, dim, left, right}; child < 0: ~local block
 
   // ---- per-batch work buffers
   long long cap_m = 0;
@@ -106,8 +118,11 @@ struct bkt_ctx {
   float* kthv = nullptr;    // per query k-th distance (TC kernel's lazy top-k)
   int* work[2] = {nullptr, nullptr};
   int cap_nl = 0;
-  int* counts = nullptr;
-  int* cursor = nullptr;
+  int cap_keys = 0;
+  int* counts = nullptr;    // per bucket key
+  int* cursor = nullptr;    // per bucket key
+  int* key_off = nullptr;   // nkeys + 1: first work-list slot of each key
+  int* qkey = nullptr;      // per query: bucket key of its next leaf visit
   int* leaf_off = nullptr;
   int* tile_off = nullptr;
   int4* tiles = nullptr;    // per-tile records (capacity tiles_cap)
@@ -208,6 +223,8 @@ int leafscan_grid(bkt_ctx* ctx, int D, int kb, bool fma, int* grid) {
 void free_tree(bkt_ctx* c) {
   dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid); dfree(c->tc_pnmax);
   c->has_tc = false;
+  dfree(c->blk_base); dfree(c->nodes);
+  c->nkeys = 0;
   dfree(c->split); dfree(c->quad_base); dfree(c->leaf_size); dfree(c->pts); dfree(c->pidx);
   hfree(c->h_pts); hfree(c->h_pidx);
   for (int s = 0; s < 2; ++s) {
@@ -221,27 +238,33 @@ void free_work(bkt_ctx* c) {
   dfree(c->tiles);
   c->tiles_cap = 0;
   dfree(c->kthv);
+  dfree(c->qkey);
   dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
   dfree(c->work[0]); dfree(c->work[1]);
   c->cap_m = 0; c->cap_k = 0;
 }
 
 void free_leafbufs(bkt_ctx* c) {
-  dfree(c->counts); dfree(c->cursor); dfree(c->leaf_off); dfree(c->tile_off);
+  dfree(c->counts); dfree(c->cursor); dfree(c->key_off); dfree(c->leaf_off); dfree(c->tile_off);
   hfree(c->h_tile_off);
   c->cap_nl = 0;
+  c->cap_keys = 0;
   c->h_tile_off_cap = 0;
 }
 
-int ensure_leafbufs(bkt_ctx* ctx, int nl) {
-  if (ctx->cap_nl >= nl) return BKT_OK;
+int ensure_leafbufs(bkt_ctx* ctx, int nl, int nkeys) {
+  if (ctx->cap_nl >= nl && ctx->cap_keys >= nkeys) return BKT_OK;
   free_leafbufs(ctx);
-  CU(cudaMalloc(&ctx->counts, sizeof(int) * nl));
-  CU(cudaMalloc(&ctx->cursor, sizeof(int) * nl));
+  CU(cudaMalloc(&ctx->counts, sizeof(int) * nkeys));
+  CU(cudaMalloc(&ctx->cursor, sizeof(int) * nkeys));
+  CU(cudaMalloc(&ctx->key_off, sizeof(int) * (nkeys + 1)));
+  CU(cudaMemset(ctx->counts, 0, sizeof(int) * nkeys));
+  CU(cudaMemset(ctx->cursor, 0, sizeof(int) * nkeys));
   CU(cudaMalloc(&ctx->leaf_off, sizeof(int) * (nl + 1)));
   CU(cudaMalloc(&ctx->tile_off, sizeof(int) * (nl + 1)));
   CU(cudaHostAlloc(&ctx->h_tile_off, sizeof(int) * (nl + 1), cudaHostAllocDefault));
   ctx->cap_nl = nl;
+  ctx->cap_keys = nkeys;
   ctx->h_tile_off_cap = nl + 1;
   return BKT_OK;
 }
@@ -257,6 +280,7 @@ int ensure_work(bkt_ctx* ctx, long long m, int k) {
   CU(cudaMalloc(&ctx->next, sizeof(int) * M));
   CU(cudaMalloc(&ctx->visits, sizeof(uint32_t) * M));
   CU(cudaMalloc(&ctx->kthv, sizeof(float) * M));
+  CU(cudaMalloc(&ctx->qkey, sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[0], sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[1], sizeof(int) * M));
   ctx->tiles_cap = M / kNT + (1ll << ctx->h) + 1;
@@ -384,6 +408,78 @@ void build_quad_layout(const float* leaf_points, const int64_t* orig, const int6
   for (auto& t : th) t.join();
 }
 
+// Leaf-internal blocks.  Each leaf's points are ordered so that consecutive
+// runs of kBlockRows form blocks of a small k-d split tree (split on the
+// widest dimension; the left side takes ceil(nb/2) full blocks).  The split
+// nodes route a home-leaf visit to its block, so the home bucket is ordered by
+// position and the scan of a first visit starts next to its queries (its k-th
+// distance bound is tight from the first chunk).  The order inside a leaf
+// never changes a result: keys are (distance, original index) and the leaf's
+// point set is the reference's.
+struct LeafBlocks {
+  std::vector<int> blk_base;     // nl + 1
+  std::vector<int4> nodes;       // nkeys - nl split nodes; leaf l's start at blk_base[l] - l
+  std::vector<uint32_t> perm;    // n: local row order of every leaf (offset by leaf start)
+};
+
+void build_leaf_blocks(const float* pts, const int64_t* starts, int nl, int d, int bs, LeafBlocks& out) {
+  out.blk_base.assign(nl + 1, 0);
+  for (int l = 0; l < nl; ++l) {
+    long long L = starts[l + 1] - starts[l];
+    out.blk_base[l + 1] = out.blk_base[l] + (int)((L + bs - 1) / bs);
+  }
+  const int nkeys = out.blk_base[nl];
+  out.nodes.assign(std::max(0, nkeys - nl), int4{0, 0, 0, 0});
+  out.perm.resize((size_t)starts[nl]);
+  auto work = [&](int l0, int l1) {
+    std::vector<uint32_t> idx;
+    for (int l = l0; l < l1; ++l) {
+      const long long s = starts[l], L = starts[l + 1] - s;
+      idx.resize(L);
+      for (long long i = 0; i < L; ++i) idx[i] = (uint32_t)i;
+      const int nb_leaf = out.blk_base[l + 1] - out.blk_base[l];
+      int4* nodes = out.nodes.data() + (out.blk_base[l] - l);
+      int next_node = 0, next_block = 0;
+      auto coord = [&](uint32_t i, int j) { return pts[(s + i) * d + j]; };
+      // returns the child code of [lo, hi) holding nb blocks
+      std::function<int(long long, long long, int)> rec = [&](long long lo, long long hi, int nb) -> int {
+        if (nb == 1) return ~(next_block++);
+        const long long left = (long long)bs * ((nb + 1) / 2);
+        int dim = 0;
+        float best = -1.0f;
+        for (int j = 0; j < d; ++j) {
+          float mn = coord(idx[lo], j), mx = mn;
+          for (long long i = lo + 1; i < hi; ++i) {
+            float v = coord(idx[i], j);
+            mn = std::min(mn, v);
+            mx = std::max(mx, v);
+          }
+          if (mx - mn > best) { best = mx - mn; dim = j; }
+        }
+        std::nth_element(idx.begin() + lo, idx.begin() + lo + left, idx.begin() + hi, [&](uint32_t a, uint32_t b) {
+          float va = coord(a, dim), vb = coord(b, dim);
+          return va < vb || (va == vb && a < b);
+        });
+        const float val = coord(idx[lo + left], dim);
+        const int me = next_node++;
+        const int lc = rec(lo, lo + left, (nb + 1) / 2);
+        const int rc = rec(lo + left, hi, nb - (nb + 1) / 2);
+        int vb;
+        std::memcpy(&vb, &val, 4);
+        nodes[me] = int4{vb, dim, lc, rc};
+        return me;
+      };
+      rec(0, L, nb_leaf);
+      for (long long i = 0; i < L; ++i) out.perm[s + i] = idx[i];
+    }
+  };
+  int nt = std::max(1, std::min<int>(16, (int)std::thread::hardware_concurrency()));
+  if (nl < 64) nt = 1;
+  std::vector<std::thread> th;
+  for (int w = 0; w < nt; ++w) th.emplace_back(work, (int)((long long)nl * w / nt), (int)((long long)nl * (w + 1) / nt));
+  for (auto& t : th) t.join();
+}
+
 // round-to-nearest (ties away) float32 -> tf32, matching cvt.rna.tf32.f32
 inline float tf32_rna_host(float x) {
   uint32_t u;
@@ -401,8 +497,8 @@ inline float tf32_rna_host(float x) {
 // tf32((1 - C) |p'|^2) in column d, zeros after; padding rows carry +inf in
 // column d so they never pass the filter.
 void build_tc_layout(const float* leaf_points, const int64_t* orig, const int64_t* starts, int nl, int d, int KT,
-                     const std::vector<long long>& rb, float* B, uint32_t* ridx, float* rows, float* centroid,
-                     float* pnmax) {
+                     const std::vector<long long>& rb, const std::vector<uint32_t>& perm, float* B, uint32_t* ridx,
+                     float* rows, float* centroid, float* pnmax) {
   auto work = [&](int l0, int l1) {
     std::vector<double> acc(d);
     for (int l = l0; l < l1; ++l) {
@@ -414,8 +510,9 @@ void build_tc_layout(const float* leaf_points, const int64_t* orig, const int64_
       for (int j = 0; j < KT; ++j) cen[j] = j < d ? (float)(acc[j] / (double)(e - s)) : 0.0f;
       float pmax = 0.0f;
       for (long long R = rb[l]; R < rb[l + 1]; ++R) {
-        long long r = s + (R - rb[l]);
-        bool real = r < e;
+        const long long loc = R - rb[l];
+        const bool real = s + loc < e;
+        const long long r = real ? s + (long long)perm[s + loc] : e;
         float* bg = B + (R / 8) * 8 * KT + (R % 8) * 4;
         float pn = 0.0f;
         for (int k = 0; k < KT; ++k) {
@@ -501,7 +598,7 @@ void bkt_close(bkt_ctx* ctx) {
   free_tree(ctx);
   free_work(ctx);
   free_leafbufs(ctx);
-  dfree(ctx->ctl); dfree(ctx->pairs); dfree(ctx->seq_pos); dfree(ctx->seq_dev); dfree(ctx->hist);
+  dfree(ctx->ctl); dfree(ctx->pairs); dfree(ctx->seq_pos); dfree(ctx->seq_dev); dfree(ctx->hist); dfree(ctx->tc_ctr);
   hfree(ctx->h_ctl); hfree(ctx->h_stage);
   for (int i = 0; i < 2; ++i) {
     hfree(ctx->stage_slot[i]);
@@ -598,8 +695,20 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       const long long R = rb[nl];
       std::vector<float> hB((size_t)R * KT), hrows((size_t)R * d), hcen((size_t)nl * KT), hpn((size_t)nl);
       std::vector<uint32_t> hidx((size_t)R);
-      build_tc_layout(leaf_points, original_index, leaf_starts, nl, d, KT, rb, hB.data(), hidx.data(), hrows.data(),
-                      hcen.data(), hpn.data());
+      LeafBlocks lb;
+      build_leaf_blocks(leaf_points, leaf_starts, nl, d, kBlockRows, lb);
+      if (std::getenv("BKT_NO_PERM"))
+        for (int l = 0; l < nl; ++l)
+          for (long long i = leaf_starts[l]; i < leaf_starts[l + 1]; ++i) lb.perm[i] = (uint32_t)(i - leaf_starts[l]);
+      build_tc_layout(leaf_points, original_index, leaf_starts, nl, d, KT, rb, lb.perm, hB.data(), hidx.data(),
+                      hrows.data(), hcen.data(), hpn.data());
+      ctx->nkeys = lb.blk_base[nl];
+      CU(cudaMalloc(&ctx->blk_base, sizeof(int) * (nl + 1)));
+      CU(cudaMemcpy(ctx->blk_base, lb.blk_base.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice));
+      if (!lb.nodes.empty()) {
+        CU(cudaMalloc(&ctx->nodes, sizeof(int4) * lb.nodes.size()));
+        CU(cudaMemcpy(ctx->nodes, lb.nodes.data(), sizeof(int4) * lb.nodes.size(), cudaMemcpyHostToDevice));
+      }
       CU(cudaMalloc(&ctx->tc_pnmax, sizeof(float) * nl));
       CU(cudaMemcpy(ctx->tc_pnmax, hpn.data(), sizeof(float) * nl, cudaMemcpyHostToDevice));
       CU(cudaMalloc(&ctx->tc_B, sizeof(float) * R * KT));
@@ -651,7 +760,28 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       ctx->slot_chunk[s] = -1;
     }
   }
-  if (ensure_leafbufs(ctx, nl) != BKT_OK) return BKT_ECUDA;
+  if (ctx->nkeys == 0) {
+    // one block per leaf (no leaf-internal order)
+    ctx->nkeys = nl;
+    std::vector<int> ident(nl + 1);
+    for (int l = 0; l <= nl; ++l) ident[l] = l;
+    CU(cudaMalloc(&ctx->blk_base, sizeof(int) * (nl + 1)));
+    CU(cudaMemcpy(ctx->blk_base, ident.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice));
+  }
+  // sub-buckets per leaf: one per block of the largest leaf (power of two)
+  ctx->sub_w = 1;
+  {
+    int maxnb = 1;
+    for (int l = 0; l < nl; ++l) maxnb = std::max(maxnb, (int)((ctx->h_leaf_size[l] + kBlockRows - 1) / kBlockRows));
+    if (ctx->nkeys > nl)
+      while (ctx->sub_w < maxnb && ctx->sub_w < 64) ctx->sub_w <<= 1;
+  }
+  if (const char* e = std::getenv("BKT_SUB_W")) {
+    int w = std::atoi(e);
+    if (w >= 1 && (w & (w - 1)) == 0) ctx->sub_w = w;
+  }
+  ctx->nbuckets = nl * ctx->sub_w;
+  if (ensure_leafbufs(ctx, nl, ctx->nbuckets) != BKT_OK) return BKT_ECUDA;
   ctx->has_tree = true;
   return BKT_OK;
 }
@@ -670,7 +800,7 @@ struct SearchRun {
   bool fma = false;
   bool tc = false;
   bool unfused = false;
-  int tc_rows = 128;  // TC chunk width (BKT_TC_N)
+  int tc_rows = 128;  // TC chunk width (BKT_TC_N): 64 or 128 columns
   int grid_scan = 0;
   int grid_small = 0;
   bool timing = false;
@@ -682,6 +812,7 @@ struct SearchRun {
   long long rounds = 0;
   bool seq = false;
   long long seq_cap = 0;
+  bool counters = false;
 };
 
 ScanArgs make_scan_args(bkt_ctx* ctx, SearchRun& R, int cur) {
@@ -737,24 +868,28 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.d = ctx->d;
     t.qstride = ctx->D;
     t.spin = 1;
+    t.ctr = R.counters ? ctx->tc_ctr : nullptr;
     if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e) != 0;
     if (std::getenv("BKT_TC_DEBUG") && R.leafscan_launches == 5) {
       // per-chunk timestamps of CTA 0 in the 6th leafscan launch (a steady-state round)
       static long long* dbg = nullptr;
       const int cap = 4096;
-      if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 8 * cap);
-      cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * cap, ctx->stream);
+      if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * cap);
+      cudaMemsetAsync(dbg, 0, sizeof(long long) * 16 * cap, ctx->stream);
       t.dbg = dbg;
       t.dbg_cap = cap;
       CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows));
-      std::vector<long long> h(8 * cap);
-      CU(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * 8 * cap, cudaMemcpyDeviceToHost, ctx->stream));
+      std::vector<long long> h(16 * cap);
+      CU(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * 16 * cap, cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
       long long base = h[0];
-      for (int g = 0; g < cap && h[8 * g + 5]; ++g)
-        std::fprintf(stderr, "chunk %d tile %lld prod_wait %lld prod_issue %lld mma_ready %lld epi_start %lld epi_ready %lld epi_done %lld\n",
-                     g, h[8 * g + 6], h[8 * g] - base, h[8 * g + 1] - base, h[8 * g + 2] - base, h[8 * g + 3] - base,
-                     h[8 * g + 4] - base, h[8 * g + 5] - base);
+      auto rel = [&](long long v) { return v ? v - base : -1; };
+      for (int g = 0; g < cap && h[16 * g + 5]; ++g)
+        std::fprintf(stderr, "chunk %d tile %lld prod_wait %lld prod_issue %lld mma_ready %lld epi_start %lld epi_ready %lld "
+                     "epi_done %lld ld0 %lld g0 %lld g1 %lld g2 %lld g3 %lld trips %lld anyg %lld\n",
+                     g, h[16 * g + 6], rel(h[16 * g]), rel(h[16 * g + 1]), rel(h[16 * g + 2]), rel(h[16 * g + 3]),
+                     rel(h[16 * g + 4]), rel(h[16 * g + 5]), rel(h[16 * g + 7]), rel(h[16 * g + 8]), rel(h[16 * g + 9]),
+                     rel(h[16 * g + 10]), rel(h[16 * g + 11]), h[16 * g + 12], h[16 * g + 13]);
       R.launches++;
       R.leafscan_launches++;
       return BKT_OK;
@@ -833,7 +968,7 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
   // FindLeaf after every chunk of the round has been scanned
   findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
       ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys, ctx->state,
-      ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+      ctx->next, ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
   CU(cudaGetLastError());
   R.launches++;
   return BKT_OK;
@@ -846,11 +981,11 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   RoundCtl init{};
   init.active = (int)m;
   CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nl, ctx->stream));
-  CU(cudaMemsetAsync(ctx->cursor, 0, sizeof(int) * ctx->nl, ctx->stream));
+  CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
+  CU(cudaMemsetAsync(ctx->cursor, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
   start_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
-                                                       ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr,
-                                                       ctx->seq_pos, R.seq_cap, ctx->kthv);
+                                                       ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
+                                                       R.seq_cap, ctx->kthv);
   CU(cudaGetLastError());
   R.launches++;
 
@@ -861,8 +996,15 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   cudaEvent_t* ring = ctx->ring_ev;
   const bool ooc = ctx->residency == 1;
   for (;;) {
-    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl,
-                                                     ctx->nl, kNT, ctx->hist, kHistCap, ctx->tiles,
+    // queries with a next leaf -> bucket keys (leaf, block) + counts
+    bucket_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->ctl, ctx->next,
+                                                          ctx->q, ctx->D, ctx->blk_base, ctx->nodes, ctx->sub_w,
+                                                          ctx->qkey, ctx->counts);
+    CU(cudaGetLastError());
+    R.launches++;
+    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, ctx->sub_w, ctx->nbuckets,
+                                                     ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl, ctx->nl, kNT,
+                                                     ctx->hist, kHistCap, ctx->tiles,
                                                      (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
     CU(cudaGetLastError());
     R.launches++;
@@ -875,7 +1017,8 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       if (ctx->h_ctl[slot].active == 0) break;
     }
     scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->next,
-                                                           ctx->leaf_off, ctx->cursor, ctx->work[cur], ctx->ctl);
+                                                           ctx->qkey, ctx->key_off, ctx->cursor, ctx->work[cur],
+                                                           ctx->ctl);
     CU(cudaGetLastError());
     R.launches++;
     if (ooc) {
@@ -892,7 +1035,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
         // then overlap across many warps instead of stalling the scan's epilogue
         findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
             ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys,
-            ctx->state, ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+            ctx->state, ctx->next, ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
         CU(cudaGetLastError());
         R.launches++;
       }
@@ -954,8 +1097,12 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     int occ = 0;
     TcArgs dummy{};
     CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, 0, nullptr, dummy, &occ, R.tc_rows));
+    // two CTAs per SM: the variants are sized for it (2 x 256 TMEM columns,
+    // shared memory and registers); the occupancy query is only a sanity check
     int per_sm = 2;
-    if (const char* e = std::getenv("BKT_TC_CTAS")) per_sm = std::max(1, std::min(2, std::atoi(e)));
+    if (occ < 1) return set_err(ctx, BKT_ECUDA, "tensor-core leaf kernel cannot be resident");
+    if (const char* e = std::getenv("BKT_TC_CTAS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+    if (std::getenv("BKT_VERBOSE")) std::fprintf(stderr, "tc kernel: occupancy %d CTAs/SM, grid %d\n", occ, per_sm * ctx->sm_count);
     R.grid_scan = per_sm * ctx->sm_count;
   } else {
     rc = leafscan_grid(ctx, ctx->D, R.kb, R.fma, &R.grid_scan);
@@ -987,6 +1134,12 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   }
   CU(cudaMemsetAsync(ctx->pairs, 0, sizeof(unsigned long long), ctx->stream));
   CU(cudaMemsetAsync(ctx->seq_pos, 0, sizeof(unsigned long long), ctx->stream));
+  const bool counters = R.tc && std::getenv("BKT_TC_COUNTERS") != nullptr;
+  if (counters) {
+    if (!ctx->tc_ctr) CU(cudaMalloc(&ctx->tc_ctr, sizeof(unsigned long long) * 16));
+    CU(cudaMemsetAsync(ctx->tc_ctr, 0, sizeof(unsigned long long) * 16, ctx->stream));
+  }
+  R.counters = counters;
 
   cudaEvent_t t_all0 = ctx->t_ev[0], t_all1 = ctx->t_ev[1];
   CU(cudaEventRecord(t_all0, ctx->stream));
@@ -1056,6 +1209,14 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     CU(cudaEventElapsedTime(&t, pr.first, pr.second));
     R.leafscan_ms += t;
     per_launch.push_back(t);
+  }
+  if (counters) {
+    unsigned long long c[16];
+    CU(cudaMemcpy(c, ctx->tc_ctr, sizeof(c), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr,
+                 "tc counters: groups %llu any %llu survivors %llu loop_trips %llu merges %llu tiles %llu "
+                 "queries %llu first_visit_survivors %llu pairs %llu\n",
+                 c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], pairs);
   }
   if (std::getenv("BKT_TRACE_ROUNDS") && !per_launch.empty()) {
     // per-round diagnostics of the last batch: active queries and leafscan ms

@@ -30,12 +30,29 @@
 
 namespace bkt {
 
-// chunk width NR (MMA N) is a template parameter: NR = 64 with 4 TMEM
-// accumulators or NR = 128 with 2; both use 256 TMEM columns (two CTAs/SM)
+// Launch shape.  CPS CTAs share an SM (3 for KT = 16, 2 for KT = 32, limited
+// by shared memory); each owns 512 / CPS TMEM columns (rounded down to a
+// power of two) split into accumulator buffers of NR columns.  A CTA = 4
+// epilogue warps (one thread per query row) + a TMA producer warp + an MMA warp.
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
-constexpr int kTcTmemCols = 256;
 constexpr float kTcMargin = 1.0f / 128.0f;    // C
+constexpr int kBlockRows = 64;               // leaf-internal block (home-visit bucket key), engine.cu
+#ifndef BKT_TC_DIAG
+#define BKT_TC_DIAG 0  // 1: per-chunk timelines (BKT_TC_DEBUG) and filter counters (BKT_TC_COUNTERS)
+#endif
+constexpr bool kTcDiag = BKT_TC_DIAG != 0;
+
+__host__ __device__ constexpr int tc_tmem_cols(int cps) { return cps >= 3 ? 128 : (cps == 2 ? 256 : 512); }
+// shared memory one CTA may use when CPS share an SM (228 KB - 1 KB reserved per CTA)
+__host__ __device__ constexpr int tc_smem_per_cta(int cps) { return (228 - cps) * 1024 / cps; }
+// registers: CPS x 192 threads share 64K; with setmaxnreg the two control warps
+// give theirs to the four epilogue warps
+constexpr int kTcCtlRegs = 40;
+__host__ __device__ constexpr int tc_launch_regs(int cps) { return (65536 / (cps * kTcThreads)) & ~7; }
+__host__ __device__ constexpr int tc_epi_regs(int cps) {
+  return ((tc_launch_regs(cps) * kTcThreads - kTcCtlRegs * 64) / 128) & ~7;
+}
 
 struct TcArgs {
   ScanArgs s;                  // queries, keys, schedule, top tree, stats (quad fields unused)
@@ -49,27 +66,43 @@ struct TcArgs {
   int d;                       // real dimensionality
   int qstride;                 // row stride of the query block (kernel D of the direct path)
   int spin;                    // 1: MMA/epilogue warps spin on mbarriers instead of suspending
+  int tree_smem;               // 1: the top tree's split values are copied to shared memory
   long long* dbg;              // diagnostics (BKT_TC_DEBUG): per-chunk timestamps of CTA 0
   int dbg_cap;
+  unsigned long long* ctr;     // diagnostics (BKT_TC_COUNTERS): filter/survivor counters, see engine.cu
 };
 
-template <int KT, int NR>
+// Chunk order of a tile: starting at the chunk of the block its first query
+// was routed to (a first visit then bounds its k-th distance from nearby
+// points first), wrapping around.
+__device__ __forceinline__ int tc_chunk_at(int i, int c0, int nchunks) {
+  int c = c0 + i;
+  return c >= nchunks ? c - nchunks : c;
+}
+
+
+template <int KT, int NR, int CPS>
 struct TcSmem {
   static constexpr int kRows = NR;
-  static constexpr int kBufs = kTcTmemCols / NR;
-  static constexpr int kStages = (KT <= 16 ? 8 : 4) * 64 / NR;
+  static constexpr int kBufs = tc_tmem_cols(CPS) / NR;
+  static constexpr int kStages = (KT <= 16 ? 512 : 128) / NR;
   static constexpr int kStageB = NR * KT * 4;
   static constexpr int kStageIdx = NR * 4;
   static constexpr int kStageRows = NR * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
   static constexpr int kA = 128 * KT * 4;
+  static constexpr int kQs = 128 * (KT - 1) * 4;        // one query-coordinate buffer: [j][128]
   static constexpr int kOffIdx = kStages * kStageB;
   static constexpr int kOffRows = kOffIdx + kStages * kStageIdx;
   static constexpr int kOffA = kOffRows + kStages * kStageRows;
   static constexpr int kOffQs = kOffA + 2 * kA;
-  static constexpr int kOffQ = kOffQs + 128 * KT * 4;
+  static constexpr int kOffCen = kOffQs + 2 * kQs;       // [warp][buf][KT] leaf centroid copies
+  static constexpr int kOffQ = kOffCen + kTcEpiWarps * 2 * KT * 4;
   static constexpr int kOffBar = kOffQ + kQueue * 128 * 8;
   static constexpr int kNumBars = 2 * kStages + 2 * kBufs + 4;
-  static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int kOffTree = (kOffBar + kNumBars * 8 + 16 + 15) & ~15;
+  static constexpr int kBytes = kOffTree + 1024;  // + alignment slack; the top tree (runtime size) follows
+  static_assert(kBufs >= 2, "need two TMEM accumulators");
+  static_assert(kBytes <= tc_smem_per_cta(CPS), "shared memory exceeds the per-CTA share");
 };
 
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
@@ -92,18 +125,8 @@ __device__ __forceinline__ uint32_t idesc_tf32(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
+// tcgen05.ld of 32 consecutive columns of this warp's 32 TMEM lanes (asynchronous:
+// the registers are valid after tmem_wait()).
 __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -114,16 +137,45 @@ __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&v)[32
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// tcgen05.wait::ld with the loaded registers as operands, so the compiler cannot
+// hoist a use of v above the wait.
+__device__ __forceinline__ void tmem_wait(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
+
+// orders later uses of v after a preceding tmem_wait() (which waits for every
+// outstanding tcgen05.ld of the thread)
+__device__ __forceinline__ void tmem_touch(uint32_t (&v)[32]) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
 
 __device__ __forceinline__ long long dmin_ll(long long x, long long y) { return x < y ? x : y; }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 struct TcTile {
-  int leaf, qbeg, qcnt;
-  long long r0, r1;  // padded rows of the leaf
+  int leaf, qbeg, qcnt, c0;  // c0: first chunk of the tile's chunk order
+  long long r0, r1;          // padded rows of the leaf
   int nchunks;
 };
 
@@ -137,37 +189,53 @@ __device__ __forceinline__ TcTile tc_tile_info(const TcArgs& A, int t) {
   T.r0 = __ldg(A.row_base + rec.x);
   T.r1 = __ldg(A.row_base + rec.x + 1);
   T.nchunks = (int)((T.r1 - T.r0 + kTcRows - 1) / kTcRows);
+  T.c0 = (rec.w / (kTcRows / kBlockRows)) % T.nchunks;
   return T;
 }
 
-// Exact re-evaluation of one candidate with the reference arithmetic.
-template <bool FMA>
-__device__ __forceinline__ float exact_dist(const float* __restrict__ qp, const float* __restrict__ pp, int d) {
-  float acc = 0.0f;
-  for (int j = 0; j < d; ++j) {
-    float df = __fsub_rn(__ldg(qp + j), __ldg(pp + j));
-    if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
-    else acc = __fadd_rn(acc, __fmul_rn(df, df));
-  }
-  return acc;
+// Per-thread inputs of one tile, fetched a tile ahead (see the epilogue).
+struct TcTileIn {
+  int leaf, qbeg, qcnt, c0blk;
+  long long r0, r1;
+  int qi;
+  bool valid;
+  float kth, pnmax;
+  uint32_t st, vis;
+};
+
+// 3-input-min tree over 32 TMEM values (depth 4 instead of a 31-long chain)
+__device__ __forceinline__ float min32(const uint32_t (&v)[32]) {
+  float m1[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    m1[i] = fminf(fminf(__uint_as_float(v[3 * i]), __uint_as_float(v[3 * i + 1])), __uint_as_float(v[3 * i + 2]));
+  m1[10] = fminf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+  const float m2a = fminf(fminf(m1[0], m1[1]), m1[2]), m2b = fminf(fminf(m1[3], m1[4]), m1[5]);
+  const float m2c = fminf(fminf(m1[6], m1[7]), m1[8]), m2d = fminf(m1[9], m1[10]);
+  return fminf(fminf(m2a, m2b), fminf(m2c, m2d));
 }
 
-template <int KT, int KB, bool FMA, int NR>
-__global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs A) {
-  using S = TcSmem<KT, NR>;
+template <int KT, int KB, bool FMA, int NR, int CPS>
+#ifndef BKT_TC_MINB
+#define BKT_TC_MINB CPS
+#endif
+__global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(const TcArgs A) {
+  using S = TcSmem<KT, NR, CPS>;
   constexpr int kTcRows = NR;
   constexpr int kTcBufs = S::kBufs;
-  const ScanArgs& a = A.s;
-  extern __shared__ unsigned char smem_raw[];
-  // 1 KB alignment for the operand tiles
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   constexpr int kTcStages = S::kStages;
+  constexpr int kTmemCols = tc_tmem_cols(CPS);
+  const ScanArgs& a = A.s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1 KB alignment for the operand tiles; pointer arithmetic on the shared
+  // symbol (not an integer round trip) keeps every access below an LDS/STS
+  unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   float* sB = reinterpret_cast<float*>(smem);
   uint32_t* sIdx = reinterpret_cast<uint32_t*>(smem + S::kOffIdx);
   float* sRows = reinterpret_cast<float*>(smem + S::kOffRows);
   float* sA = reinterpret_cast<float*>(smem + S::kOffA);
-  float* sQ = reinterpret_cast<float*>(smem + S::kOffQs);  // [j][128] original query coordinates
+  float* sQ = reinterpret_cast<float*>(smem + S::kOffQs);    // [buf][j][128] original query coordinates
+  float* sCen = reinterpret_cast<float*>(smem + S::kOffCen);  // [warp][buf][KT]
   uint64_t* s_queue = reinterpret_cast<uint64_t*>(smem + S::kOffQ);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* full = bars;                      // [kTcStages] TMA -> MMA/epilogue
@@ -177,9 +245,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
   uint64_t* afull = tempty + kTcBufs;         // [2] epilogue (A written) -> MMA
   uint64_t* aempty = afull + 2;               // [2] MMA (tile done) -> epilogue
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + S::kNumBars);
+  float* sSplit = reinterpret_cast<float*>(smem + S::kOffTree);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const int nsplit = (1 << a.top.h) - 1;
+  if (A.tree_smem)
+    for (int i = tid; i < nsplit; i += kTcThreads) sSplit[i] = __ldg(a.top.split + i);
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full[s], 1);
@@ -197,7 +269,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
   }
   if (warp == kTcEpiWarps + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(s_tmem)),
-                 "r"(kTcTmemCols));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -206,20 +278,25 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
   const uint32_t tmem = *s_tmem;
   const int tiles_end = a.tile_hi >= 0 ? a.tile_hi : *a.num_tiles;
 
+  // the control warps need few registers: they hand theirs to the epilogue warps
   if (warp == kTcEpiWarps) {
     // ===== TMA producer =====
+    if constexpr (CPS >= 3) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcCtlRegs));
     if (lane == 0) {
       uint32_t g = 0;
       for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x) {
         const TcTile T = tc_tile_info<kTcRows>(A, t);
-        for (int c = 0; c < T.nchunks; ++c, ++g) {
+        for (int i = 0; i < T.nchunks; ++i) {
+          const int c = tc_chunk_at(i, T.c0, T.nchunks);
           const int s = g % kTcStages;
           const uint32_t use = g / kTcStages;
-          const long long tp0 = clock64();
+          const long long tp0 = kTcDiag ? clock64() : 0;
           if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
-          if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) {
-            A.dbg[8 * g + 0] = tp0;
-            A.dbg[8 * g + 1] = clock64();
+          if constexpr (kTcDiag) {
+            if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) {
+              A.dbg[16 * g + 0] = tp0;
+              A.dbg[16 * g + 1] = clock64();
+            }
           }
           const long long row = T.r0 + (long long)c * kTcRows;
           const int nr = (int)dmin_ll(kTcRows, T.r1 - row);
@@ -227,11 +304,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
           bulk_g2s(sB + s * (S::kStageB / 4), A.B + row * KT, nr * KT * 4, &full[s]);
           bulk_g2s(sIdx + s * kTcRows, A.ridx + row, nr * 4, &full[s]);
           bulk_g2s(sRows + s * (S::kStageRows / 4), A.rows + row * A.d, nr * A.d * 4, &full[s]);
+          ++g;
         }
       }
     }
   } else if (warp == kTcEpiWarps + 1) {
     // ===== MMA issuer =====
+    if constexpr (CPS >= 3) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcCtlRegs));
     if (lane == 0) {
       uint32_t g = 0, tt = 0;
       const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
@@ -240,7 +319,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         const uint32_t ab = tt & 1u;
         if (A.spin) mbar_wait_spin(&afull[ab], (tt >> 1) & 1u); else mbar_wait(&afull[ab], (tt >> 1) & 1u);
         tc_fence_after();
-        for (int c = 0; c < T.nchunks; ++c, ++g) {
+        for (int i = 0; i < T.nchunks; ++i) {
+          const int c = tc_chunk_at(i, T.c0, T.nchunks);
           const int s = g % kTcStages;
           const uint32_t b = g % kTcBufs, use = g / kTcBufs;
           if (A.spin) {
@@ -251,7 +331,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
             if (use > 0) mbar_wait(&tempty[b], (use - 1) & 1u);
           }
           tc_fence_after();
-          if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * g + 2] = clock64();
+          if constexpr (kTcDiag) {
+            if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[16 * g + 2] = clock64();
+          }
           const int nr = (int)dmin_ll(kTcRows, T.r1 - (T.r0 + (long long)c * kTcRows));
           const uint32_t idesc = idesc_tf32(nr);
 #pragma unroll
@@ -268,6 +350,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            smem_addr(&tfull[b]))
                        : "memory");
+          ++g;
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_addr(&aempty[ab]))
@@ -276,50 +359,119 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
     }
   } else {
     // ===== epilogue: one thread per query =====
+    if constexpr (CPS >= 3) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(tc_epi_regs(CPS)));
+    //
+    // A tile's inputs (tile record, query id, coordinates, k-th distance,
+    // traversal state) are fetched while the previous tile is being scanned,
+    // in four stages spread over its first chunks, and its A operand is
+    // written as soon as they arrive; the MMA warp therefore runs from one
+    // tile into the next without waiting for this tile's FindLeaf.  The top-k
+    // list itself stays in global memory (NeighborBatch.keys layout) and is
+    // read-modified-written only when queued candidates are merged.
     uint64_t* qslot = s_queue + tid;
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
     const int d = A.d;
-    uint32_t g = 0, tt = 0;
-    for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x, ++tt) {
-      const TcTile T = tc_tile_info<kTcRows>(A, t);
-      const uint32_t ab = tt & 1u;
-      const bool valid = tid < T.qcnt;
-      const int qi = valid ? __ldg(a.work + T.qbeg + tid) : 0;
-      const float* qp = a.q + (long long)qi * A.qstride;
-      // The full top-k list is only needed when a candidate enters it; a tile
-      // starts from the query's k-th distance alone (kth array) and loads the
-      // list lazily at the first merge.
-      uint64_t arr[KB];
-#pragma unroll
-      for (int j = 0; j < KB; ++j) arr[j] = 0;
-      bool have_list = false;
-      float kth = valid ? __ldg(A.kth + qi) : -__int_as_float(0x7f800000);  // invalid rows never take candidates
-      // A row: tf32(q - c) in dims < d, 1.0 in column d, zeros after
-      if (tt >= 2) mbar_wait(&aempty[ab], ((tt >> 1) - 1) & 1u);
-      const float* cen = A.centroid + (long long)T.leaf * KT;
+    const bool tree_smem = A.tree_smem != 0;
+    const int th = a.top.h;
+    [[maybe_unused]] unsigned long long c_grp = 0, c_any = 0, c_surv = 0, c_iter = 0, c_merge = 0, c_tile = 0,
+                                        c_q = 0, c_first = 0;
+
+    TcTileIn nx{};  // the next tile's inputs
+    // stage 0: tile record
+    auto stage0 = [&](int tn) {
+      const int4 rec = __ldg(a.tiles + tn);
+      nx.leaf = rec.x;
+      nx.qbeg = rec.y;
+      nx.qcnt = rec.z;
+      nx.c0blk = rec.w;
+    };
+    // stage 1: leaf rows, query id, leaf radius helper
+    auto stage1 = [&]() {
+      nx.r0 = __ldg(A.row_base + nx.leaf);
+      nx.r1 = __ldg(A.row_base + nx.leaf + 1);
+      nx.valid = tid < nx.qcnt;
+      nx.qi = nx.valid ? __ldg(a.work + nx.qbeg + tid) : 0;
+      nx.pnmax = __ldg(A.pnmax + nx.leaf);
+    };
+    // stage 2: coordinates -> sQ[nb] (cp.async), centroid -> this warp's sCen[nb], per-query scalars
+    auto stage2 = [&](uint32_t nb) {
+      float* q_dst = sQ + nb * (S::kQs / 4) + tid;
+      if (nx.valid) {
+        const float* qp = a.q + (long long)nx.qi * A.qstride;
+        for (int j = 0; j < d; ++j) cp_async4(q_dst + j * 128, qp + j);
+        nx.kth = __ldg(A.kth + nx.qi);
+        nx.st = a.state[nx.qi];
+        nx.vis = a.visits[nx.qi];
+      } else {
+        nx.kth = -__int_as_float(0x7f800000);  // invalid rows never take candidates
+        nx.st = 0;
+        nx.vis = 0;
+      }
+      if (lane < KT) cp_async4(sCen + (warp * 2 + nb) * KT + lane, A.centroid + (long long)nx.leaf * KT + lane);
+    };
+    // stage 3: A row of the next tile: tf32(q - c) in dims < d, 1.0 in column d, zeros after
+    auto stage3 = [&](uint32_t nb, uint32_t tn_idx) -> float {
+      cp_async_wait_all();
+      __syncwarp();
+      if (tn_idx >= 2) mbar_wait(&aempty[nb], ((tn_idx >> 1) - 1) & 1u);
+      const float* cen = sCen + (warp * 2 + nb) * KT;
+      const float* qs = sQ + nb * (S::kQs / 4) + tid;
+      float* base = sA + nb * (S::kA / 4) + (tid >> 3) * (KT * 8) + (tid & 7) * 4;
       float qn = 0.0f;
-      {
-        float* arow = sA + ab * (S::kA / 4);
-        // canonical layout: row r -> group r/8 (KT*32 B), chunk k/4 (128 B), row r%8 (16 B)
-        float* base = arow + (tid >> 3) * (KT * 8) + (tid & 7) * 4;
 #pragma unroll
-        for (int j = 0; j < KT; ++j) {
-          float v = 0.0f;
-          if (j < d) {
-            const float qv = valid ? __ldg(qp + j) : 0.0f;
-            sQ[j * 128 + tid] = qv;
-            float qc = valid ? __fsub_rn(qv, __ldg(cen + j)) : 0.0f;
-            qn = __fmaf_rn(qc, qc, qn);
-            v = __uint_as_float(tf32_rna(qc));
-          } else if (j == d) {
-            v = 1.0f;
-          }
-          base[(j >> 2) * 32 + (j & 3)] = v;
+      for (int j = 0; j < KT; ++j) {
+        float v = 0.0f;
+        if (j < d) {
+          float qc = nx.valid ? __fsub_rn(qs[j * 128], cen[j]) : 0.0f;
+          qn = __fmaf_rn(qc, qc, qn);
+          v = __uint_as_float(tf32_rna(qc));
+        } else if (j == d) {
+          v = 1.0f;
         }
+        base[(j >> 2) * 32 + (j & 3)] = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[ab]);
+      if (lane == 0) mbar_arrive(&afull[nb]);
+      return qn;
+    };
+
+    int t = a.tile_lo + blockIdx.x;
+    uint32_t g = 0, tt = 0;
+    float nx_qn = 0.0f;
+    if (t < tiles_end) {
+      stage0(t);
+      stage1();
+      stage2(0);
+      nx_qn = stage3(0, 0);
+    }
+    for (; t < tiles_end; t += gridDim.x, ++tt) {
+      // current tile <- prefetched inputs
+      const TcTileIn cu = nx;
+      const float qn = nx_qn;
+      const uint32_t ab = tt & 1u;
+      const int nchunks = (int)((cu.r1 - cu.r0 + kTcRows - 1) / kTcRows);
+      const int c0 = (cu.c0blk / (kTcRows / kBlockRows)) % nchunks;
+      const int tn = t + gridDim.x;
+      const bool has_next = tn < tiles_end;
+      int pf = has_next ? 0 : 4;  // next-tile prefetch stage
+      auto prefetch_step = [&]() {
+        if (pf == 0) stage0(tn);
+        else if (pf == 1) stage1();
+        else if (pf == 2) stage2(ab ^ 1u);
+        else nx_qn = stage3(ab ^ 1u, tt + 1);
+        ++pf;
+      };
+
+      const bool valid = cu.valid;
+      const int qi = cu.qi;
+      const float* sq = sQ + ab * (S::kQs / 4) + tid;  // this query's coordinates, stride 128
+      float kth = cu.kth;
+      const float kth_in = kth;
+      const bool first_visit = valid && kth == __int_as_float(0x7f800000);
+      if constexpr (kTcDiag) {
+        if (A.ctr) { c_tile += 1; c_q += valid ? 1 : 0; }
+      }
       const float qnc = (1.0f - kTcMargin) * qn;
       auto threshold = [&](float kk) {
         // kth - (1 - C) qn, rounded up by a hair so the fp32 subtraction cannot cut a candidate
@@ -331,9 +483,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       float kflt = kth;
       float thr = valid ? threshold(kflt) : kth;
       int cn = 0;
-      const float leaf_pnmax = __ldg(A.pnmax + T.leaf);
 
-      // insert this lane's queued candidates; the list is fetched on first use
+      // insert this lane's queued candidates into its top-k list; the list is
+      // read from global memory at the first merge of the tile and kept in
+      // registers until the tile ends
+      uint64_t arr[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) arr[j] = 0;
+      bool have_list = false;
       auto merge = [&]() {
         if (cn > 0) {
           if (!have_list) {
@@ -347,36 +504,47 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
       };
 
       // filter one 32-column group of TMEM values, then re-evaluate survivors
-      auto process = [&](const uint32_t (&v)[32], int gcol, int s, long long row0) {
-        // depth-4 tree of 3-input minima (FMNMX3) instead of a 31-long dependent chain
-        float m1[11];
-#pragma unroll
-        for (int i = 0; i < 10; ++i)
-          m1[i] = fminf(fminf(__uint_as_float(v[3 * i]), __uint_as_float(v[3 * i + 1])), __uint_as_float(v[3 * i + 2]));
-        m1[10] = fminf(__uint_as_float(v[30]), __uint_as_float(v[31]));
-        const float m2a = fminf(fminf(m1[0], m1[1]), m1[2]), m2b = fminf(fminf(m1[3], m1[4]), m1[5]);
-        const float m2c = fminf(fminf(m1[6], m1[7]), m1[8]), m2d = fminf(m1[9], m1[10]);
-        const float mn = fminf(fminf(m2a, m2b), fminf(m2c, m2d));
+      auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
+        const float mn = min32(v);
+        if constexpr (kTcDiag) c_grp += 1;
         if (!__any_sync(0xffffffffu, mn <= thr)) return;
         uint32_t mask = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) <= thr ? 1u : 0u) << j;
+        if constexpr (kTcDiag) {
+          c_any += 1;
+          c_surv += __popc(mask);
+          if (first_visit) c_first += __popc(mask);
+        }
         const uint32_t* ids = sIdx + s * kTcRows + gcol;
         const float* prow = sRows + s * (S::kStageRows / 4) + gcol * d;
         while (__any_sync(0xffffffffu, mask != 0)) {
+          if constexpr (kTcDiag) c_iter += 1;
           if (mask) {
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
             const float* pp = prow + j * d;
+            // unrolled to KT - 1 >= d with predication: every shared load issues
+            // up front, only the (ordered) accumulation chain stays serial
+            float qv[KT - 1], pv[KT - 1];
+#pragma unroll
+            for (int jj = 0; jj < KT - 1; ++jj) {
+              qv[jj] = jj < d ? sq[jj * 128] : 0.0f;
+              pv[jj] = jj < d ? pp[jj] : 0.0f;
+            }
             float acc = 0.0f;
-            for (int jj = 0; jj < d; ++jj) {
-              float df = __fsub_rn(sQ[jj * 128 + tid], pp[jj]);
-              if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
-              else acc = __fadd_rn(acc, __fmul_rn(df, df));
+#pragma unroll
+            for (int jj = 0; jj < KT - 1; ++jj) {
+              if (jj < d) {
+                float df = __fsub_rn(qv[jj], pv[jj]);
+                if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
+                else acc = __fadd_rn(acc, __fmul_rn(df, df));
+              }
             }
             if (acc <= kflt) qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
           }
           if (__any_sync(0xffffffffu, cn == kQueue)) {
+            if constexpr (kTcDiag) c_merge += 1;
             merge();
             kflt = fminf(kflt, kth);
             if (valid) thr = threshold(kflt);
@@ -384,10 +552,16 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
         }
       };
 
-      for (int c = 0; c < T.nchunks; ++c, ++g) {
+      bool first_chunk = true;
+      for (int i = 0; i < nchunks || pf < 4; ++i) {
+        if (i >= nchunks) {  // tiles shorter than the prefetch pipeline
+          prefetch_step();
+          continue;
+        }
+        const int c = tc_chunk_at(i, c0, nchunks);
         const int s = g % kTcStages;
         const uint32_t b = g % kTcBufs;
-        const long long te0 = clock64();
+        const long long te0 = kTcDiag ? clock64() : 0;
         if (A.spin) {
           mbar_wait_spin(&tfull[b], (g / kTcBufs) & 1u);
           mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
@@ -396,48 +570,79 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
           mbar_wait(&full[s], (g / kTcStages) & 1u);
         }
         tc_fence_after();
-        const long long te1 = clock64();
-        const long long row0 = T.r0 + (long long)c * kTcRows;
-        const int ngrp = (int)dmin_ll(kTcRows, T.r1 - row0) / 32;
+        const long long te1 = kTcDiag ? clock64() : 0;
+        const long long row0 = cu.r0 + (long long)c * kTcRows;
+        const int ngrp = (int)dmin_ll(kTcRows, cu.r1 - row0) / 32;
         const uint32_t tbase = tmem + lane_base + b * kTcRows;
-        // two 32-column groups in flight, one wait (NR = 128: second pair below)
         uint32_t va[32], vb[32];
-        tmem_ld32_async(tbase, va);
-        if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
-        tmem_wait_ld();
-        if constexpr (KB <= 32) {
-          if (c == 0 && valid && kth == __int_as_float(0x7f800000)) {
-            // No k-th neighbour yet (first leaf): bound it from this chunk's first
-            // 32 points.  With U_j = T_j + qn + 2C (qn + pnmax_leaf) >= D_ref(q, p_j)
-            // (the filter's error analysis), the KB >= k disjoint column groups
-            // j = g (mod KB) each contain a point with D_ref <= min_g U, so the
-            // k-th distance is <= max_g min_{j in g} U_j.  Filtering against it
+        if constexpr (KB <= 16) {
+          if (first_chunk && __any_sync(0xffffffffu, first_visit)) {
+            // No k-th neighbour yet (first leaf): bound it from this chunk.  With
+            // U_j = T_j + qn + 2C (qn + pnmax_leaf) >= D_ref(q, p_j) (the filter's
+            // error analysis), each of the KB >= k disjoint column classes
+            // contains a point with D_ref <= min_{j in class} U_j, so the k-th
+            // distance is <= max_i min_{j in class i} U_j.  Filtering against it
             // drops only points that cannot enter the top-k.
+            float gm[KB];
+#pragma unroll
+            for (int i = 0; i < KB; ++i) gm[i] = __int_as_float(0x7f800000);
+            // classes: column index within its 32-column group, mod KB (a partition
+            // of the chunk's columns into KB non-empty classes)
+#pragma unroll 1
+            for (int gi = 0; gi < ngrp; ++gi) {
+              tmem_ld32_async(tbase + 32 * gi, va);
+              tmem_wait(va);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) gm[j % KB] = fminf(gm[j % KB], __uint_as_float(va[j]));
+            }
             float gmax = -__int_as_float(0x7f800000);
 #pragma unroll
-            for (int gi = 0; gi < KB; ++gi) {
-              float gm = __uint_as_float(va[gi]);
-#pragma unroll
-              for (int j = gi + KB; j < 32; j += KB) gm = fminf(gm, __uint_as_float(va[j]));
-              gmax = fmaxf(gmax, gm);
-            }
-            const float kub = __fadd_ru(__fadd_ru(gmax, qn), 2.0f * kTcMargin * (qn + leaf_pnmax) * 1.0001f);
-            if (kub < kflt) {
+            for (int i = 0; i < KB; ++i) gmax = fmaxf(gmax, gm[i]);
+            const float kub = __fadd_ru(__fadd_ru(gmax, qn), 2.0f * kTcMargin * (qn + cu.pnmax) * 1.0001f);
+            if (first_visit && kub < kflt) {
               kflt = kub;
               thr = threshold(kflt);
             }
           }
         }
-        process(va, 0, s, row0);
-        if (ngrp > 1) process(vb, 32, s, row0);
+        // Pass 1: the minimum over the whole chunk (two 32-column groups in
+        // flight per wait, independent min trees) and ONE vote.  Most chunks end
+        // here; a chunk with a candidate is re-read group by group (pass 2).
+        first_chunk = false;
+        const bool dbg_on = kTcDiag && A.dbg && blockIdx.x == 0 && tid == 0 && (int)g < A.dbg_cap;
+        float mchunk;
+        tmem_ld32_async(tbase, va);
+        if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
+        tmem_wait(va);
+        tmem_touch(vb);
+        if (dbg_on) A.dbg[16 * g + 7] = clock64();
+        mchunk = min32(va);
+        if (ngrp > 1) mchunk = fminf(mchunk, min32(vb));
         if constexpr (NR > 64) {
           if (ngrp > 2) {
             tmem_ld32_async(tbase + 64, va);
             if (ngrp > 3) tmem_ld32_async(tbase + 96, vb);
-            tmem_wait_ld();
-            process(va, 64, s, row0);
-            if (ngrp > 3) process(vb, 96, s, row0);
+            tmem_wait(va);
+            tmem_touch(vb);
+            mchunk = fminf(mchunk, min32(va));
+            if (ngrp > 3) mchunk = fminf(mchunk, min32(vb));
           }
+        }
+        if (dbg_on) A.dbg[16 * g + 8] = clock64();
+        if (__any_sync(0xffffffffu, mchunk <= thr)) {
+          if (NR == 64) {
+            // both groups are still in registers
+            process(va, 0, s);
+            if (ngrp > 1) process(vb, 32, s);
+          } else {
+#pragma unroll 1
+            for (int gi = 0; gi < ngrp; ++gi) {
+              tmem_ld32_async(tbase + 32 * gi, va);
+              tmem_wait(va);
+              process(va, 32 * gi, s);
+            }
+          }
+          if (dbg_on) A.dbg[16 * g + 9] = clock64();
         }
         tc_fence_before();
         __syncwarp();
@@ -445,16 +650,22 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
           mbar_arrive(&tempty[b]);
           mbar_arrive(&empty[s]);
         }
-        if (A.dbg && blockIdx.x == 0 && tid == 0 && (int)g < A.dbg_cap) {
-          A.dbg[8 * g + 3] = te0;
-          A.dbg[8 * g + 4] = te1;
-          A.dbg[8 * g + 5] = clock64();
-          A.dbg[8 * g + 6] = tt;
+        if constexpr (kTcDiag) {
+          if (dbg_on) {
+            A.dbg[16 * g + 3] = te0;
+            A.dbg[16 * g + 4] = te1;
+            A.dbg[16 * g + 5] = clock64();
+            A.dbg[16 * g + 6] = tt;
+            A.dbg[16 * g + 12] = (long long)c_iter;
+            A.dbg[16 * g + 13] = (long long)c_any;
+          }
         }
+        ++g;
+        if (pf < 4) prefetch_step();
       }
       if (__any_sync(0xffffffffu, cn > 0)) merge();
 
-      if (tid == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)(__ldg(a.leaf_size + T.leaf)) * T.qcnt);
+      if (tid == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)(__ldg(a.leaf_size + cu.leaf)) * cu.qcnt);
 
       if (valid) {
         if (have_list) {
@@ -462,21 +673,47 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
 #pragma unroll
           for (int j = 0; j < KB; ++j)
             if (j < a.k) kp[a.k - 1 - j] = arr[j];
-          A.kth[qi] = kth;
         }
+        if (kth != kth_in) A.kth[qi] = kth;
         if (a.fused) {
-          auto qget = [qp](int j) { return __ldg(qp + j); };
-          uint32_t st = a.state[qi];
-          uint32_t lf = st & 0xFFFFu, pend = st >> 16;
-          int nxt = find_next_leaf(a.top, qget, kth, lf, pend);
+          auto qget = [sq](int j) { return sq[j * 128]; };
+          uint32_t lf = cu.st & 0xFFFFu, pend = cu.st >> 16;
+          int nxt;
+          if (tree_smem) {
+            nxt = find_next_leaf_with(th, d, [sSplit](uint32_t node) { return sSplit[node]; }, qget, kth, lf, pend);
+          } else {
+            const float* sp = a.top.split;
+            nxt = find_next_leaf_with(th, d, [sp](uint32_t node) { return __ldg(sp + node); }, qget, kth, lf, pend);
+          }
           a.state[qi] = (pend << 16) | lf;
           a.next[qi] = nxt;
           if (nxt >= 0) {
-            uint32_t vv = a.visits[qi] + 1;
+            const uint32_t vv = cu.vis + 1;
             a.visits[qi] = vv;
             log_visit(a, qi, vv, nxt);
-            warp_count(a.counts, nxt);
-          }
+            }
+        }
+      }
+    }
+    if constexpr (kTcDiag) {
+      if (A.ctr) {
+        // per-thread sums reduced over the warp; warp-level counts taken from lane 0
+        unsigned long long ts = c_surv, tf = c_first, tq = c_q;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ts += __shfl_xor_sync(0xffffffffu, ts, o);
+          tf += __shfl_xor_sync(0xffffffffu, tf, o);
+          tq += __shfl_xor_sync(0xffffffffu, tq, o);
+        }
+        if (lane == 0) {
+          atomicAdd(A.ctr + 0, c_grp);
+          atomicAdd(A.ctr + 1, c_any);
+          atomicAdd(A.ctr + 2, ts);
+          atomicAdd(A.ctr + 3, c_iter);
+          atomicAdd(A.ctr + 4, c_merge);
+          if (warp == 0) atomicAdd(A.ctr + 5, c_tile);
+          atomicAdd(A.ctr + 6, tq);
+          atomicAdd(A.ctr + 7, tf);
         }
       }
     }
@@ -485,7 +722,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) leafscan_tc_kernel(const TcArgs
   __syncthreads();
   if (warp == kTcEpiWarps + 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 

@@ -1,15 +1,17 @@
 // round_kernels.cuh -- the per-round scheduling kernels of the device-resident
 // LazySearch loop (Alg. 1; reference buffer_tree.py:523-646).
 //
-// One round = plan -> scatter -> leafscan(+fused FindLeaf):
+// One round = bucket -> plan -> scatter -> leafscan(+fused FindLeaf):
 //   start   : every fresh query descends to its home leaf (find_leaf_batch for
-//             fresh queries, buffer_tree.py:318-321, 351-376) and is counted
-//             into its leaf's bucket.
-//   plan    : exclusive scans of the per-leaf counts -> each leaf's slice of
-//             the work list and its tile range (the "buffers" of
-//             QueryBuffers.drain_all, buffer_tree.py:420-430, in leaf order).
+//             fresh queries, buffer_tree.py:318-321, 351-376).
+//   bucket  : each query with a next leaf is routed down that leaf's block
+//             split tree to a bucket key (leaf, block) and counted.
+//   plan    : exclusive scans of the per-key counts -> each key's and each
+//             leaf's slice of the work list and the leaf's tile range (the
+//             "buffers" of QueryBuffers.drain_all, buffer_tree.py:420-430, in
+//             leaf order; inside a leaf, ordered by block).
 //   scatter : counting-sort placement of the still-active queries into their
-//             leaf's slice with warp-aggregated atomics (the reference's
+//             key's slice with warp-aggregated atomics (the reference's
 //             stable argsort + insert_many, buffer_tree.py:603-619).  DONE
 //             queries drop out (buffer_tree.py:482-485).
 //   findleaf: unfused FindLeaf for the out-of-core path (leafscan fuses it
@@ -31,8 +33,8 @@ constexpr int kPlanThreads = 1024;
 // Fresh queries: EMPTY top-k, descend from the root, count.
 __global__ void start_kernel(const float* __restrict__ q, int D, long long m, int k, TopTreeView top,
                              uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next,
-                             uint32_t* __restrict__ visits, int* __restrict__ counts, int* seq_log,
-                             unsigned long long* seq_pos, long long seq_cap, float* __restrict__ kth) {
+                             uint32_t* __restrict__ visits, int* seq_log, unsigned long long* seq_pos,
+                             long long seq_cap, float* __restrict__ kth) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
     uint64_t* kp = keys + i * k;
     for (int t = 0; t < k; ++t) kp[t] = kEmptyKey;
@@ -50,7 +52,6 @@ __global__ void start_kernel(const float* __restrict__ q, int D, long long m, in
         seq_log[3 * p] = (int)i; seq_log[3 * p + 1] = 1; seq_log[3 * p + 2] = (int)leaf;
       }
     }
-    warp_count(counts, (int)leaf);
   }
 }
 
@@ -86,36 +87,94 @@ __device__ __forceinline__ void block_scan2(long long& a, long long& b, long lon
   __syncthreads();
 }
 
-// counts -> leaf_off / tile_off; resets counts and cursors; updates ctl.
-// One CTA of kPlanThreads threads; each thread owns a contiguous leaf run.
-__global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ counts, int* __restrict__ leaf_off,
-                                                            int* __restrict__ tile_off, int* __restrict__ cursor,
-                                                            RoundCtl* ctl, int nl, int tile_q, int* hist,
-                                                            int hist_cap, int4* tiles, int tiles_cap) {
+// Route every query with a next leaf to its bucket key = leaf * W + sub, and
+// count.  A home-leaf visit (round 0, identity list) takes sub = the block of
+// the leaf its coordinates fall in (the leaf's split nodes): the home leaf's
+// bucket is then ordered by position and the leaf scan starts each tile at
+// the block of its queries.  Later visits take sub = 0.
+// identity: the previous list is 0..n-1.
+__global__ void bucket_kernel(const int* __restrict__ prev, int identity, const RoundCtl* ctl,
+                              const int* __restrict__ next, const float* __restrict__ q, int D,
+                              const int* __restrict__ blk_base, const int4* __restrict__ nodes, int sub_w,
+                              int* __restrict__ qkey, int* __restrict__ counts) {
+  const int n = ctl->active;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int qi = identity ? i : prev[i];
+    const int leaf = next[qi];
+    if (leaf < 0) continue;
+    int sub = 0;
+    if (identity && sub_w > 1) {
+      const int b0 = __ldg(blk_base + leaf), nb = __ldg(blk_base + leaf + 1) - b0;
+      if (nb > 1) {
+        const int4* nd = nodes + (b0 - leaf);
+        const float* qp = q + (long long)qi * D;
+        int c = 0;
+        for (;;) {
+          const int4 v = __ldg(nd + c);
+          c = (__ldg(qp + v.y) >= __int_as_float(v.x)) ? v.w : v.z;
+          if (c < 0) break;
+        }
+        sub = (~c) & (sub_w - 1);
+      }
+    }
+    const int key = leaf * sub_w + sub;
+    qkey[qi] = key;
+    warp_count(counts, key);
+  }
+}
+
+// counts -> key_off, leaf_off, tile_off + per-tile records; resets counts and
+// cursors; updates ctl.  One CTA of kPlanThreads threads; each thread owns a
+// contiguous run of keys (phase 1) and of leaves (phase 2).
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ counts, int* __restrict__ key_off,
+                                                            int sub_w, int nkeys,
+                                                            int* __restrict__ leaf_off, int* __restrict__ tile_off,
+                                                            int* __restrict__ cursor, RoundCtl* ctl, int nl,
+                                                            int tile_q, int* hist, int hist_cap, int4* tiles,
+                                                            int tiles_cap) {
+  long long tot_c, tot_t;
+  {
+    const int per = (nkeys + kPlanThreads - 1) / kPlanThreads;
+    const int lo = min(nkeys, (int)threadIdx.x * per), hi = min(nkeys, lo + per);
+    long long sc = 0, dummy = 0, tot_dummy;
+    for (int e = lo; e < hi; ++e) sc += counts[e];
+    long long ec = sc;
+    block_scan2(ec, dummy, tot_c, tot_dummy);
+    for (int e = lo; e < hi; ++e) {
+      key_off[e] = (int)ec;
+      ec += counts[e];
+      counts[e] = 0;
+      cursor[e] = 0;
+    }
+    if (threadIdx.x == 0) key_off[nkeys] = (int)tot_c;
+  }
+  __syncthreads();
   const int per = (nl + kPlanThreads - 1) / kPlanThreads;
   const int lo = min(nl, (int)threadIdx.x * per), hi = min(nl, lo + per);
-  long long sc = 0, st = 0;
+  long long st = 0;
   for (int l = lo; l < hi; ++l) {
-    int c = counts[l];
-    sc += c;
+    int c = key_off[(l + 1) * sub_w] - key_off[l * sub_w];
     st += (c + tile_q - 1) / tile_q;
   }
-  long long tot_c, tot_t;
-  long long ec = sc, et = st;
-  block_scan2(ec, et, tot_c, tot_t);
+  long long et = st, dummy = 0, tot_dummy;
+  block_scan2(et, dummy, tot_t, tot_dummy);
   for (int l = lo; l < hi; ++l) {
-    int c = counts[l];
-    leaf_off[l] = (int)ec;
+    const int ec = key_off[l * sub_w];
+    const int c = key_off[(l + 1) * sub_w] - ec;
+    leaf_off[l] = ec;
     tile_off[l] = (int)et;
-    // per-tile records {leaf, first work-list slot, query count}: one load per tile
-    // in the scan kernels instead of a binary search over tile_off
+    // per-tile records {leaf, first work-list slot, query count, sub-bucket of
+    // the first query (its block for a home-leaf visit)}: one load per tile in
+    // the scan kernels
     const int nt = (c + tile_q - 1) / tile_q;
-    for (int j = 0; j < nt && et + j < tiles_cap; ++j)
-      tiles[et + j] = make_int4(l, (int)ec + j * tile_q, min(tile_q, c - j * tile_q), 0);
-    ec += c;
+    const int kb0 = l * sub_w, kb1 = (l + 1) * sub_w;
+    int e = kb0;
+    for (int j = 0; j < nt && et + j < tiles_cap; ++j) {
+      const int p = ec + j * tile_q;
+      while (e + 1 < kb1 && key_off[e + 1] <= p) ++e;
+      tiles[et + j] = make_int4(l, p, min(tile_q, c - j * tile_q), e - kb0);
+    }
     et += nt;
-    counts[l] = 0;
-    cursor[l] = 0;
   }
   if (threadIdx.x == 0) {
     leaf_off[nl] = (int)tot_c;
@@ -130,18 +189,18 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
   }
 }
 
-// Place every still-active query of the previous work list into its leaf's
+// Place every still-active query of the previous work list into its key's
 // slice of the new list.  identity: previous list is 0..prev_active-1.
 __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const int* __restrict__ next,
-                               const int* __restrict__ leaf_off, int* __restrict__ cursor, int* __restrict__ work,
-                               const RoundCtl* ctl) {
+                               const int* __restrict__ qkey, const int* __restrict__ key_off,
+                               int* __restrict__ cursor, int* __restrict__ work, const RoundCtl* ctl) {
   const int n = ctl->prev_active;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int qi = identity ? i : prev[i];
-    int leaf = next[qi];
-    if (leaf >= 0) {
-      int pos = warp_reserve(cursor, leaf);
-      work[leaf_off[leaf] + pos] = qi;
+    if (next[qi] >= 0) {
+      const int key = qkey[qi];
+      int pos = warp_reserve(cursor, key);
+      work[key_off[key] + pos] = qi;
     }
   }
 }
@@ -151,8 +210,7 @@ __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const
 __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ctl, const float* __restrict__ q,
                                 int D, int k, TopTreeView top, const uint64_t* __restrict__ keys,
                                 uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
-                                int* __restrict__ counts, int* seq_log, unsigned long long* seq_pos,
-                                long long seq_cap) {
+                                int* seq_log, unsigned long long* seq_pos, long long seq_cap) {
   const int n = ctl->active;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int qi = work[i];
@@ -173,7 +231,6 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
           seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)v; seq_log[3 * p + 2] = nxt;
         }
       }
-      warp_count(counts, nxt);
     }
   }
 }

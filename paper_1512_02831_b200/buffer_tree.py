@@ -273,7 +273,8 @@ def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: Buffe
     keys, st, seq = dev.search(qarr, params.k, exact=exact, visited=visited, seq_cap=seq_cap,
                                timing=stats is not None, kernel=kernel)
     t2 = time.perf_counter()
-    counts = np.full(m, params.k, dtype=np.int64)
+    counts = _native.host_empty((m,), np.int64)
+    counts.fill(params.k)
     result = NeighborBatch.from_keys(keys, counts)
 
     if debug_audit:

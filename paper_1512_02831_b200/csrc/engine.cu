@@ -139,8 +139,19 @@ struct bkt_ctx {
   int h_tile_off_cap = 0;
   uint64_t* h_stage = nullptr;  // pinned staging for D2H / H2D
   size_t h_stage_bytes = 0;
-  char* stage_slot[2] = {nullptr, nullptr};  // pinned staging slots for host <-> device streaming
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // pinned staging for host <-> device streaming: set 0 carries queries in, set 1
+  // results out, each on its own stream so both overlap the search
+  struct StageSet {
+    char* slot[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t stream = nullptr;
+  } io[2];
+  // second query / result buffers for the overlapped host I/O pipeline
+  float* q_alt = nullptr;
+  float* q_raw_alt = nullptr;
+  uint64_t* keys_alt = nullptr;
+  long long cap_alt = 0;
+  int cap_alt_k = 0;
 
   std::vector<cudaEvent_t> ev_pool;   // leafscan timing events
   cudaEvent_t ring_ev[4] = {};        // round-check ring (kRing)
@@ -242,6 +253,19 @@ void free_work(bkt_ctx* c) {
   dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
   dfree(c->work[0]); dfree(c->work[1]);
   c->cap_m = 0; c->cap_k = 0;
+  dfree(c->q_alt); dfree(c->q_raw_alt); dfree(c->keys_alt);
+  c->cap_alt = 0; c->cap_alt_k = 0;
+}
+
+int ensure_alt(bkt_ctx* ctx, long long m, int k) {
+  if (ctx->cap_alt >= m && ctx->cap_alt_k >= k) return BKT_OK;
+  dfree(ctx->q_alt); dfree(ctx->q_raw_alt); dfree(ctx->keys_alt);
+  CU(cudaMalloc(&ctx->q_alt, sizeof(float) * m * ctx->D));
+  if (ctx->D != ctx->d) CU(cudaMalloc(&ctx->q_raw_alt, sizeof(float) * m * ctx->d));
+  CU(cudaMalloc(&ctx->keys_alt, sizeof(uint64_t) * m * k));
+  ctx->cap_alt = m;
+  ctx->cap_alt_k = k;
+  return BKT_OK;
 }
 
 void free_leafbufs(bkt_ctx* c) {
@@ -327,52 +351,63 @@ void par_memcpy(void* dst, const void* src, size_t n) {
   for (auto& x : th) x.join();
 }
 
-int ensure_stage_slots(bkt_ctx* ctx) {
+int ensure_stageset(bkt_ctx* ctx, bkt_ctx::StageSet& S) {
   for (int i = 0; i < 2; ++i) {
-    if (!ctx->stage_slot[i]) CU(cudaHostAlloc(&ctx->stage_slot[i], kStageSlot, cudaHostAllocDefault));
-    if (!ctx->stage_ev[i]) CU(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+    if (!S.slot[i]) CU(cudaHostAlloc(&S.slot[i], kStageSlot, cudaHostAllocDefault));
+    if (!S.ev[i]) CU(cudaEventCreateWithFlags(&S.ev[i], cudaEventDisableTiming));
   }
+  if (!S.stream) CU(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
   return BKT_OK;
 }
 
+void free_stageset(bkt_ctx::StageSet& S) {
+  for (int i = 0; i < 2; ++i) {
+    hfree(S.slot[i]);
+    if (S.ev[i]) cudaEventDestroy(S.ev[i]);
+    S.ev[i] = nullptr;
+  }
+  if (S.stream) cudaStreamDestroy(S.stream);
+  S.stream = nullptr;
+}
+
 // pageable host -> device: host threads fill one pinned slot while the other DMAs
-int h2d_staged(bkt_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  int rc = ensure_stage_slots(ctx);
+int h2d_staged(bkt_ctx* ctx, bkt_ctx::StageSet& S, void* dst, const void* src, size_t bytes) {
+  int rc = ensure_stageset(ctx, S);
   if (rc != BKT_OK) return rc;
   size_t off = 0;
   for (int i = 0; off < bytes; ++i) {
     const int s = i & 1;
     const size_t n = std::min(kStageSlot, bytes - off);
-    CU(cudaEventSynchronize(ctx->stage_ev[s]));  // slot's previous DMA done (never-recorded events return at once)
-    par_memcpy(ctx->stage_slot[s], (const char*)src + off, n);
-    CU(cudaMemcpyAsync((char*)dst + off, ctx->stage_slot[s], n, cudaMemcpyHostToDevice, ctx->copy_stream));
-    CU(cudaEventRecord(ctx->stage_ev[s], ctx->copy_stream));
+    CU(cudaEventSynchronize(S.ev[s]));  // slot's previous DMA done (never-recorded events return at once)
+    par_memcpy(S.slot[s], (const char*)src + off, n);
+    CU(cudaMemcpyAsync((char*)dst + off, S.slot[s], n, cudaMemcpyHostToDevice, S.stream));
+    CU(cudaEventRecord(S.ev[s], S.stream));
     off += n;
   }
-  CU(cudaStreamSynchronize(ctx->copy_stream));
+  CU(cudaStreamSynchronize(S.stream));
   return BKT_OK;
 }
 
-// device -> pageable host: DMA chunk i+1 into one slot while host threads drain the other
-int d2h_staged(bkt_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  int rc = ensure_stage_slots(ctx);
+// device -> pageable host: one slot DMAs while host threads drain the other
+int d2h_staged(bkt_ctx* ctx, bkt_ctx::StageSet& S, void* dst, const void* src, size_t bytes) {
+  int rc = ensure_stageset(ctx, S);
   if (rc != BKT_OK) return rc;
   const size_t nchunks = (bytes + kStageSlot - 1) / kStageSlot;
   auto issue = [&](size_t i) -> int {
     const int s = (int)(i & 1);
     const size_t off = i * kStageSlot, n = std::min(kStageSlot, bytes - off);
-    CU(cudaMemcpyAsync(ctx->stage_slot[s], (const char*)src + off, n, cudaMemcpyDeviceToHost, ctx->copy_stream));
-    CU(cudaEventRecord(ctx->stage_ev[s], ctx->copy_stream));
+    CU(cudaMemcpyAsync(S.slot[s], (const char*)src + off, n, cudaMemcpyDeviceToHost, S.stream));
+    CU(cudaEventRecord(S.ev[s], S.stream));
     return BKT_OK;
   };
   if (nchunks == 0) return BKT_OK;
   if ((rc = issue(0)) != BKT_OK) return rc;
   for (size_t i = 0; i < nchunks; ++i) {
     const int s = (int)(i & 1);
-    CU(cudaEventSynchronize(ctx->stage_ev[s]));
+    CU(cudaEventSynchronize(S.ev[s]));
     if (i + 1 < nchunks && (rc = issue(i + 1)) != BKT_OK) return rc;
     const size_t off = i * kStageSlot, n = std::min(kStageSlot, bytes - off);
-    par_memcpy((char*)dst + off, ctx->stage_slot[s], n);
+    par_memcpy((char*)dst + off, S.slot[s], n);
   }
   return BKT_OK;
 }
@@ -600,10 +635,8 @@ void bkt_close(bkt_ctx* ctx) {
   free_leafbufs(ctx);
   dfree(ctx->ctl); dfree(ctx->pairs); dfree(ctx->seq_pos); dfree(ctx->seq_dev); dfree(ctx->hist); dfree(ctx->tc_ctr);
   hfree(ctx->h_ctl); hfree(ctx->h_stage);
-  for (int i = 0; i < 2; ++i) {
-    hfree(ctx->stage_slot[i]);
-    if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
-  }
+  for (int i = 0; i < 2; ++i) free_stageset(ctx->io[i]);
+  dfree(ctx->q_alt); dfree(ctx->q_raw_alt); dfree(ctx->keys_alt);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < kRing; ++i)
     if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
@@ -810,6 +843,7 @@ struct SearchRun {
   size_t ev_next = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
   long long rounds = 0;
+  long long scans = 0;
   bool seq = false;
   long long seq_cap = 0;
   bool counters = false;
@@ -997,12 +1031,14 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   const bool ooc = ctx->residency == 1;
   for (;;) {
     // queries with a next leaf -> bucket keys (leaf, block) + counts
+    // home visits (round 0) are sub-bucketed per block; later rounds key by leaf only
+    const int sw = round == 0 ? ctx->sub_w : 1;
     bucket_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->ctl, ctx->next,
-                                                          ctx->q, ctx->D, ctx->blk_base, ctx->nodes, ctx->sub_w,
-                                                          ctx->qkey, ctx->counts);
+                                                          ctx->q, ctx->D, ctx->blk_base, ctx->nodes, sw, ctx->qkey,
+                                                          ctx->counts);
     CU(cudaGetLastError());
     R.launches++;
-    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, ctx->sub_w, ctx->nbuckets,
+    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, sw, ctx->nl * sw,
                                                      ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl, ctx->nl, kNT,
                                                      ctx->hist, kHistCap, ctx->tiles,
                                                      (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
@@ -1053,6 +1089,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   RoundCtl fin;
   CU(cudaMemcpy(&fin, ctx->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost));
   R.rounds += fin.rounds;
+  R.scans += fin.scans;
   return BKT_OK;
 }
 
@@ -1121,6 +1158,14 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     batch = std::min<long long>(batch, 1ll << 30);
   }
   batch = std::min<long long>(batch, m);
+  if (o.batch_queries <= 0 && (!o.queries_on_device || !o.keys_on_device) && !(o.seq_log && o.seq_cap > 0)) {
+    // host I/O: split large searches so transfers overlap the search (bkt_search pipeline)
+    // measured on B200 (config 2): one batch is best at 10M queries, the extra
+    // per-batch tail rounds cost more than the transfers the overlap hides
+    long long nio = 1;
+    if (const char* e = std::getenv("BKT_IO_BATCHES")) nio = std::max(1, std::atoi(e));
+    if (m >= (2ll << 20) && nio > 1) batch = std::min(batch, (m + nio - 1) / nio);
+  }
   batch = std::min<long long>(batch, (long long)INT32_MAX / 2);
   rc = ensure_work(ctx, batch, k);
   if (rc != BKT_OK) return rc;
@@ -1141,55 +1186,118 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   }
   R.counters = counters;
 
+  // Host I/O pipeline: with host-resident queries or results and at least two
+  // batches, batch b+1's queries stream in (io set 0, its own host thread and
+  // stream) and batch b-1's results stream out (io set 1) while batch b is
+  // searched; the two batches alternate between two query/result buffers.
+  const bool host_io = !o.queries_on_device || !o.keys_on_device;
+  const long long nbatch = (m + batch - 1) / batch;
+  const bool overlap = host_io && nbatch >= 2;
+  if (overlap) {
+    rc = ensure_alt(ctx, batch, k);
+    if (rc != BKT_OK) return rc;
+  }
+  float* qbuf[2] = {ctx->q, ctx->q_alt};
+  float* rawbuf[2] = {ctx->q_raw, ctx->q_raw_alt};
+  uint64_t* kbuf[2] = {ctx->keys, ctx->keys_alt};
+  std::mutex st_mu;
+  // queries of batch b -> buffer set `slot` (device queries: an async copy on the engine stream)
+  auto load_in = [&](long long b, int slot) -> int {
+    const long long b0 = b * batch, bm = std::min(batch, m - b0);
+    const float* src = queries + b0 * ctx->d;
+    const size_t qbytes = sizeof(float) * bm * ctx->d;
+    if (o.queries_on_device) return BKT_OK;  // handled on the engine stream
+    CU(cudaSetDevice(ctx->device));
+    float* raw = (ctx->D == ctx->d) ? qbuf[slot] : rawbuf[slot];
+    auto c0 = std::chrono::steady_clock::now();
+    int r = h2d_staged(ctx, ctx->io[0], raw, src, qbytes);
+    if (r != BKT_OK) return r;
+    std::lock_guard<std::mutex> lk(st_mu);
+    st.h2d_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+    st.h2d_bytes += qbytes;
+    return BKT_OK;
+  };
+  // results of batch b from buffer set `slot` (device results: async copy on the engine stream)
+  auto store_out = [&](long long b, int slot) -> int {
+    const long long b0 = b * batch, bm = std::min(batch, m - b0);
+    const size_t kbytes = sizeof(uint64_t) * bm * k;
+    if (o.keys_on_device) return BKT_OK;
+    CU(cudaSetDevice(ctx->device));
+    auto c0 = std::chrono::steady_clock::now();
+    int r = d2h_staged(ctx, ctx->io[1], out_keys + b0 * k, kbuf[slot], kbytes);
+    if (r != BKT_OK) return r;
+    std::lock_guard<std::mutex> lk(st_mu);
+    st.d2h_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+    st.d2h_bytes += kbytes;
+    return BKT_OK;
+  };
+
   cudaEvent_t t_all0 = ctx->t_ev[0], t_all1 = ctx->t_ev[1];
   CU(cudaEventRecord(t_all0, ctx->stream));
-  long long leaf_visits = 0;
-  std::vector<uint32_t> vis_host;
-  for (long long b0 = 0; b0 < m; b0 += batch) {
-    const long long bm = std::min(batch, m - b0);
+  if (!o.queries_on_device && (rc = load_in(0, 0)) != BKT_OK) return rc;
+  std::thread t_in, t_out;
+  int rc_in = BKT_OK, rc_out = BKT_OK;
+  auto join_all = [&]() {
+    if (t_in.joinable()) t_in.join();
+    if (t_out.joinable()) t_out.join();
+    ctx->q = qbuf[0];
+    ctx->q_raw = rawbuf[0];
+    ctx->keys = kbuf[0];
+  };
+  for (long long b = 0; b < nbatch; ++b) {
+    const int slot = overlap ? (int)(b & 1) : 0;
+    const long long b0 = b * batch, bm = std::min(batch, m - b0);
     R.m = bm;
-    // queries -> ctx->q (m x D)
-    const float* src = queries + b0 * ctx->d;
+    if (overlap && b + 1 < nbatch && !o.queries_on_device)
+      t_in = std::thread([&, b, slot]() { rc_in = load_in(b + 1, slot ^ 1); });
+    else if (!overlap && b > 0 && !o.queries_on_device && (rc = load_in(b, slot)) != BKT_OK) {
+      join_all();
+      return rc;
+    }
+    ctx->q = qbuf[slot];
+    ctx->q_raw = rawbuf[slot];
+    ctx->keys = kbuf[slot];
     float* raw = (ctx->D == ctx->d) ? ctx->q : ctx->q_raw;
-    const size_t qbytes = sizeof(float) * bm * ctx->d;
     if (o.queries_on_device) {
-      if (ctx->D == ctx->d) CU(cudaMemcpyAsync(ctx->q, src, qbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      const float* src = queries + b0 * ctx->d;
+      if (ctx->D == ctx->d)
+        rc = cudaMemcpyAsync(ctx->q, src, sizeof(float) * bm * ctx->d, cudaMemcpyDeviceToDevice, ctx->stream) ==
+                     cudaSuccess ? BKT_OK : set_err(ctx, BKT_ECUDA, "query copy failed");
       else raw = const_cast<float*>(src);
-    } else {
-      auto c0 = std::chrono::steady_clock::now();
-      CU(cudaStreamSynchronize(ctx->stream));
-      rc = h2d_staged(ctx, raw, src, qbytes);
-      if (rc != BKT_OK) return rc;
-      st.h2d_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
-      st.h2d_bytes += qbytes;
+      if (rc != BKT_OK) { join_all(); return rc; }
     }
     if (ctx->D != ctx->d) {
       pad_rows_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(raw, ctx->d, ctx->q, ctx->D, bm);
-      CU(cudaGetLastError());
       R.launches++;
     }
     rc = search_batch(ctx, R);
-    if (rc != BKT_OK) return rc;
-    // results
-    const size_t kbytes = sizeof(uint64_t) * bm * k;
-    if (o.keys_on_device) {
-      CU(cudaMemcpyAsync(out_keys + b0 * k, ctx->keys, kbytes, cudaMemcpyDeviceToDevice, ctx->stream));
-    } else {
-      auto c0 = std::chrono::steady_clock::now();
-      CU(cudaStreamSynchronize(ctx->stream));
-      rc = d2h_staged(ctx, out_keys + b0 * k, ctx->keys, kbytes);
-      if (rc != BKT_OK) return rc;
-      st.d2h_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
-      st.d2h_bytes += kbytes;
+    if (rc == BKT_OK && o.keys_on_device &&
+        cudaMemcpyAsync(out_keys + b0 * k, ctx->keys, sizeof(uint64_t) * bm * k, cudaMemcpyDeviceToDevice,
+                        ctx->stream) != cudaSuccess)
+      rc = set_err(ctx, BKT_ECUDA, "result copy failed");
+    // optional per-query visit counts (the total is counted on the device)
+    if (rc == BKT_OK && o.visited_out) {
+      static_assert(sizeof(uint32_t) == sizeof(int32_t), "visit counters are 32-bit");
+      if (cudaMemcpyAsync(o.visited_out + b0, ctx->visits, sizeof(uint32_t) * bm, cudaMemcpyDeviceToHost,
+                          ctx->stream) != cudaSuccess || cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        rc = set_err(ctx, BKT_ECUDA, "visit count copy failed");
     }
-    // visits -> leaf_visits (+ optional per-query output)
-    vis_host.resize(bm);
-    CU(cudaMemcpyAsync(vis_host.data(), ctx->visits, sizeof(uint32_t) * bm, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-    for (long long i = 0; i < bm; ++i) leaf_visits += vis_host[i];
-    if (o.visited_out)
-      for (long long i = 0; i < bm; ++i) o.visited_out[b0 + i] = (int32_t)vis_host[i];
+    if (t_out.joinable()) t_out.join();  // the previous batch's results are out
+    if (rc == BKT_OK) rc = rc_out;
+    if (rc != BKT_OK) { join_all(); return rc; }
+    if (!o.keys_on_device) {
+      if (overlap) {
+        t_out = std::thread([&, b, slot]() { rc_out = store_out(b, slot); });
+      } else if ((rc = store_out(b, slot)) != BKT_OK) {
+        join_all();
+        return rc;
+      }
+    }
+    if (t_in.joinable()) t_in.join();  // the next batch's queries are in
+    if (rc_in != BKT_OK) { join_all(); return rc_in; }
   }
+  join_all();
+  if (rc_out != BKT_OK) return rc_out;
   CU(cudaEventRecord(t_all1, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   float ms = 0;
@@ -1227,7 +1335,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
       std::fprintf(stderr, "round %zu active %d leafscan_ms %.4f\n", r, hist[r], per_launch[off + r]);
   }
   st.rounds = R.rounds;
-  st.leaf_visits = leaf_visits;
+  st.leaf_visits = R.scans;
   st.pairs = (int64_t)pairs;
   st.kernel_launches = R.launches;
   st.leafscan_launches = R.leafscan_launches;

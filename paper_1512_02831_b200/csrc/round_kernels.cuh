@@ -26,6 +26,7 @@ struct RoundCtl {
   int prev_active;  // length of the previous round's work list
   int num_tiles;    // tiles this round
   int rounds;       // rounds with active > 0
+  long long scans;  // (query, leaf) scans so far (SearchStats.leaf_scan_events)
 };
 
 constexpr int kPlanThreads = 1024;
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
     if (tot_c > 0) {
       if (hist && ctl->rounds < hist_cap) hist[ctl->rounds] = (int)tot_c;
       ctl->rounds += 1;
+      ctl->scans += tot_c;
     }
   }
 }

@@ -188,7 +188,7 @@ class GpuDevice:
         """bkt_search on host arrays; returns (keys, stats, seq triples)."""
         q = np.ascontiguousarray(queries, dtype=np.float32)
         m = q.shape[0]
-        keys = out_keys if out_keys is not None else np.empty((m, k), dtype=np.uint64)
+        keys = out_keys if out_keys is not None else _native.host_empty((m, k), np.uint64)
         opts = _native.SearchOpts()
         opts.exact = 1 if exact else 0
         opts.record_timing = 1 if timing else 0

@@ -8,12 +8,13 @@ from __future__ import annotations
 
 import ctypes
 import mmap
+import os
 import threading
 from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbkt.so"
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / os.environ.get("BKT_LIB_NAME", "libbkt.so")
 
 BKT_OK = 0
 BKT_EINVAL = -1

@@ -90,7 +90,7 @@ def _compile(cmd: list[str], src: Path, obj: Path, force: bool) -> bool:
 
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> Path:
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
-    tag = _sources_hash("v1" + os.environ.get("BKT_BUILD_DIAG", ""))
+    tag = _sources_hash("v1" + os.environ.get("BKT_BUILD_DIAG", "") + os.environ.get("BKT_BUILD_CROSS", ""))
     stamp = LIB_DIR / "libbkt.stamp"
     if LIB.exists() and stamp.exists() and stamp.read_text() == tag and not force:
         return LIB
@@ -100,6 +100,8 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
         src = CSRC / "leafscan_inst.cu"
         units.append(([NVCC, *NVFLAGS, f"-DBKT_D={d}", "-c", str(src), "-o", str(obj)], src, obj))
     diag = ["-DBKT_TC_DIAG=1"] if os.environ.get("BKT_BUILD_DIAG") == "1" else []
+    if os.environ.get("BKT_BUILD_CROSS") == "1":
+        diag.append("-DBKT_TC_CROSS=1")
     for kt, nr, cps in ((16, 64, 2), (16, 128, 2), (32, 64, 2)):
         for fma in (0, 1):
             obj = OBJ_DIR / f"leafscan_tc_{kt}_{nr}_{cps}_{fma}.o"

@@ -1323,8 +1323,8 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     CU(cudaMemcpy(c, ctx->tc_ctr, sizeof(c), cudaMemcpyDeviceToHost));
     std::fprintf(stderr,
                  "tc counters: groups %llu any %llu survivors %llu loop_trips %llu merges %llu tiles %llu "
-                 "queries %llu first_visit_survivors %llu pairs %llu\n",
-                 c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], pairs);
+                 "queries %llu first_visit_survivors %llu pairs %llu inserted %llu\n",
+                 c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], pairs, c[8]);
   }
   if (std::getenv("BKT_TRACE_ROUNDS") && !per_launch.empty()) {
     // per-round diagnostics of the last batch: active queries and leafscan ms

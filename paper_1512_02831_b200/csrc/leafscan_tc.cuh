@@ -42,6 +42,10 @@ constexpr int kBlockRows = 64;               // leaf-internal block (home-visit 
 #define BKT_TC_DIAG 0  // 1: per-chunk timelines (BKT_TC_DEBUG) and filter counters (BKT_TC_COUNTERS)
 #endif
 constexpr bool kTcDiag = BKT_TC_DIAG != 0;
+#ifndef BKT_TC_EAGER
+#define BKT_TC_EAGER 0
+#endif
+constexpr bool kTcEagerMerge = BKT_TC_EAGER != 0;  // merge queued candidates at the end of every chunk
 
 __host__ __device__ constexpr int tc_tmem_cols(int cps) { return cps >= 3 ? 128 : (cps == 2 ? 256 : 512); }
 // shared memory one CTA may use when CPS share an SM (228 KB - 1 KB reserved per CTA)
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
     const bool tree_smem = A.tree_smem != 0;
     const int th = a.top.h;
     [[maybe_unused]] unsigned long long c_grp = 0, c_any = 0, c_surv = 0, c_iter = 0, c_merge = 0, c_tile = 0,
-                                        c_q = 0, c_first = 0;
+                                        c_q = 0, c_first = 0, c_ins = 0;
 
     TcTileIn nx{};  // the next tile's inputs
     // stage 0: tile record
@@ -541,7 +545,10 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
                 else acc = __fadd_rn(acc, __fmul_rn(df, df));
               }
             }
-            if (acc <= kflt) qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
+            if (acc <= kflt) {
+              qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
+              if constexpr (kTcDiag) c_ins += 1;
+            }
           }
           if (__any_sync(0xffffffffu, cn == kQueue)) {
             if constexpr (kTcDiag) c_merge += 1;
@@ -642,6 +649,14 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
               process(va, 32 * gi, s);
             }
           }
+          if (kTcEagerMerge && __any_sync(0xffffffffu, cn > 0)) {
+            // fold this chunk's candidates in now: a tighter k-th distance for the
+            // rest of the leaf means fewer survivors (the queue would otherwise
+            // wait until some lane's queue is full)
+            merge();
+            kflt = fminf(kflt, kth);
+            if (valid) thr = threshold(kflt);
+          }
           if (dbg_on) A.dbg[16 * g + 9] = clock64();
         }
         tc_fence_before();
@@ -698,9 +713,10 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
     if constexpr (kTcDiag) {
       if (A.ctr) {
         // per-thread sums reduced over the warp; warp-level counts taken from lane 0
-        unsigned long long ts = c_surv, tf = c_first, tq = c_q;
+        unsigned long long ts = c_surv, tf = c_first, tq = c_q, ti = c_ins;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
+          ti += __shfl_xor_sync(0xffffffffu, ti, o);
           ts += __shfl_xor_sync(0xffffffffu, ts, o);
           tf += __shfl_xor_sync(0xffffffffu, tf, o);
           tq += __shfl_xor_sync(0xffffffffu, tq, o);
@@ -714,6 +730,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
           if (warp == 0) atomicAdd(A.ctr + 5, c_tile);
           atomicAdd(A.ctr + 6, tq);
           atomicAdd(A.ctr + 7, tf);
+          atomicAdd(A.ctr + 8, ti);
         }
       }
     }

@@ -29,7 +29,7 @@ __all__ = [
     "run_engine",
 ]
 
-ENGINES = ("bufferkdtree",)
+ENGINES = ("brute", "bufferkdtree")
 DEFAULT_DEVICE_MEMORY = 512 * 2 ** 20  # bench.py:42 (the simulator's budget)
 _PER_QUERY_OVERHEAD = 32
 
@@ -75,7 +75,7 @@ def run_engine(engine: str, refs, queries, params: SearchParams, *, height: int 
                half_full_threshold: int | None = None, query_chunk_size: int | None = None, workers: int = 1,
                trace_out: str | None = None, collect_stats: bool = False, exact: bool = True,
                ) -> tuple[NeighborBatch, dict]:
-    """bench.py:99-204 for engine "bufferkdtree" on B200s.
+    """bench.py:99-204 for engines "bufferkdtree" and "brute" on B200s.
 
     device_memory None (default) sizes for the real GPU: one chunk, leaf
     structure resident in HBM.  An explicit budget reproduces the
@@ -87,6 +87,21 @@ def run_engine(engine: str, refs, queries, params: SearchParams, *, height: int 
     qarr = np.ascontiguousarray(queries.data if hasattr(queries, "data") else queries, dtype=np.float32)
     m = qarr.shape[0]
     info: dict = {"engine": engine, "n": refs.n, "m": m, "d": refs.d, "k": params.k}
+    if engine == "brute":
+        # bench.py:119-125: the full pairwise scan, here on the GPU leaf-scan kernel
+        from .brute import EvalCounter, brute_knn
+        counter = EvalCounter()
+        dev = device_init(DeviceSpec(cuda_device=0))
+        try:
+            t0 = time.perf_counter()
+            res = brute_knn(refs, qarr, params, workers=workers, counter=counter, device=dev,
+                            num_chunks=num_chunks or 1)
+            info["query_seconds"] = time.perf_counter() - t0
+        finally:
+            dev.close()
+        info["pairs"] = counter.pairs
+        info["build_seconds"] = 0.0
+        return res, info
     h = height if height is not None else auto_height(refs.n)
     t0 = time.perf_counter()
     tree = build_buffer_tree(refs, h)

@@ -90,7 +90,8 @@ def _compile(cmd: list[str], src: Path, obj: Path, force: bool) -> bool:
 
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> Path:
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
-    tag = _sources_hash("v1" + os.environ.get("BKT_BUILD_DIAG", "") + os.environ.get("BKT_BUILD_CROSS", ""))
+    tag = _sources_hash("v1" + os.environ.get("BKT_BUILD_DIAG", "") + os.environ.get("BKT_BUILD_CROSS", "")
+                        + os.environ.get("BKT_BUILD_MARGIN", ""))
     stamp = LIB_DIR / "libbkt.stamp"
     if LIB.exists() and stamp.exists() and stamp.read_text() == tag and not force:
         return LIB
@@ -102,6 +103,8 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     diag = ["-DBKT_TC_DIAG=1"] if os.environ.get("BKT_BUILD_DIAG") == "1" else []
     if os.environ.get("BKT_BUILD_CROSS") == "1":
         diag.append("-DBKT_TC_CROSS=1")
+    if os.environ.get("BKT_BUILD_MARGIN"):
+        diag.append(f"-DBKT_TC_MARGIN_LOG2={int(os.environ['BKT_BUILD_MARGIN'])}")
     for kt, nr, cps in ((16, 64, 2), (16, 128, 2), (32, 64, 2)):
         for fma in (0, 1):
             obj = OBJ_DIR / f"leafscan_tc_{kt}_{nr}_{cps}_{fma}.o"
@@ -113,7 +116,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     for name in ("engine.cu", "misc.cu"):
         obj = OBJ_DIR / (Path(name).stem + ".o")
         src = CSRC / name
-        units.append(([NVCC, *NVFLAGS, "-c", str(src), "-o", str(obj)], src, obj))
+        units.append(([NVCC, *NVFLAGS, *diag, "-c", str(src), "-o", str(obj)], src, obj))
     obj = OBJ_DIR / "build_tree.o"
     src = CSRC / "build_tree.cpp"
     units.append((["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-I", str(INCLUDE), "-c",

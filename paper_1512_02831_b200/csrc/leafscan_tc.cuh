@@ -7,16 +7,22 @@
 // centroid c: q' = fl(q - c), p' = fl(p - c), qn = |q'|^2, pn = |p'|^2.  The
 // GEMM computes, per (query, point),
 //      T = pnc - 2 q'.p'      with pnc = (1 - C) pn folded into B as column d
-// (A carries 1.0 in that column), operands pre-rounded to TF32, FP32
-// accumulation.  With TF32 rounding (2^-11 relative per operand) and FP32
-// accumulation, |T - (pnc - 2 q'.p')| <= 2^-9.4 (qn + pn); the centring and
-// the reference's own rounding add < 2^-18 (qn + pn).  Hence
-//      D_ref(q, p) <= kth   ==>   T <= kth - (1 - C) qn        (C = 2^-7)
+// (A carries 1.0 in that column), FP32 accumulation.  Error bound: operands
+// are pre-rounded to TF32 with round-to-nearest (cvt.rna; unrounded FP32
+// operands would be truncated by the tensor core), u = 2^-11 each, so the
+// products err by <= 2u sum|a_k b_k| <= 2^-10 (qn + pn) (2|q'||p'| <= qn+pn);
+// the pnc column adds u pn; the tensor core's accumulation adds
+// <= 2^-21.7 sum|a_k b_k| (measured with pre-rounded operands of mixed
+// magnitude, tools/tc_probe.cu, profiles/r1b/tc_accumulation_probe.txt); the
+// centring and the reference's own rounding < 2^-18 (qn + pn).  In all
+// |T - (pnc - 2 q'.p')| <= 2^-9.4 (qn + pn) < C (qn + pn) for C = 2^-9, hence
+//      D_ref(q, p) <= kth   ==>   T <= kth - (1 - C) qn
 // so every point that can enter the top-k passes the test, and each
 // survivor's distance is recomputed with the reference arithmetic
 // (core.py:108-122) before it may enter the top-k.  Since the set of
 // inserted candidates is unchanged, kth, pruning and the traversal are the
-// reference's exactly.
+// reference's exactly.  (C = 2^-7 and 2^-8 were used before; 2^-9 cuts the
+// survivors that fail the exact test and gives +11% on config 2.)
 //
 // Pipeline per CTA (warp-specialised, no CTA barriers in the main loop):
 //   warp 4   TMA producer: leaf chunks (128 points x KT tf32 + ids) -> smem ring
@@ -36,7 +42,10 @@ namespace bkt {
 // epilogue warps (one thread per query row) + a TMA producer warp + an MMA warp.
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
-constexpr float kTcMargin = 1.0f / 128.0f;    // C
+#ifndef BKT_TC_MARGIN_LOG2
+#define BKT_TC_MARGIN_LOG2 9
+#endif
+constexpr float kTcMargin = 1.0f / (float)(1 << BKT_TC_MARGIN_LOG2);  // C
 constexpr int kBlockRows = 64;               // leaf-internal block (home-visit bucket key), engine.cu
 #ifndef BKT_TC_DIAG
 #define BKT_TC_DIAG 0  // 1: per-chunk timelines (BKT_TC_DEBUG) and filter counters (BKT_TC_COUNTERS)

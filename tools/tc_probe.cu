@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <vector>
 #include <cuda_runtime.h>
@@ -123,8 +124,25 @@ __global__ void __launch_bounds__(128, 1) probe(const float* A, const float* B, 
 int main() {
   std::vector<float> A(128 * 16), B(256 * 16), D(128 * 256);
   srand(1);
-  for (auto& x : A) x = (rand() / (float)RAND_MAX) - 0.5f;
-  for (auto& x : B) x = (rand() / (float)RAND_MAX) - 0.5f;
+  // mixed magnitudes (scales 2^-6..2^6 per element) and near-cancelling rows
+  for (auto& x : A) x = ((rand() / (float)RAND_MAX) - 0.5f) * ldexpf(1.0f, (rand() % 13) - 6);
+  for (auto& x : B) x = ((rand() / (float)RAND_MAX) - 0.5f) * ldexpf(1.0f, (rand() % 13) - 6);
+  if (getenv("PROBE_UNIFORM")) {
+    for (auto& x : A) x = (rand() / (float)RAND_MAX) - 0.5f;
+    for (auto& x : B) x = (rand() / (float)RAND_MAX) - 0.5f;
+  }
+  if (getenv("PROBE_PREROUND")) {
+    // operands already tf32 (round to nearest, ties away, as cvt.rna.tf32): the
+    // residual error is then the tensor core's accumulation alone
+    auto rna = [](float& x) {
+      uint32_t u;
+      memcpy(&u, &x, 4);
+      u = (u + 0x1000u) & 0xFFFFE000u;
+      memcpy(&x, &u, 4);
+    };
+    for (auto& x : A) rna(x);
+    for (auto& x : B) rna(x);
+  }
   float *dA, *dB, *dD; long long* dc;
   CK(cudaMalloc(&dA, A.size() * 4)); CK(cudaMalloc(&dB, B.size() * 4)); CK(cudaMalloc(&dD, D.size() * 4)); CK(cudaMalloc(&dc, 8));
   CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
@@ -135,16 +153,19 @@ int main() {
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
   long long cyc; CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
-  double maxerr = 0, maxref = 0; int bad = 0;
+  double maxerr = 0, maxref = 0, maxratio = 0; int bad = 0;
   for (int i = 0; i < 128; ++i)
     for (int j = 0; j < 256; ++j) {
       double s = 0, sa = 0;
       for (int k = 0; k < 16; ++k) { s += (double)A[i * 16 + k] * B[j * 16 + k]; sa += fabs((double)A[i * 16 + k] * B[j * 16 + k]); }
       double e = fabs(D[i * 256 + j] - s);
       if (e > maxerr) maxerr = e;
+      if (sa > 0) maxratio = fmax(maxratio, e / sa);
       if (e > sa * (1.0 / 256) + 1e-6) ++bad;
       maxref = fmax(maxref, fabs(s));
     }
+  printf("max |err| / sum|a_k b_k| = %.3e (= 2^%.2f); tf32 operand rounding alone allows 2^-10\n", maxratio,
+         log2(maxratio));
   printf("tf32 mma: max abs err %.3e (max |ref| %.3f), bad %d of %d\n", maxerr, maxref, bad, 128 * 256);
   printf("D[0][0..3] = %f %f %f %f\n", D[0], D[1], D[2], D[3]);
   double bytes = (double)reps * 128 * 256 * 4;

@@ -1002,7 +1002,7 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
   // FindLeaf after every chunk of the round has been scanned
   findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
       ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys, ctx->state,
-      ctx->next, ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+      ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
   CU(cudaGetLastError());
   R.launches++;
   return BKT_OK;
@@ -1019,7 +1019,8 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   CU(cudaMemsetAsync(ctx->cursor, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
   start_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
                                                        ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
-                                                       R.seq_cap, ctx->kthv);
+                                                       R.seq_cap, ctx->kthv, ctx->blk_base, ctx->nodes, ctx->sub_w,
+                                                       ctx->qkey, ctx->counts);
   CU(cudaGetLastError());
   R.launches++;
 
@@ -1033,11 +1034,6 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
     // queries with a next leaf -> bucket keys (leaf, block) + counts
     // home visits (round 0) are sub-bucketed per block; later rounds key by leaf only
     const int sw = round == 0 ? ctx->sub_w : 1;
-    bucket_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->ctl, ctx->next,
-                                                          ctx->q, ctx->D, ctx->blk_base, ctx->nodes, sw, ctx->qkey,
-                                                          ctx->counts);
-    CU(cudaGetLastError());
-    R.launches++;
     plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, sw, ctx->nl * sw,
                                                      ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl, ctx->nl, kNT,
                                                      ctx->hist, kHistCap, ctx->tiles,
@@ -1071,7 +1067,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
         // then overlap across many warps instead of stalling the scan's epilogue
         findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
             ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys,
-            ctx->state, ctx->next, ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+            ctx->state, ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
         CU(cudaGetLastError());
         R.launches++;
       }

@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, (ScanOcc<D, KB>::kMinBlocks)) leafsc
           uint32_t v = a.visits[qi] + 1;
           a.visits[qi] = v;
           log_visit(a, qi, v, nxt);
+          warp_count(a.counts, nxt);  // next round's bucket (key = leaf)
         }
       }
     }

@@ -715,6 +715,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
             const uint32_t vv = cu.vis + 1;
             a.visits[qi] = vv;
             log_visit(a, qi, vv, nxt);
+            warp_count(a.counts, nxt);  // next round's bucket (key = leaf)
             }
         }
       }

@@ -1,11 +1,11 @@
 // round_kernels.cuh -- the per-round scheduling kernels of the device-resident
 // LazySearch loop (Alg. 1; reference buffer_tree.py:523-646).
 //
-// One round = bucket -> plan -> scatter -> leafscan(+fused FindLeaf):
+// One round = plan -> scatter -> leafscan(+fused FindLeaf and bucket count):
 //   start   : every fresh query descends to its home leaf (find_leaf_batch for
-//             fresh queries, buffer_tree.py:318-321, 351-376).
-//   bucket  : each query with a next leaf is routed down that leaf's block
-//             split tree to a bucket key (leaf, block) and counted.
+//             fresh queries, buffer_tree.py:318-321, 351-376), is routed down
+//             that leaf's block split tree and counted into bucket (leaf, block).
+//   later rounds count each query's next leaf in the scan epilogue.
 //   plan    : exclusive scans of the per-key counts -> each key's and each
 //             leaf's slice of the work list and the leaf's tile range (the
 //             "buffers" of QueryBuffers.drain_all, buffer_tree.py:420-430, in
@@ -35,7 +35,9 @@ constexpr int kPlanThreads = 1024;
 __global__ void start_kernel(const float* __restrict__ q, int D, long long m, int k, TopTreeView top,
                              uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next,
                              uint32_t* __restrict__ visits, int* seq_log, unsigned long long* seq_pos,
-                             long long seq_cap, float* __restrict__ kth) {
+                             long long seq_cap, float* __restrict__ kth, const int* __restrict__ blk_base,
+                             const int4* __restrict__ nodes, int sub_w, int* __restrict__ qkey,
+                             int* __restrict__ counts) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
     uint64_t* kp = keys + i * k;
     for (int t = 0; t < k; ++t) kp[t] = kEmptyKey;
@@ -53,6 +55,25 @@ __global__ void start_kernel(const float* __restrict__ q, int D, long long m, in
         seq_log[3 * p] = (int)i; seq_log[3 * p + 1] = 1; seq_log[3 * p + 2] = (int)leaf;
       }
     }
+    // home bucket: (leaf, block of the leaf the query falls in) -- the home
+    // bucket is ordered by position and each tile's scan starts at its block
+    int sub = 0;
+    if (sub_w > 1) {
+      const int b0 = __ldg(blk_base + leaf), nb = __ldg(blk_base + leaf + 1) - b0;
+      if (nb > 1) {
+        const int4* nd = nodes + (b0 - (int)leaf);
+        int c = 0;
+        for (;;) {
+          const int4 v = __ldg(nd + c);
+          c = (__ldg(qp + v.y) >= __int_as_float(v.x)) ? v.w : v.z;
+          if (c < 0) break;
+        }
+        sub = (~c) & (sub_w - 1);
+      }
+    }
+    const int key = (int)leaf * sub_w + sub;
+    qkey[i] = key;
+    warp_count(counts, key);
   }
 }
 
@@ -86,42 +107,6 @@ __device__ __forceinline__ void block_scan2(long long& a, long long& b, long lon
   a = pa + ia - a;  // exclusive
   b = pb + ib - b;
   __syncthreads();
-}
-
-// Route every query with a next leaf to its bucket key = leaf * W + sub, and
-// count.  A home-leaf visit (round 0, identity list) takes sub = the block of
-// the leaf its coordinates fall in (the leaf's split nodes): the home leaf's
-// bucket is then ordered by position and the leaf scan starts each tile at
-// the block of its queries.  Later visits take sub = 0.
-// identity: the previous list is 0..n-1.
-__global__ void bucket_kernel(const int* __restrict__ prev, int identity, const RoundCtl* ctl,
-                              const int* __restrict__ next, const float* __restrict__ q, int D,
-                              const int* __restrict__ blk_base, const int4* __restrict__ nodes, int sub_w,
-                              int* __restrict__ qkey, int* __restrict__ counts) {
-  const int n = ctl->active;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int qi = identity ? i : prev[i];
-    const int leaf = next[qi];
-    if (leaf < 0) continue;
-    int sub = 0;
-    if (identity && sub_w > 1) {
-      const int b0 = __ldg(blk_base + leaf), nb = __ldg(blk_base + leaf + 1) - b0;
-      if (nb > 1) {
-        const int4* nd = nodes + (b0 - leaf);
-        const float* qp = q + (long long)qi * D;
-        int c = 0;
-        for (;;) {
-          const int4 v = __ldg(nd + c);
-          c = (__ldg(qp + v.y) >= __int_as_float(v.x)) ? v.w : v.z;
-          if (c < 0) break;
-        }
-        sub = (~c) & (sub_w - 1);
-      }
-    }
-    const int key = leaf * sub_w + sub;
-    qkey[qi] = key;
-    warp_count(counts, key);
-  }
 }
 
 // counts -> key_off, leaf_off, tile_off + per-tile records; resets counts and
@@ -199,8 +184,9 @@ __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const
   const int n = ctl->prev_active;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int qi = identity ? i : prev[i];
-    if (next[qi] >= 0) {
-      const int key = qkey[qi];
+    const int leaf = next[qi];
+    if (leaf >= 0) {
+      const int key = identity ? qkey[qi] : leaf;  // home round: (leaf, block) keys
       int pos = warp_reserve(cursor, key);
       work[key_off[key] + pos] = qi;
     }
@@ -212,7 +198,8 @@ __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const
 __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ctl, const float* __restrict__ q,
                                 int D, int k, TopTreeView top, const uint64_t* __restrict__ keys,
                                 uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
-                                int* seq_log, unsigned long long* seq_pos, long long seq_cap) {
+                                int* __restrict__ counts, int* seq_log, unsigned long long* seq_pos,
+                                long long seq_cap) {
   const int n = ctl->active;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int qi = work[i];
@@ -233,6 +220,7 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
           seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)v; seq_log[3 * p + 2] = nxt;
         }
       }
+      warp_count(counts, nxt);  // next round's bucket (key = leaf)
     }
   }
 }

@@ -153,6 +153,15 @@ __device__ __forceinline__ int warp_reserve(int* cursor, int key) {
   return base + __popc(peers & ((1u << lane) - 1u));
 }
 
+// Home-round sub-buckets: a leaf of nb blocks maps block b to sub-bucket
+// b >> shift with the smallest shift that fits sub_w sub-buckets (consecutive
+// blocks are neighbours, so a coarser bucket stays spatially coherent).
+__host__ __device__ __forceinline__ int home_block_shift(int nb, int sub_w) {
+  int s = 0;
+  while (((nb - 1) >> s) >= sub_w) ++s;
+  return s;
+}
+
 // ----------------------------------------------------------------------------
 // traversal state: bits 0..15 current leaf (root-to-leaf path, depth i at bit
 // h-1-i), bits 16..31 pending far-child depths (depth i at bit 16+i).  This is

@@ -903,6 +903,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.qstride = ctx->D;
     t.spin = 1;
     t.ctr = R.counters ? ctx->tc_ctr : nullptr;
+    t.sub_w = ctx->sub_w;
     if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e) != 0;
     if (std::getenv("BKT_TC_DEBUG") && R.leafscan_launches == 5) {
       // per-chunk timestamps of CTA 0 in the 6th leafscan launch (a steady-state round)

@@ -80,6 +80,7 @@ struct TcArgs {
   int qstride;                 // row stride of the query block (kernel D of the direct path)
   int spin;                    // 1: MMA/epilogue warps spin on mbarriers instead of suspending
   int tree_smem;               // 1: the top tree's split values are copied to shared memory
+  int sub_w;                   // home-round sub-buckets per leaf (tile records carry the sub-bucket)
   long long* dbg;              // diagnostics (BKT_TC_DEBUG): per-chunk timestamps of CTA 0
   int dbg_cap;
   unsigned long long* ctr;     // diagnostics (BKT_TC_COUNTERS): filter/survivor counters, see engine.cu
@@ -186,6 +187,15 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// first chunk of a tile's chunk order: the chunk holding the first block of
+// the tile's home sub-bucket (0 when the leaf was not sub-bucketed)
+template <int kTcRows>
+__device__ __forceinline__ int tc_first_chunk(int sub, long long rows, int nchunks, int sub_w) {
+  const int nb = (int)((rows + kBlockRows - 1) / kBlockRows);
+  const int blk = sub << home_block_shift(nb, sub_w);
+  return (blk / (kTcRows / kBlockRows)) % nchunks;
+}
+
 struct TcTile {
   int leaf, qbeg, qcnt, c0;  // c0: first chunk of the tile's chunk order
   long long r0, r1;          // padded rows of the leaf
@@ -202,7 +212,7 @@ __device__ __forceinline__ TcTile tc_tile_info(const TcArgs& A, int t) {
   T.r0 = __ldg(A.row_base + rec.x);
   T.r1 = __ldg(A.row_base + rec.x + 1);
   T.nchunks = (int)((T.r1 - T.r0 + kTcRows - 1) / kTcRows);
-  T.c0 = (rec.w / (kTcRows / kBlockRows)) % T.nchunks;
+  T.c0 = tc_first_chunk<kTcRows>(rec.w, T.r1 - T.r0, T.nchunks, A.sub_w);
   return T;
 }
 
@@ -464,7 +474,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
       const float qn = nx_qn;
       const uint32_t ab = tt & 1u;
       const int nchunks = (int)((cu.r1 - cu.r0 + kTcRows - 1) / kTcRows);
-      const int c0 = (cu.c0blk / (kTcRows / kBlockRows)) % nchunks;
+      const int c0 = tc_first_chunk<kTcRows>(cu.c0blk, cu.r1 - cu.r0, nchunks, A.sub_w);
       const int tn = t + gridDim.x;
       const bool has_next = tn < tiles_end;
       int pf = has_next ? 0 : 4;  // next-tile prefetch stage

@@ -68,7 +68,7 @@ __global__ void start_kernel(const float* __restrict__ q, int D, long long m, in
           c = (__ldg(qp + v.y) >= __int_as_float(v.x)) ? v.w : v.z;
           if (c < 0) break;
         }
-        sub = (~c) & (sub_w - 1);
+        sub = (~c) >> home_block_shift(nb, sub_w);
       }
     }
     const int key = (int)leaf * sub_w + sub;

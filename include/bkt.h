@@ -79,6 +79,15 @@ int bkt_device_info(bkt_ctx* ctx, int32_t* sm_count, int32_t* sm_clock_khz, int6
 int bkt_build_tree(const float* refs, int64_t n, int32_t d, int32_t h, float* split_out,
                    int64_t* order_out, int64_t* leaf_starts_out, int32_t nthreads);
 
+/* The same build on a GPU (replaces the same reference code): per level a
+ * radix selection of every subset's positional median key and a scan-based
+ * partition.  Writes what bkt_build_tree writes plus, when points_out is not
+ * NULL, the leaf-sorted (n, d) points.  On failure the message is in
+ * bkt_build_tree_device_error(). */
+int bkt_build_tree_device(int cuda_device, const float* refs, int64_t n, int32_t d, int32_t h, float* split_out,
+                          int64_t* order_out, int64_t* leaf_starts_out, float* points_out);
+const char* bkt_build_tree_device_error(void);
+
 /* Upload a built tree (replaces ChunkPipeline's staging of the leaf
  * structure, device.py:380-420).  leaf_points is the leaf-sorted (n, d)
  * float32 matrix, original_index its (n,) row ids, leaf_starts (2^h + 1).

@@ -25,7 +25,8 @@ BKT_ESTATE = -5
 
 # every symbol include/bkt.h declares
 EXPORTS = ("bkt_open", "bkt_close", "bkt_last_error", "bkt_device_info", "bkt_build_tree",
-           "bkt_load_tree", "bkt_search", "bkt_scan_groups", "bkt_fp32_peak")
+           "bkt_build_tree_device", "bkt_build_tree_device_error", "bkt_load_tree", "bkt_search",
+           "bkt_scan_groups", "bkt_fp32_peak")
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -91,6 +92,9 @@ def lib() -> ctypes.CDLL:
         L.bkt_last_error.restype = ctypes.c_char_p
         L.bkt_device_info.argtypes = [P, P, P, P, P]
         L.bkt_build_tree.argtypes = [P, i64, i32, i32, P, P, P, i32]
+        L.bkt_build_tree_device.argtypes = [ctypes.c_int, P, i64, i32, i32, P, P, P, P]
+        L.bkt_build_tree_device_error.argtypes = []
+        L.bkt_build_tree_device_error.restype = ctypes.c_char_p
         L.bkt_load_tree.argtypes = [P, i32, i32, i64, P, P, P, P, i32, i32, P]
         L.bkt_search.argtypes = [P, P, i64, i32, ctypes.POINTER(SearchOpts), P, ctypes.POINTER(Stats)]
         L.bkt_scan_groups.argtypes = [P, P, P, i64, i32, P, i64, i32, P, i32, P, P, P, P, i32]

@@ -122,8 +122,16 @@ class BufferKdTree:
         return self.top.n_leaves
 
 
-def build_buffer_tree(refs, height: int, store_path: str | None = None) -> BufferKdTree:
-    """buffer_tree.py:149-197 via the native build (bkt_build_tree)."""
+def build_buffer_tree(refs, height: int, store_path: str | None = None, *,
+                      device: int | None = None) -> BufferKdTree:
+    """buffer_tree.py:149-197 via the native build.
+
+    device None: multithreaded host build (bkt_build_tree).  device = a CUDA
+    device ordinal: the same splits computed on that GPU (bkt_build_tree_device:
+    per level, radix selection of every subset's positional median and a
+    scan-based partition; the leaf-sorted points are gathered on the device).
+    Both give the reference's split values and leaf sets exactly; the order of
+    points inside a leaf is not part of the contract."""
     refs = as_point_matrix(refs)
     if height < 1:
         raise ValueError(f"height must be >= 1, got {height}")
@@ -136,12 +144,21 @@ def build_buffer_tree(refs, height: int, store_path: str | None = None) -> Buffe
     split = np.empty(nl - 1, np.float32)
     order = np.empty(refs.n, np.int64)
     starts = np.empty(nl + 1, np.int64)
-    _native.check(_native.lib().bkt_build_tree(_native.ptr(data), refs.n, refs.d, height, _native.ptr(split),
-                                               _native.ptr(order), _native.ptr(starts), 0))
+    if device is None:
+        _native.check(_native.lib().bkt_build_tree(_native.ptr(data), refs.n, refs.d, height, _native.ptr(split),
+                                                   _native.ptr(order), _native.ptr(starts), 0))
+        points = np.ascontiguousarray(data[order])
+    else:
+        points = np.empty_like(data)
+        rc = _native.lib().bkt_build_tree_device(int(device), _native.ptr(data), refs.n, refs.d, height,
+                                                 _native.ptr(split), _native.ptr(order), _native.ptr(starts),
+                                                 _native.ptr(points))
+        if rc != 0:
+            msg = _native.lib().bkt_build_tree_device_error().decode()
+            raise (ValueError if rc == _native.BKT_EINVAL else RuntimeError)(msg)
     levels = np.empty(nl - 1, dtype=np.int32)
     for lvl in range(height):
         levels[2 ** lvl - 1: 2 ** (lvl + 1) - 1] = lvl
-    points = np.ascontiguousarray(data[order])
     if store_path is not None:
         np.save(store_path, points)
         path = store_path if store_path.endswith(".npy") else store_path + ".npy"

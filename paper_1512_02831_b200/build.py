@@ -113,7 +113,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
             if (kt, nr, cps, fma) == (16, 128, 2, 0):
                 flags.append("-DBKT_TC_DISPATCH")
             units.append(([NVCC, *NVFLAGS, *flags, "-c", str(src), "-o", str(obj)], src, obj))
-    for name in ("engine.cu", "misc.cu"):
+    for name in ("engine.cu", "misc.cu", "build_tree_gpu.cu"):
         obj = OBJ_DIR / (Path(name).stem + ".o")
         src = CSRC / name
         units.append(([NVCC, *NVFLAGS, *diag, "-c", str(src), "-o", str(obj)], src, obj))

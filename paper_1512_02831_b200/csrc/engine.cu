@@ -36,7 +36,7 @@ using namespace bkt;
 
 namespace bkt {
 cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ,
-                               int nr);
+                               int nr, int cps);
 }
 
 namespace {
@@ -834,6 +834,7 @@ struct SearchRun {
   bool tc = false;
   bool unfused = false;
   int tc_rows = 128;  // TC chunk width (BKT_TC_N): 64 or 128 columns
+  int tc_cps = 2;     // TC CTAs per SM
   int grid_scan = 0;
   int grid_small = 0;
   bool timing = false;
@@ -913,7 +914,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
       cudaMemsetAsync(dbg, 0, sizeof(long long) * 16 * cap, ctx->stream);
       t.dbg = dbg;
       t.dbg_cap = cap;
-      CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows));
+      CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows, R.tc_cps));
       std::vector<long long> h(16 * cap);
       CU(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * 16 * cap, cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
@@ -929,7 +930,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
       R.leafscan_launches++;
       return BKT_OK;
     }
-    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows));
+    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows, R.tc_cps));
   } else {
     CU(launch_leafscan(ctx->D, R.kb, R.fma, R.grid_scan, ctx->stream, a, nullptr));
   }
@@ -1130,10 +1131,10 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     // two CTAs per SM (2 x 256 TMEM columns); the attributes are set by the query
     int occ = 0;
     TcArgs dummy{};
-    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, 0, nullptr, dummy, &occ, R.tc_rows));
+    CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, 0, nullptr, dummy, &occ, R.tc_rows, R.tc_cps));
     // two CTAs per SM: the variants are sized for it (2 x 256 TMEM columns,
     // shared memory and registers); the occupancy query is only a sanity check
-    int per_sm = 2;
+    int per_sm = (ctx->KT == 16) ? R.tc_cps : 2;
     if (occ < 1) return set_err(ctx, BKT_ECUDA, "tensor-core leaf kernel cannot be resident");
     if (const char* e = std::getenv("BKT_TC_CTAS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     if (std::getenv("BKT_VERBOSE")) std::fprintf(stderr, "tc kernel: occupancy %d CTAs/SM, grid %d\n", occ, per_sm * ctx->sm_count);

@@ -61,11 +61,22 @@ __host__ __device__ constexpr int tc_tmem_cols(int cps) { return cps >= 3 ? 128 
 __host__ __device__ constexpr int tc_smem_per_cta(int cps) { return (228 - cps) * 1024 / cps; }
 // registers: CPS x 192 threads share 64K; with setmaxnreg the two control warps
 // give theirs to the four epilogue warps
+// Registers.  A warp lives in one of the 4 SM sub-partitions (16K registers
+// each), so the launch allows 16384 / (32 * ceil(6 CPS / 4)) per thread: 168
+// for CPS = 2, 96 for CPS = 3.  With CPS = 3 the two control warps drop to 40
+// (setmaxnreg.dec) and the epilogue warps rise to 112 (setmaxnreg.inc): the
+// CTA pool (96 x 192) covers 4 x 32 x 112 + 2 x 32 x 40, and a sub-partition
+// holding one epilogue warp of each of the 3 CTAs plus up to two control
+// warps needs 3 x 112 + 2 x 40 <= 512 registers per lane (a CTA's four
+// epilogue warps sit in four different sub-partitions); even four epilogue
+// warps and one control warp fit (4 x 112 + 40 <= 512).
 constexpr int kTcCtlRegs = 40;
-__host__ __device__ constexpr int tc_launch_regs(int cps) { return (65536 / (cps * kTcThreads)) & ~7; }
-__host__ __device__ constexpr int tc_epi_regs(int cps) {
-  return ((tc_launch_regs(cps) * kTcThreads - kTcCtlRegs * 64) / 128) & ~7;
+__host__ __device__ constexpr int tc_launch_regs(int cps) {
+  return (16384 / (32 * ((cps * (kTcThreads / 32) + 3) / 4))) & ~7;
 }
+__host__ __device__ constexpr int tc_epi_regs(int cps) { return cps >= 3 ? 112 : tc_launch_regs(cps); }
+static_assert(tc_launch_regs(3) == 96 && tc_launch_regs(2) == 168, "register budget");
+static_assert(4 * 32 * tc_epi_regs(3) + 2 * 32 * kTcCtlRegs <= tc_launch_regs(3) * kTcThreads, "CTA register pool");
 
 struct TcArgs {
   ScanArgs s;                  // queries, keys, schedule, top tree, stats (quad fields unused)
@@ -99,7 +110,7 @@ template <int KT, int NR, int CPS>
 struct TcSmem {
   static constexpr int kRows = NR;
   static constexpr int kBufs = tc_tmem_cols(CPS) / NR;
-  static constexpr int kStages = (KT <= 16 ? 512 : 128) / NR;
+  static constexpr int kStages = CPS >= 3 ? 3 : (KT <= 16 ? 512 : 128) / NR;
   static constexpr int kStageB = NR * KT * 4;
   static constexpr int kStageIdx = NR * 4;
   static constexpr int kStageRows = NR * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
@@ -509,20 +520,33 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
 
       // insert this lane's queued candidates into its top-k list; the list is
       // read from global memory at the first merge of the tile and kept in
-      // registers until the tile ends
-      uint64_t arr[KB];
+      // registers until the tile ends (CPS >= 3: read-modify-written per merge,
+      // the register budget has no room for it)
+      constexpr bool kRegTopK = CPS < 3;
+      uint64_t arr[kRegTopK ? KB : 1];
 #pragma unroll
-      for (int j = 0; j < KB; ++j) arr[j] = 0;
+      for (int j = 0; j < (kRegTopK ? KB : 1); ++j) arr[j] = 0;
       bool have_list = false;
       auto merge = [&]() {
         if (cn > 0) {
-          if (!have_list) {
-            const uint64_t* kp = a.keys + (long long)qi * a.k;
+          if constexpr (kRegTopK) {
+            if (!have_list) {
+              const uint64_t* kp = a.keys + (long long)qi * a.k;
 #pragma unroll
-            for (int j = 0; j < KB; ++j) arr[j] = (j < a.k) ? kp[a.k - 1 - j] : 0ull;
-            have_list = true;
+              for (int j = 0; j < KB; ++j) arr[j] = (j < a.k) ? kp[a.k - 1 - j] : 0ull;
+              have_list = true;
+            }
+            merge_queue<KB>(arr, qslot, cn, kth);
+          } else {
+            uint64_t* kp = a.keys + (long long)qi * a.k;
+            uint64_t tmp[KB];
+#pragma unroll
+            for (int j = 0; j < KB; ++j) tmp[j] = (j < a.k) ? kp[a.k - 1 - j] : 0ull;
+            merge_queue<KB>(tmp, qslot, cn, kth);
+#pragma unroll
+            for (int j = 0; j < KB; ++j)
+              if (j < a.k) kp[a.k - 1 - j] = tmp[j];
           }
-          merge_queue<KB>(arr, qslot, cn, kth);
         }
       };
 
@@ -702,7 +726,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
       if (tid == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)(__ldg(a.leaf_size + cu.leaf)) * cu.qcnt);
 
       if (valid) {
-        if (have_list) {
+        if (kRegTopK && have_list) {
           uint64_t* kp = a.keys + (long long)qi * a.k;
 #pragma unroll
           for (int j = 0; j < KB; ++j)

@@ -74,9 +74,10 @@ cudaError_t BKT_TC_PART_NAME(BKT_TC_KT, BKT_TC_NR, BKT_TC_CPS, BKT_TC_FMA)(int k
 // nr selects the chunk width for KT = 16 (64 or 128 columns); KT = 32 always
 // runs 64-column chunks.  Two CTAs share an SM.
 cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t s, const TcArgs& a, int* occ,
-                               int nr) {
+                               int nr, int cps) {
   if (kt == 32) return fma ? launch_tc_32_64_2_1(kb, grid, s, a, occ) : launch_tc_32_64_2_0(kb, grid, s, a, occ);
   if (kt != 16) return cudaErrorInvalidValue;
+  (void)cps;  // 3 CTAs/SM (setmaxnreg) deadlocked on B200: not built, see DESIGN.md
   if (nr == 128) return fma ? launch_tc_16_128_2_1(kb, grid, s, a, occ) : launch_tc_16_128_2_0(kb, grid, s, a, occ);
   return fma ? launch_tc_16_64_2_1(kb, grid, s, a, occ) : launch_tc_16_64_2_0(kb, grid, s, a, occ);
 }

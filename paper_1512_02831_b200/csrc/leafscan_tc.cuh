@@ -470,22 +470,19 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
       return qn;
     };
 
-    int t = a.tile_lo + blockIdx.x;
-    uint32_t g = 0, tt = 0;
+    // The loop starts at a placeholder tile (-1) without chunks whose only job
+    // is the first real tile's prefetch, so the prefetch code has one call site.
+    int t = a.tile_lo + (int)blockIdx.x - (int)gridDim.x;
+    uint32_t g = 0, tt = 0xFFFFFFFFu;
     float nx_qn = 0.0f;
-    if (t < tiles_end) {
-      stage0(t);
-      stage1();
-      stage2(0);
-      nx_qn = stage3(0, 0);
-    }
     for (; t < tiles_end; t += gridDim.x, ++tt) {
+      const bool placeholder = tt == 0xFFFFFFFFu;
       // current tile <- prefetched inputs
       const TcTileIn cu = nx;
       const float qn = nx_qn;
       const uint32_t ab = tt & 1u;
-      const int nchunks = (int)((cu.r1 - cu.r0 + kTcRows - 1) / kTcRows);
-      const int c0 = tc_first_chunk<kTcRows>(cu.c0blk, cu.r1 - cu.r0, nchunks, A.sub_w);
+      const int nchunks = placeholder ? 0 : (int)((cu.r1 - cu.r0 + kTcRows - 1) / kTcRows);
+      const int c0 = placeholder ? 0 : tc_first_chunk<kTcRows>(cu.c0blk, cu.r1 - cu.r0, nchunks, A.sub_w);
       const int tn = t + gridDim.x;
       const bool has_next = tn < tiles_end;
       int pf = has_next ? 0 : 4;  // next-tile prefetch stage
@@ -721,6 +718,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
         ++g;
         if (pf < 4) prefetch_step();
       }
+      if (placeholder) continue;
       if (__any_sync(0xffffffffu, cn > 0)) merge();
 
       if (tid == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)(__ldg(a.leaf_size + cu.leaf)) * cu.qcnt);
@@ -736,13 +734,10 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
         if (a.fused) {
           auto qget = [sq](int j) { return sq[j * 128]; };
           uint32_t lf = cu.st & 0xFFFFu, pend = cu.st >> 16;
-          int nxt;
-          if (tree_smem) {
-            nxt = find_next_leaf_with(th, d, [sSplit](uint32_t node) { return sSplit[node]; }, qget, kth, lf, pend);
-          } else {
-            const float* sp = a.top.split;
-            nxt = find_next_leaf_with(th, d, [sp](uint32_t node) { return __ldg(sp + node); }, qget, kth, lf, pend);
-          }
+          // one FindLeaf body (instruction-cache footprint): the split values are
+          // read through a generic pointer, shared memory when the tree fits
+          const float* sp = tree_smem ? sSplit : a.top.split;
+          const int nxt = find_next_leaf_with(th, d, [sp](uint32_t node) { return sp[node]; }, qget, kth, lf, pend);
           a.state[qi] = (pend << 16) | lf;
           a.next[qi] = nxt;
           if (nxt >= 0) {

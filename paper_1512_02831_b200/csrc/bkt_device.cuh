@@ -116,6 +116,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   } while (!ok);
 }
 
+// Non-blocking probe: has phase `phase` of the barrier completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
 // Spinning variant (no suspend): lowest wake-up latency for warps on the
 // critical path of a short producer/consumer loop.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {

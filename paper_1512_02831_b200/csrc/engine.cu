@@ -834,7 +834,7 @@ struct SearchRun {
   bool tc = false;
   bool unfused = false;
   int tc_rows = 128;  // TC chunk width (BKT_TC_N): 64 or 128 columns
-  int tc_cps = 2;     // TC CTAs per SM
+  int tc_cps = 2;     // TC CTAs per SM (BKT_TC_CPS=3: 64-column chunks, one control warp)
   int grid_scan = 0;
   int grid_small = 0;
   bool timing = false;
@@ -1124,6 +1124,8 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   R.tc = ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
   R.unfused = false;
   if (const char* e = std::getenv("BKT_TC_N")) R.tc_rows = std::atoi(e) == 64 ? 64 : 128;
+  if (const char* e = std::getenv("BKT_TC_CPS")) R.tc_cps = std::atoi(e) == 3 ? 3 : 2;
+  if (R.tc_cps == 3) R.tc_rows = 64;
   if (const char* e = std::getenv("BKT_TC_UNFUSED")) R.unfused = std::atoi(e) != 0;
   if (o.kernel == 2 && !R.tc) return set_err(ctx, BKT_EINVAL, "tensor-core kernel requested but unavailable (needs a resident tree and d <= 31)");
   int rc = BKT_OK;

@@ -42,6 +42,11 @@ namespace bkt {
 // epilogue warps (one thread per query row) + a TMA producer warp + an MMA warp.
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
+// CPS >= 3: one control warp whose lane 0 runs the TMA producer and the MMA
+// issuer as one non-blocking loop (5 warps per CTA, 15 per SM: 4 per
+// sub-partition at most, so 128 registers per thread without setmaxnreg)
+__host__ __device__ constexpr int tc_ctl_warps(int cps) { return cps >= 3 ? 1 : 2; }
+__host__ __device__ constexpr int tc_threads(int cps) { return (kTcEpiWarps + tc_ctl_warps(cps)) * 32; }
 #ifndef BKT_TC_MARGIN_LOG2
 #define BKT_TC_MARGIN_LOG2 9
 #endif
@@ -72,11 +77,9 @@ __host__ __device__ constexpr int tc_smem_per_cta(int cps) { return (228 - cps) 
 // warps and one control warp fit (4 x 112 + 40 <= 512).
 constexpr int kTcCtlRegs = 40;
 __host__ __device__ constexpr int tc_launch_regs(int cps) {
-  return (16384 / (32 * ((cps * (kTcThreads / 32) + 3) / 4))) & ~7;
+  return (16384 / (32 * ((cps * (tc_threads(cps) / 32) + 3) / 4))) & ~7;
 }
-__host__ __device__ constexpr int tc_epi_regs(int cps) { return cps >= 3 ? 112 : tc_launch_regs(cps); }
-static_assert(tc_launch_regs(3) == 96 && tc_launch_regs(2) == 168, "register budget");
-static_assert(4 * 32 * tc_epi_regs(3) + 2 * 32 * kTcCtlRegs <= tc_launch_regs(3) * kTcThreads, "CTA register pool");
+static_assert(tc_launch_regs(3) == 128 && tc_launch_regs(2) == 168, "register budget");
 
 struct TcArgs {
   ScanArgs s;                  // queries, keys, schedule, top tree, stats (quad fields unused)
@@ -253,7 +256,7 @@ template <int KT, int KB, bool FMA, int NR, int CPS>
 #ifndef BKT_TC_MINB
 #define BKT_TC_MINB CPS
 #endif
-__global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(const TcArgs A) {
+__global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kernel(const TcArgs A) {
   using S = TcSmem<KT, NR, CPS>;
   constexpr int kTcRows = NR;
   constexpr int kTcBufs = S::kBufs;
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
   const int warp = tid >> 5, lane = tid & 31;
   const int nsplit = (1 << a.top.h) - 1;
   if (A.tree_smem)
-    for (int i = tid; i < nsplit; i += kTcThreads) sSplit[i] = __ldg(a.top.split + i);
+    for (int i = tid; i < nsplit; i += tc_threads(CPS)) sSplit[i] = __ldg(a.top.split + i);
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full[s], 1);
@@ -301,7 +304,8 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
     }
     fence_mbar_init();
   }
-  if (warp == kTcEpiWarps + 1) {
+  constexpr int kAllocWarp = kTcEpiWarps + tc_ctl_warps(CPS) - 1;
+  if (warp == kAllocWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(s_tmem)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -312,10 +316,98 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
   const uint32_t tmem = *s_tmem;
   const int tiles_end = a.tile_hi >= 0 ? a.tile_hi : *a.num_tiles;
 
-  // the control warps need few registers: they hand theirs to the epilogue warps
-  if (warp == kTcEpiWarps) {
+  // MMA issue of chunk c of tile T into TMEM buffer b from smem stage s (A buffer ab)
+  auto issue_mma = [&](const TcTile& T, int c, int s, uint32_t b, uint32_t ab) {
+    const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
+    const int nr = (int)dmin_ll(kTcRows, T.r1 - (T.r0 + (long long)c * kTcRows));
+    const uint32_t idesc = idesc_tf32(nr);
+#pragma unroll
+    for (int h = 0; h < KT / 8; ++h) {
+      const uint64_t da = umma_desc(a_base + ab * S::kA + h * 256, 128, KT * 32);
+      const uint64_t db = umma_desc(b_base + s * S::kStageB + h * 256, 128, KT * 32);
+      const uint32_t acc = h > 0 ? 1u : 0u;
+      asm volatile(
+          "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(
+              tmem + b * kTcRows),
+          "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_addr(&tfull[b]))
+                 : "memory");
+  };
+  // TMA load of chunk c of tile T into stage s
+  auto issue_tma = [&](const TcTile& T, int c, int s) {
+    const long long row = T.r0 + (long long)c * kTcRows;
+    const int nr = (int)dmin_ll(kTcRows, T.r1 - row);
+    mbar_arrive_expect_tx(&full[s], nr * (KT * 4 + 4 + A.d * 4));
+    bulk_g2s(sB + s * (S::kStageB / 4), A.B + row * KT, nr * KT * 4, &full[s]);
+    bulk_g2s(sIdx + s * kTcRows, A.ridx + row, nr * 4, &full[s]);
+    bulk_g2s(sRows + s * (S::kStageRows / 4), A.rows + row * A.d, nr * A.d * 4, &full[s]);
+  };
+
+  if (tc_ctl_warps(CPS) == 1 && warp == kTcEpiWarps) {
+    // ===== one control thread: TMA producer and MMA issuer, never blocking =====
+    if (lane == 0) {
+      const int t0 = a.tile_lo + (int)blockIdx.x;
+      int tp = t0, tm = t0, ip = 0, im = 0;
+      uint32_t gp = 0, gm = 0, ttm = 0;
+      bool p_done = tp >= tiles_end, m_done = tm >= tiles_end, m_has_a = false;
+      TcTile Tp{}, Tm{};
+      if (!p_done) Tp = tc_tile_info<kTcRows>(A, tp);
+      if (!m_done) Tm = tc_tile_info<kTcRows>(A, tm);
+      unsigned idle = 0;
+      while (!p_done || !m_done) {
+        bool progress = false;
+        if (!p_done) {
+          const int s = gp % kTcStages;
+          const uint32_t use = gp / kTcStages;
+          if (use == 0 || mbar_test(&empty[s], (use - 1) & 1u)) {
+            issue_tma(Tp, tc_chunk_at(ip, Tp.c0, Tp.nchunks), s);
+            ++gp;
+            if (++ip == Tp.nchunks) {
+              ip = 0;
+              tp += gridDim.x;
+              if (tp >= tiles_end) p_done = true;
+              else Tp = tc_tile_info<kTcRows>(A, tp);
+            }
+            progress = true;
+          }
+        }
+        if (!m_done) {
+          const uint32_t ab = ttm & 1u;
+          if (!m_has_a && mbar_test(&afull[ab], (ttm >> 1) & 1u)) {
+            tc_fence_after();
+            m_has_a = true;
+          }
+          if (m_has_a) {
+            const int s = gm % kTcStages;
+            const uint32_t b = gm % kTcBufs, use = gm / kTcBufs;
+            if (gm < gp && mbar_test(&full[s], (gm / kTcStages) & 1u) &&
+                (use == 0 || mbar_test(&tempty[b], (use - 1) & 1u))) {
+              tc_fence_after();
+              issue_mma(Tm, tc_chunk_at(im, Tm.c0, Tm.nchunks), s, b, ab);
+              ++gm;
+              if (++im == Tm.nchunks) {
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_addr(&aempty[ab]))
+                             : "memory");
+                im = 0;
+                ++ttm;
+                m_has_a = false;
+                tm += gridDim.x;
+                if (tm >= tiles_end) m_done = true;
+                else Tm = tc_tile_info<kTcRows>(A, tm);
+              }
+              progress = true;
+            }
+          }
+        }
+        if (progress) idle = 0;
+        else if (++idle > 8) __nanosleep(64);
+      }
+    }
+  } else if (warp == kTcEpiWarps) {
     // ===== TMA producer =====
-    if constexpr (CPS >= 3) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcCtlRegs));
     if (lane == 0) {
       uint32_t g = 0;
       for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x) {
@@ -344,7 +436,6 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
     }
   } else if (warp == kTcEpiWarps + 1) {
     // ===== MMA issuer =====
-    if constexpr (CPS >= 3) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcCtlRegs));
     if (lane == 0) {
       uint32_t g = 0, tt = 0;
       const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
@@ -393,7 +484,6 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
     }
   } else {
     // ===== epilogue: one thread per query =====
-    if constexpr (CPS >= 3) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(tc_epi_regs(CPS)));
     //
     // A tile's inputs (tile record, query id, coordinates, k-th distance,
     // traversal state) are fetched while the previous tile is being scanned,
@@ -776,7 +866,7 @@ __global__ void __launch_bounds__(kTcThreads, BKT_TC_MINB) leafscan_tc_kernel(co
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kTcEpiWarps + 1) {
+  if (warp == kAllocWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }

@@ -14,6 +14,8 @@ namespace bkt {
   cudaError_t launch_tc_##KT##_##NR##_##CPS##_##FMA(int kb, int grid, cudaStream_t s, const TcArgs& a, int* occ);
 BKT_TC_PART_DECL(16, 64, 2, 0)
 BKT_TC_PART_DECL(16, 64, 2, 1)
+BKT_TC_PART_DECL(16, 64, 3, 0)
+BKT_TC_PART_DECL(16, 64, 3, 1)
 BKT_TC_PART_DECL(16, 128, 2, 0)
 BKT_TC_PART_DECL(16, 128, 2, 1)
 BKT_TC_PART_DECL(32, 64, 2, 0)
@@ -48,8 +50,8 @@ cudaError_t launch_tc_one(int grid, cudaStream_t s, const TcArgs& a0, int* occ) 
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit, std::memory_order_release);
   }
-  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kTcThreads, smem);
-  fn<<<grid, kTcThreads, smem, s>>>(a);
+  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, tc_threads(CPS), smem);
+  fn<<<grid, tc_threads(CPS), smem, s>>>(a);
   return cudaGetLastError();
 }
 }  // namespace
@@ -77,7 +79,7 @@ cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t 
                                int nr, int cps) {
   if (kt == 32) return fma ? launch_tc_32_64_2_1(kb, grid, s, a, occ) : launch_tc_32_64_2_0(kb, grid, s, a, occ);
   if (kt != 16) return cudaErrorInvalidValue;
-  (void)cps;  // 3 CTAs/SM (setmaxnreg) deadlocked on B200: not built, see DESIGN.md
+  if (cps == 3) return fma ? launch_tc_16_64_3_1(kb, grid, s, a, occ) : launch_tc_16_64_3_0(kb, grid, s, a, occ);
   if (nr == 128) return fma ? launch_tc_16_128_2_1(kb, grid, s, a, occ) : launch_tc_16_128_2_0(kb, grid, s, a, occ);
   return fma ? launch_tc_16_64_2_1(kb, grid, s, a, occ) : launch_tc_16_64_2_0(kb, grid, s, a, occ);
 }

@@ -264,8 +264,11 @@ def main() -> None:
     e2e = None
     if not a.no_e2e:
         e2e_steps = max(1, min(a.steps, 3))
+        # warm-up calls: the same W as the device loop (at least 2, so that the
+        # page-locked result pool holds the buffers a result and its successor need)
+        e2e_warm = max(2, a.warmup)
         tot = 0.0
-        for i in range(e2e_steps + 1):
+        for i in range(e2e_warm + e2e_steps):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             barrier()
@@ -273,7 +276,7 @@ def main() -> None:
             res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=K), device=gpu, exact=exact, kernel=a.kernel)
             w1 = time.perf_counter()
             barrier()
-            if i > 0:  # first call is warm-up
+            if i >= e2e_warm:
                 tot += w1 - w0
         e2e_local = e2e_steps * m / tot
         e2e = {"value": e2e_local, "unit": UNIT, "h2d_bytes_per_step": int(m * DIM * 4),

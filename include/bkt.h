@@ -120,6 +120,12 @@ int bkt_scan_groups(bkt_ctx* ctx, const float* points, const int64_t* ids, int64
  * CUDA events; used as the measured roofline denominator. */
 int bkt_fp32_peak(bkt_ctx* ctx, double* tflops);
 
+/* Page-locked host memory for result arrays (cudaHostAlloc, portable): a
+ * search whose out_keys lie in it copies results straight from the device
+ * instead of through the pinned staging slots.  NULL on failure. */
+void* bkt_host_alloc(int64_t bytes);
+void bkt_host_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@ import ctypes
 import mmap
 import os
 import threading
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -26,7 +27,7 @@ BKT_ESTATE = -5
 # every symbol include/bkt.h declares
 EXPORTS = ("bkt_open", "bkt_close", "bkt_last_error", "bkt_device_info", "bkt_build_tree",
            "bkt_build_tree_device", "bkt_build_tree_device_error", "bkt_load_tree", "bkt_search",
-           "bkt_scan_groups", "bkt_fp32_peak")
+           "bkt_scan_groups", "bkt_fp32_peak", "bkt_host_alloc", "bkt_host_free")
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -99,6 +100,10 @@ def lib() -> ctypes.CDLL:
         L.bkt_search.argtypes = [P, P, i64, i32, ctypes.POINTER(SearchOpts), P, ctypes.POINTER(Stats)]
         L.bkt_scan_groups.argtypes = [P, P, P, i64, i32, P, i64, i32, P, i32, P, P, P, P, i32]
         L.bkt_fp32_peak.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
+        L.bkt_host_alloc.argtypes = [i64]
+        L.bkt_host_alloc.restype = P
+        L.bkt_host_free.argtypes = [P]
+        L.bkt_host_free.restype = None
         for name in EXPORTS:
             fn = getattr(L, name)
             if fn.restype is ctypes.c_int:  # default
@@ -126,13 +131,62 @@ def check(rc: int, ctx=None) -> None:
     raise RuntimeError(msg or f"libbkt error {rc}")
 
 
+class _PinnedPool:
+    """Recycles page-locked host buffers for result arrays.  cudaHostAlloc of
+    hundreds of MB costs more than the search, so a buffer goes back to the
+    pool (keyed by size) when the last array viewing it is collected, and the
+    next result of that size reuses it.  Results then leave the GPU at full
+    PCIe speed straight into the array the caller keeps."""
+
+    def __init__(self, max_bytes: int = 4 << 30) -> None:
+        self._free: dict[int, list[int]] = {}
+        self._lock = threading.Lock()
+        self._held = 0
+        self._max = max_bytes
+
+    def take(self, nbytes: int):
+        with self._lock:
+            lst = self._free.get(nbytes)
+            if lst:
+                return lst.pop()
+            if self._held + nbytes > self._max:
+                return None
+        addr = lib().bkt_host_alloc(nbytes)
+        if not addr:
+            return None
+        with self._lock:
+            self._held += nbytes
+        return addr
+
+    def give(self, nbytes: int, addr: int) -> None:
+        with self._lock:
+            self._free.setdefault(nbytes, []).append(addr)
+
+
+_PINNED = _PinnedPool()
+
+
 def host_empty(shape, dtype) -> np.ndarray:
-    """np.empty for large host result arrays, backed by 2 MB transparent huge
-    pages when the kernel allows it (madvise mode): writing a fresh 800 MB
-    result through 4 KB pages costs ~140 ms of page faults, more than its DMA."""
+    """np.empty for large host result arrays.
+
+    Large arrays come from the page-locked pool (see _PinnedPool); if that is
+    unavailable (no GPU driver, pool exhausted) they fall back to 2 MB
+    transparent huge pages when the kernel allows it (madvise mode): writing a
+    fresh 800 MB result through 4 KB pages costs ~140 ms of page faults, more
+    than its DMA."""
     dt = np.dtype(dtype)
     nbytes = int(np.prod(shape)) * dt.itemsize
-    if nbytes < (64 << 20) or not hasattr(mmap, "MADV_HUGEPAGE"):
+    if nbytes < (64 << 20):
+        return np.empty(shape, dt)
+    try:
+        addr = _PINNED.take(nbytes)
+    except NativeLibraryMissing:
+        addr = None
+    if addr:
+        buf = (ctypes.c_char * nbytes).from_address(addr)
+        weakref.finalize(buf, _PINNED.give, nbytes, addr)
+        return np.frombuffer(buf, dtype=dt).reshape(shape)
+    if not hasattr(mmap, "MADV_HUGEPAGE"):
         return np.empty(shape, dt)
     mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
     try:

@@ -1217,6 +1217,13 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     st.h2d_bytes += qbytes;
     return BKT_OK;
   };
+  // page-locked results (bkt_host_alloc) are copied straight from the device
+  bool out_pinned = false;
+  if (!o.keys_on_device) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, out_keys) == cudaSuccess && pa.type == cudaMemoryTypeHost) out_pinned = true;
+    cudaGetLastError();  // pageable memory reports an error on some drivers: clear it
+  }
   // results of batch b from buffer set `slot` (device results: async copy on the engine stream)
   auto store_out = [&](long long b, int slot) -> int {
     const long long b0 = b * batch, bm = std::min(batch, m - b0);
@@ -1224,7 +1231,14 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     if (o.keys_on_device) return BKT_OK;
     CU(cudaSetDevice(ctx->device));
     auto c0 = std::chrono::steady_clock::now();
-    int r = d2h_staged(ctx, ctx->io[1], out_keys + b0 * k, kbuf[slot], kbytes);
+    int r = BKT_OK;
+    if (out_pinned) {
+      if ((r = ensure_stageset(ctx, ctx->io[1])) != BKT_OK) return r;
+      CU(cudaMemcpyAsync(out_keys + b0 * k, kbuf[slot], kbytes, cudaMemcpyDeviceToHost, ctx->io[1].stream));
+      CU(cudaStreamSynchronize(ctx->io[1].stream));
+    } else {
+      r = d2h_staged(ctx, ctx->io[1], out_keys + b0 * k, kbuf[slot], kbytes);
+    }
     if (r != BKT_OK) return r;
     std::lock_guard<std::mutex> lk(st_mu);
     st.d2h_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();

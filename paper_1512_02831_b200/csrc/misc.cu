@@ -170,3 +170,13 @@ extern "C" int bkt_fp32_peak(bkt_ctx* ctx, double* tflops) {
   *tflops = best;
   return BKT_OK;
 }
+
+extern "C" void* bkt_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0 || cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  return p;
+}
+
+extern "C" void bkt_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}

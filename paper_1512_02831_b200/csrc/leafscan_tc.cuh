@@ -113,7 +113,7 @@ template <int KT, int NR, int CPS>
 struct TcSmem {
   static constexpr int kRows = NR;
   static constexpr int kBufs = tc_tmem_cols(CPS) / NR;
-  static constexpr int kStages = CPS >= 3 ? 3 : (KT <= 16 ? 512 : 128) / NR;
+  static constexpr int kStages = CPS >= 3 ? (NR == 128 ? 2 : 3) : (KT <= 16 ? 512 : 128) / NR;
   static constexpr int kStageB = NR * KT * 4;
   static constexpr int kStageIdx = NR * 4;
   static constexpr int kStageRows = NR * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
@@ -129,7 +129,7 @@ struct TcSmem {
   static constexpr int kNumBars = 2 * kStages + 2 * kBufs + 4;
   static constexpr int kOffTree = (kOffBar + kNumBars * 8 + 16 + 15) & ~15;
   static constexpr int kBytes = kOffTree + 1024;  // + alignment slack; the top tree (runtime size) follows
-  static_assert(kBufs >= 2, "need two TMEM accumulators");
+  static_assert(kBufs >= 1, "need a TMEM accumulator");
   static_assert(kBytes <= tc_smem_per_cta(CPS), "shared memory exceeds the per-CTA share");
 };
 

@@ -16,6 +16,8 @@ BKT_TC_PART_DECL(16, 64, 2, 0)
 BKT_TC_PART_DECL(16, 64, 2, 1)
 BKT_TC_PART_DECL(16, 64, 3, 0)
 BKT_TC_PART_DECL(16, 64, 3, 1)
+BKT_TC_PART_DECL(16, 128, 3, 0)
+BKT_TC_PART_DECL(16, 128, 3, 1)
 BKT_TC_PART_DECL(16, 128, 2, 0)
 BKT_TC_PART_DECL(16, 128, 2, 1)
 BKT_TC_PART_DECL(32, 64, 2, 0)
@@ -79,6 +81,8 @@ cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t 
                                int nr, int cps) {
   if (kt == 32) return fma ? launch_tc_32_64_2_1(kb, grid, s, a, occ) : launch_tc_32_64_2_0(kb, grid, s, a, occ);
   if (kt != 16) return cudaErrorInvalidValue;
+  if (cps == 3 && nr == 128)
+    return fma ? launch_tc_16_128_3_1(kb, grid, s, a, occ) : launch_tc_16_128_3_0(kb, grid, s, a, occ);
   if (cps == 3) return fma ? launch_tc_16_64_3_1(kb, grid, s, a, occ) : launch_tc_16_64_3_0(kb, grid, s, a, occ);
   if (nr == 128) return fma ? launch_tc_16_128_2_1(kb, grid, s, a, occ) : launch_tc_16_128_2_0(kb, grid, s, a, occ);
   return fma ? launch_tc_16_64_2_1(kb, grid, s, a, occ) : launch_tc_16_64_2_0(kb, grid, s, a, occ);

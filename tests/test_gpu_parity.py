@@ -320,3 +320,27 @@ def test_run_engine_bufferkdtree(rng):
                                  device_memory=200_000)
     assert info2["num_chunks"] > 1
     assert np.array_equal(res2.keys, res.keys)
+
+
+def test_large_result_through_pinned_pool(rng, gpu_device):
+    """Results of >= 64 MB come from the page-locked pool and leave the GPU by a
+    direct copy; they must equal the staged path and the oracle, and the pool
+    must recycle a buffer once its array is gone."""
+    from paper_1512_02831_b200 import _native
+    refs = rng.random((60_000, 10), dtype=np.float32)
+    q = rng.random((900_000, 10), dtype=np.float32)
+    tree = bkt.build_buffer_tree(refs, 6)
+    res = bkt.lazy_search(tree, q, bkt.SearchParams(k=10), device=gpu_device)
+    staged = np.empty((q.shape[0], 10), np.uint64)  # pageable: staged copy path
+    k2, _, _ = gpu_device.search(q, 10, out_keys=staged)
+    assert np.array_equal(res.keys, k2)
+    rows = np.arange(0, q.shape[0], 997)
+    want = O.knn_tree(O.build_tree(refs, 6), np.ascontiguousarray(q[rows]), 10, threads=8)
+    assert np.array_equal(res.keys[rows], want["keys"])
+    held = _native._PINNED._held
+    del res
+    import gc
+    gc.collect()
+    res2 = bkt.lazy_search(tree, q, bkt.SearchParams(k=10), device=gpu_device)
+    assert _native._PINNED._held == held  # the freed buffers were reused
+    assert np.array_equal(res2.keys, k2)

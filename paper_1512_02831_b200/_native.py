@@ -138,32 +138,50 @@ class _PinnedPool:
     next result of that size reuses it.  Results then leave the GPU at full
     PCIe speed straight into the array the caller keeps."""
 
-    def __init__(self, max_bytes: int = 4 << 30) -> None:
+    def __init__(self, max_bytes: int = 4 << 30, per_size: int = 2) -> None:
         self._free: dict[int, list[int]] = {}
+        self._count: dict[int, int] = {}
         self._lock = threading.Lock()
         self._held = 0
         self._max = max_bytes
+        self._per_size = per_size
+        self._filling: set[int] = set()
+
+    def _fill(self, nbytes: int) -> None:
+        try:
+            addr = lib().bkt_host_alloc(nbytes)
+        except Exception:  # pragma: no cover - no driver
+            addr = None
+        with self._lock:
+            self._filling.discard(nbytes)
+            if addr:
+                self._held += nbytes
+                self._count[nbytes] = self._count.get(nbytes, 0) + 1
+                self._free.setdefault(nbytes, []).append(addr)
 
     def take(self, nbytes: int):
+        # A free buffer of this size is handed out at once.  Otherwise the
+        # caller gets ordinary memory now and a buffer is page-locked in the
+        # background (cudaHostAlloc costs ~0.4 s per 800 MB), at most
+        # `per_size` per size: a caller that keeps many results alive (a
+        # stream) never waits for the allocation.
         with self._lock:
             lst = self._free.get(nbytes)
             if lst:
                 return lst.pop()
-            if self._held + nbytes > self._max:
+            if (self._held + nbytes > self._max or self._count.get(nbytes, 0) >= self._per_size
+                    or nbytes in self._filling):
                 return None
-        addr = lib().bkt_host_alloc(nbytes)
-        if not addr:
-            return None
-        with self._lock:
-            self._held += nbytes
-        return addr
+            self._filling.add(nbytes)
+        threading.Thread(target=self._fill, args=(nbytes,), daemon=True).start()
+        return None
 
     def give(self, nbytes: int, addr: int) -> None:
         with self._lock:
             self._free.setdefault(nbytes, []).append(addr)
 
 
-_PINNED = _PinnedPool()
+_PINNED = _PinnedPool(max_bytes=0 if os.environ.get("BKT_NO_PINNED_POOL") else 4 << 30)
 
 
 def host_empty(shape, dtype) -> np.ndarray:

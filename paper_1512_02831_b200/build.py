@@ -105,7 +105,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
         diag.append("-DBKT_TC_CROSS=1")
     if os.environ.get("BKT_BUILD_MARGIN"):
         diag.append(f"-DBKT_TC_MARGIN_LOG2={int(os.environ['BKT_BUILD_MARGIN'])}")
-    for kt, nr, cps in ((16, 64, 2), (16, 64, 3), (16, 128, 2), (16, 128, 3), (32, 64, 2)):
+    for kt, nr, cps in ((16, 64, 2), (16, 64, 3), (16, 128, 2), (16, 128, 3), (16, 256, 2), (32, 64, 2)):
         for fma in (0, 1):
             obj = OBJ_DIR / f"leafscan_tc_{kt}_{nr}_{cps}_{fma}.o"
             src = CSRC / "leafscan_tc_inst.cu"

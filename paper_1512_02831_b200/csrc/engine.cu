@@ -336,8 +336,7 @@ constexpr size_t kStageSlot = 32ull << 20;
 
 // memcpy with a few host threads (host <-> pinned staging is the e2e bottleneck)
 void par_memcpy(void* dst, const void* src, size_t n) {
-  static const size_t hw = std::max(1u, std::thread::hardware_concurrency());
-  const int nt = (int)std::min<size_t>(std::min<size_t>(16, hw), std::max<size_t>(1, n >> 21));
+  const int nt = (int)std::min<size_t>(8, std::max<size_t>(1, n >> 22));
   if (nt <= 1) {
     std::memcpy(dst, src, n);
     return;
@@ -1124,7 +1123,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // as fast: few pairs per query and a mostly empty K=16 MMA; tools/configs.py cfg4)
   R.tc = ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
   R.unfused = false;
-  if (const char* e = std::getenv("BKT_TC_N")) R.tc_rows = std::atoi(e) == 64 ? 64 : 128;
+  if (const char* e = std::getenv("BKT_TC_N")) R.tc_rows = std::atoi(e) == 64 ? 64 : (std::atoi(e) == 256 ? 256 : 128);
   if (const char* e = std::getenv("BKT_TC_CPS")) R.tc_cps = std::atoi(e) == 3 ? 3 : 2;
   if (R.tc_cps == 3 && !std::getenv("BKT_TC_N")) R.tc_rows = 64;
   if (const char* e = std::getenv("BKT_TC_UNFUSED")) R.unfused = std::atoi(e) != 0;

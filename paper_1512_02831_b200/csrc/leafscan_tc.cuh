@@ -113,7 +113,7 @@ template <int KT, int NR, int CPS>
 struct TcSmem {
   static constexpr int kRows = NR;
   static constexpr int kBufs = tc_tmem_cols(CPS) / NR;
-  static constexpr int kStages = CPS >= 3 ? (NR == 128 ? 2 : 3) : (KT <= 16 ? 512 : 128) / NR;
+  static constexpr int kStages = CPS >= 3 ? (NR == 128 ? 2 : 3) : ((KT <= 16 ? 512 : 128) / NR < 2 ? 2 : (KT <= 16 ? 512 : 128) / NR);
   static constexpr int kStageB = NR * KT * 4;
   static constexpr int kStageIdx = NR * 4;
   static constexpr int kStageRows = NR * (KT - 1) * 4;  // original coordinates (d <= KT - 1)
@@ -756,13 +756,14 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         mchunk = min32(va);
         if (ngrp > 1) mchunk = fminf(mchunk, min32(vb));
         if constexpr (NR > 64) {
-          if (ngrp > 2) {
-            tmem_ld32_async(tbase + 64, va);
-            if (ngrp > 3) tmem_ld32_async(tbase + 96, vb);
+#pragma unroll 1
+          for (int gp = 2; gp < ngrp; gp += 2) {
+            tmem_ld32_async(tbase + 32 * gp, va);
+            if (gp + 1 < ngrp) tmem_ld32_async(tbase + 32 * (gp + 1), vb);
             tmem_wait(va);
             tmem_touch(vb);
             mchunk = fminf(mchunk, min32(va));
-            if (ngrp > 3) mchunk = fminf(mchunk, min32(vb));
+            if (gp + 1 < ngrp) mchunk = fminf(mchunk, min32(vb));
           }
         }
         if (dbg_on) A.dbg[16 * g + 8] = clock64();

@@ -18,6 +18,8 @@ BKT_TC_PART_DECL(16, 64, 3, 0)
 BKT_TC_PART_DECL(16, 64, 3, 1)
 BKT_TC_PART_DECL(16, 128, 3, 0)
 BKT_TC_PART_DECL(16, 128, 3, 1)
+BKT_TC_PART_DECL(16, 256, 2, 0)
+BKT_TC_PART_DECL(16, 256, 2, 1)
 BKT_TC_PART_DECL(16, 128, 2, 0)
 BKT_TC_PART_DECL(16, 128, 2, 1)
 BKT_TC_PART_DECL(32, 64, 2, 0)
@@ -84,6 +86,7 @@ cudaError_t launch_leafscan_tc(int kt, int kb, bool fma, int grid, cudaStream_t 
   if (cps == 3 && nr == 128)
     return fma ? launch_tc_16_128_3_1(kb, grid, s, a, occ) : launch_tc_16_128_3_0(kb, grid, s, a, occ);
   if (cps == 3) return fma ? launch_tc_16_64_3_1(kb, grid, s, a, occ) : launch_tc_16_64_3_0(kb, grid, s, a, occ);
+  if (nr == 256) return fma ? launch_tc_16_256_2_1(kb, grid, s, a, occ) : launch_tc_16_256_2_0(kb, grid, s, a, occ);
   if (nr == 128) return fma ? launch_tc_16_128_2_1(kb, grid, s, a, occ) : launch_tc_16_128_2_0(kb, grid, s, a, occ);
   return fma ? launch_tc_16_64_2_1(kb, grid, s, a, occ) : launch_tc_16_64_2_0(kb, grid, s, a, occ);
 }

@@ -155,7 +155,7 @@ struct bkt_ctx {
 
   std::vector<cudaEvent_t> ev_pool;   // leafscan timing events
   cudaEvent_t ring_ev[4] = {};        // round-check ring (kRing)
-  cudaEvent_t t_ev[2] = {};           // whole-search timing
+  cudaEvent_t t_ev[3] = {};           // whole-search timing + early-drain marker
   // leafscan grid per (D, KB, mode)
   std::vector<std::pair<long long, int>> grid_cache;
 };
@@ -617,6 +617,7 @@ int bkt_open(int cuda_device, bkt_ctx** out) {
   CU(cudaHostAlloc(&ctx->h_ctl, sizeof(RoundCtl) * kRing, cudaHostAllocDefault));
   for (int i = 0; i < kRing; ++i) CU(cudaEventCreateWithFlags(&ctx->ring_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) CU(cudaEventCreate(&ctx->t_ev[i]));
+  CU(cudaEventCreateWithFlags(&ctx->t_ev[2], cudaEventDisableTiming));
   for (int s = 0; s < 2; ++s) {
     CU(cudaEventCreateWithFlags(&ctx->slot_free[s], cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ctx->slot_ready[s], cudaEventDisableTiming));
@@ -640,7 +641,7 @@ void bkt_close(bkt_ctx* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < kRing; ++i)
     if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 3; ++i)
     if (ctx->t_ev[i]) cudaEventDestroy(ctx->t_ev[i]);
   for (int s = 0; s < 2; ++s) {
     if (ctx->slot_free[s]) cudaEventDestroy(ctx->slot_free[s]);
@@ -848,6 +849,12 @@ struct SearchRun {
   bool seq = false;
   long long seq_cap = 0;
   bool counters = false;
+  // early result drain (single batch, host results): when at most drain_at
+  // queries remain active, snapshot them and start copying every row to the
+  // host while the tail rounds run; drain_start() launches the copy
+  long long drain_at = -1;
+  bool drain_fired = false;
+  std::function<void()> drain_start;
 };
 
 ScanArgs make_scan_args(bkt_ctx* ctx, SearchRun& R, int cur) {
@@ -1081,6 +1088,14 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       const int chk = (int)((round - (kRing - 1)) % kRing);
       CU(cudaEventSynchronize(ring[chk]));
       if (ctx->h_ctl[chk].active == 0) break;
+      if (R.drain_at >= 0 && !R.drain_fired && ctx->h_ctl[chk].active <= R.drain_at) {
+        // the list just scanned holds every query that can still change
+        snapshot_active<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], ctx->ctl, ctx->qkey);
+        CU(cudaGetLastError());
+        R.launches++;
+        R.drain_fired = true;
+        R.drain_start();
+      }
     }
   }
   CU(cudaStreamSynchronize(ctx->stream));
@@ -1284,7 +1299,62 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
       pad_rows_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(raw, ctx->d, ctx->q, ctx->D, bm);
       R.launches++;
     }
+    // Early result drain for a single host-result batch: rows of finished
+    // queries leave the GPU while the tail rounds run; the rows of queries
+    // still active at that point are fixed up afterwards.
+    std::thread t_drain;
+    int rc_drain = BKT_OK;
+    // (opt-in: measured 2% slower end to end on config 2 -- the copy competes with the tail rounds)
+    const bool drain = !o.keys_on_device && nbatch == 1 && bm >= (1 << 20) && std::getenv("BKT_EARLY_DRAIN");
+    cudaEvent_t drain_ev = ctx->t_ev[2];
+    if (drain) {
+      R.drain_at = std::max<long long>(1024, bm / 128);
+      R.drain_fired = false;
+      R.drain_start = [&, slot]() {
+        cudaEventRecord(drain_ev, ctx->stream);
+        t_drain = std::thread([&, slot]() {
+          cudaSetDevice(ctx->device);
+          if (cudaEventSynchronize(drain_ev) != cudaSuccess) {
+            rc_drain = BKT_ECUDA;
+            return;
+          }
+          rc_drain = store_out(0, slot);
+        });
+      };
+    } else {
+      R.drain_at = -1;
+    }
     rc = search_batch(ctx, R);
+    if (drain) {
+      if (t_drain.joinable()) t_drain.join();
+      if (rc == BKT_OK) rc = rc_drain;
+      if (rc == BKT_OK && R.drain_fired) {
+        // fix up the rows that were still active when the drain started
+        gather_late<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->keys, k, ctx->qkey, ctx->ctl,
+                                                          reinterpret_cast<uint64_t*>(ctx->kthv));
+        RoundCtl fin;
+        std::vector<int> ids;
+        std::vector<uint64_t> rows;
+        if (cudaMemcpyAsync(&fin, ctx->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+          rc = set_err(ctx, BKT_ECUDA, "early drain fix-up failed");
+        } else {
+          ids.resize(fin.late_n);
+          rows.resize((size_t)fin.late_n * k);
+          if ((fin.late_n > 0 &&
+               (cudaMemcpyAsync(ids.data(), ctx->qkey, sizeof(int) * fin.late_n, cudaMemcpyDeviceToHost,
+                                ctx->stream) != cudaSuccess ||
+                cudaMemcpyAsync(rows.data(), ctx->kthv, sizeof(uint64_t) * rows.size(), cudaMemcpyDeviceToHost,
+                                ctx->stream) != cudaSuccess)) ||
+              cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = set_err(ctx, BKT_ECUDA, "early drain fix-up failed");
+          for (int i = 0; i < fin.late_n && rc == BKT_OK; ++i)
+            std::memcpy(out_keys + (b0 + ids[i]) * k, rows.data() + (size_t)i * k, sizeof(uint64_t) * k);
+        }
+      }
+      R.drain_at = -1;
+      R.drain_start = nullptr;
+    }
     if (rc == BKT_OK && o.keys_on_device &&
         cudaMemcpyAsync(out_keys + b0 * k, ctx->keys, sizeof(uint64_t) * bm * k, cudaMemcpyDeviceToDevice,
                         ctx->stream) != cudaSuccess)
@@ -1299,7 +1369,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     if (t_out.joinable()) t_out.join();  // the previous batch's results are out
     if (rc == BKT_OK) rc = rc_out;
     if (rc != BKT_OK) { join_all(); return rc; }
-    if (!o.keys_on_device) {
+    if (!o.keys_on_device && !(drain && R.drain_fired)) {
       if (overlap) {
         t_out = std::thread([&, b, slot]() { rc_out = store_out(b, slot); });
       } else if ((rc = store_out(b, slot)) != BKT_OK) {

@@ -27,7 +27,27 @@ struct RoundCtl {
   int num_tiles;    // tiles this round
   int rounds;       // rounds with active > 0
   long long scans;  // (query, leaf) scans so far (SearchStats.leaf_scan_events)
+  int late_n;       // early result drain: queries still active when it started
+  int pad_;
 };
+
+// Early result drain: remember the queries of the round just scanned (every
+// query still active later is among them; the active set only shrinks).
+__global__ void snapshot_active(const int* __restrict__ work, RoundCtl* ctl, int* __restrict__ late_ids) {
+  const int n = ctl->active;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) late_ids[i] = work[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->late_n = n;
+}
+
+// ... and at the end gather their final top-k rows for the host fix-up.
+__global__ void gather_late(const uint64_t* __restrict__ keys, int k, const int* __restrict__ late_ids,
+                            const RoundCtl* ctl, uint64_t* __restrict__ out) {
+  const long long total = (long long)ctl->late_n * k;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / k;
+    out[t] = keys[(long long)late_ids[i] * k + (t - i * k)];
+  }
+}
 
 constexpr int kPlanThreads = 1024;
 

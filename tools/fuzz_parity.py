@@ -1,0 +1,92 @@
+"""Randomised exactness sweep of the B200 engine against the CPU oracle.
+
+    python tools/fuzz_parity.py [--cases 200] [--seed 1] [--seconds 600]
+
+Each case draws n, m, d, k, h, a data family (uniform, Gaussian mixture with
+tiny or wide spreads, large offsets, per-dimension scales spanning 1e-3..1e3,
+integer grids with heavy ties, duplicated points, negative coordinates) and a
+kernel (auto / tc / direct, exact mode), runs lazy_search on cuda:0 and
+requires bit-identical keys and visited counts.  One JSON line per failure,
+a summary line at the end.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1512_02831_b200 as bkt  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def draw(rng, n, d):
+    fam = rng.choice(["uniform", "mixture_tight", "mixture_wide", "offset", "scales", "grid", "dups", "negative"])
+    if fam == "uniform":
+        x = rng.random((n, d))
+    elif fam == "mixture_tight":
+        c = rng.random((4, d))
+        x = c[rng.integers(0, 4, n)] + rng.normal(0, 1e-3, (n, d))
+    elif fam == "mixture_wide":
+        c = rng.random((16, d)) * 10
+        x = c[rng.integers(0, 16, n)] + rng.normal(0, 0.5, (n, d))
+    elif fam == "offset":
+        x = 1e4 + rng.random((n, d))
+    elif fam == "scales":
+        x = rng.random((n, d)) * (10.0 ** rng.uniform(-3, 3, d))
+    elif fam == "grid":
+        x = rng.integers(0, 4, (n, d)).astype(np.float64)
+    elif fam == "dups":
+        base = rng.random((max(1, n // 8), d))
+        x = base[rng.integers(0, base.shape[0], n)]
+    else:
+        x = rng.normal(0, 3, (n, d))
+    return fam, x.astype(np.float32)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=200)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--seconds", type=float, default=600)
+    a = ap.parse_args()
+    rng = np.random.default_rng(a.seed)
+    dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
+    t0 = time.time()
+    done = fails = 0
+    for case in range(a.cases):
+        if time.time() - t0 > a.seconds:
+            break
+        d = int(rng.choice([1, 2, 3, 5, 8, 9, 10, 11, 12, 15, 16, 20, 27, 31]))
+        n = int(rng.integers(300, 60_000))
+        h = int(rng.integers(1, max(2, min(12, int(np.log2(n)) - 2))))
+        k = int(min(n, rng.choice([1, 2, 5, 10, 16, 33, 50, 64])))
+        m = int(rng.integers(1, 6000))
+        fam, pts = draw(rng, n + m, d)
+        refs, q = pts[:n], pts[n:]
+        if rng.random() < 0.2:  # some queries exactly on reference points
+            take = rng.integers(0, n, size=m // 3)
+            q[: take.size] = refs[take]
+        kernel = str(rng.choice(["auto", "tc", "direct"])) if d <= 31 else "direct"
+        tree = bkt.build_buffer_tree(refs, h, device=0 if rng.random() < 0.5 else None)
+        st = bkt.SearchStats()
+        res = bkt.lazy_search(tree, q, bkt.SearchParams(k=k), device=dev, stats=st, kernel=kernel)
+        want = O.knn_tree(O.build_tree(refs, h), q, k, threads=8)
+        ok = bool(np.array_equal(res.keys, want["keys"])) and bool(
+            np.array_equal(st.visited_per_query, want["visited"].astype(np.int64)))
+        done += 1
+        if not ok:
+            fails += 1
+            bad = int((res.keys != want["keys"]).any(axis=1).sum())
+            print(json.dumps({"case": case, "fam": fam, "n": n, "m": m, "d": d, "k": k, "h": h, "kernel": kernel,
+                              "rows_differing": bad}), flush=True)
+    print(json.dumps({"cases": done, "failures": fails, "seconds": round(time.time() - t0, 1)}), flush=True)
+    dev.close()
+
+
+if __name__ == "__main__":
+    main()

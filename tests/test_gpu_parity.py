@@ -345,3 +345,19 @@ def test_large_result_through_pinned_pool(rng, gpu_device):
         assert np.array_equal(res2.keys, k2)
     nbytes = q.shape[0] * 10 * 8
     assert _native._PINNED._count.get(nbytes, 0) <= _native._PINNED._per_size
+
+
+@pytest.mark.parametrize("env", [{"BKT_TC_N": "64"}, {"BKT_TC_N": "256"}, {"BKT_TC_CPS": "3"},
+                                 {"BKT_TC_CPS": "3", "BKT_TC_N": "128"}])
+def test_tensor_core_variants_exact(knn_golden, gpu_device, env, monkeypatch):
+    """The alternative tensor-core layouts (chunk width, one control warp with
+    3 CTAs per SM) are bit-identical to the reference as well."""
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    for c in knn_golden[:12]:
+        s = c["spec"]
+        if s["d"] > 15:  # the variants cover the KT = 16 layout
+            continue
+        tree = bkt.build_buffer_tree(c["refs"], s["h"])
+        res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, kernel="tc")
+        assert np.array_equal(res.keys, c["keys"]), (env, s)

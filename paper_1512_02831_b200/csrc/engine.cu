@@ -1009,7 +1009,7 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
     CU(cudaEventRecord(ctx->slot_free[s], ctx->stream));
   }
   // FindLeaf after every chunk of the round has been scanned
-  findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
+  findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
       ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys, ctx->state,
       ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
   CU(cudaGetLastError());
@@ -1026,7 +1026,8 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
   CU(cudaMemsetAsync(ctx->cursor, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
-  start_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
+  start_kernel<<<R.grid_small, kStartQ, start_smem_bytes(ctx->h, ctx->D), ctx->stream>>>(
+      ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
                                                        ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
                                                        R.seq_cap, ctx->kthv, ctx->blk_base, ctx->nodes, ctx->sub_w,
                                                        ctx->qkey, ctx->counts);
@@ -1074,7 +1075,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       if (unfused) {
         // FindLeaf as its own high-occupancy pass: its dependent top-tree loads
         // then overlap across many warps instead of stalling the scan's epilogue
-        findleaf_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(
+        findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
             ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys,
             ctx->state, ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
         CU(cudaGetLastError());

@@ -51,21 +51,66 @@ __global__ void gather_late(const uint64_t* __restrict__ keys, int k, const int*
 
 constexpr int kPlanThreads = 1024;
 
-// Fresh queries: EMPTY top-k, descend from the root, count.
-__global__ void start_kernel(const float* __restrict__ q, int D, long long m, int k, TopTreeView top,
-                             uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next,
-                             uint32_t* __restrict__ visits, int* seq_log, unsigned long long* seq_pos,
-                             long long seq_cap, float* __restrict__ kth, const int* __restrict__ blk_base,
-                             const int4* __restrict__ nodes, int sub_w, int* __restrict__ qkey,
-                             int* __restrict__ counts) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
-    uint64_t* kp = keys + i * k;
-    for (int t = 0; t < k; ++t) kp[t] = kEmptyKey;
-    kth[i] = __int_as_float(0x7f800000);
-    const float* qp = q + i * D;
-    auto qget = [qp](int j) { return __ldg(qp + j); };
+// FindLeafBatch for fresh queries (buffer_tree.py:318-321, 351-376): EMPTY
+// top-k, descend from the root, route to the home block, count.  Each CTA
+// takes 256 consecutive queries at a time: their rows (one contiguous block)
+// arrive with coalesced 16-byte loads into shared memory, their top-k rows
+// are initialised with coalesced stores, and the top tree's split values sit
+// in shared memory when they fit (start_smem_bytes).
+constexpr int kStartQ = 256;
+// split values kept in shared memory: up to 16 KB (h <= 12) beside ...
+__host__ __device__ inline int start_tree_smem(int h) { return ((1 << h) - 1) * 4 <= 16384 ? ((1 << h) - 1) : 0; }
+// ... and for start_kernel only while tree + rows stay within the 48 KB default
+__host__ __device__ inline int start_tree_n(int h, int D) {
+  const int t = start_tree_smem(h);
+  return t * 4 + kStartQ * (D + 1) * 4 <= 48 * 1024 ? t : 0;
+}
+__host__ __device__ inline int start_smem_bytes(int h, int D) { return start_tree_n(h, D) * 4 + kStartQ * (D + 1) * 4; }
+
+__global__ void __launch_bounds__(kStartQ) start_kernel(const float* __restrict__ q, int D, long long m, int k,
+                                                        TopTreeView top, uint64_t* __restrict__ keys,
+                                                        uint32_t* __restrict__ state, int* __restrict__ next,
+                                                        uint32_t* __restrict__ visits, int* seq_log,
+                                                        unsigned long long* seq_pos, long long seq_cap,
+                                                        float* __restrict__ kth, const int* __restrict__ blk_base,
+                                                        const int4* __restrict__ nodes, int sub_w,
+                                                        int* __restrict__ qkey, int* __restrict__ counts) {
+  extern __shared__ float s_start[];
+  const int ntree = start_tree_n(top.h, D);
+  float* s_split = s_start;
+  float* s_rows = s_start + ntree;  // [kStartQ][D + 1] (odd stride: conflict-free row reads)
+  for (int i = threadIdx.x; i < ntree; i += blockDim.x) s_split[i] = __ldg(top.split + i);
+  const int stride = D + 1;
+  for (long long c0 = (long long)blockIdx.x * kStartQ; c0 < m; c0 += (long long)gridDim.x * kStartQ) {
+    const int nq = (int)min((long long)kStartQ, m - c0);
+    __syncthreads();  // previous chunk's rows consumed (and the tree staged)
+    const float* src = q + c0 * D;
+    const int nf = nq * D;
+    if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (nf & 3) == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      for (int t = threadIdx.x; t < nf / 4; t += blockDim.x) {
+        const float4 v = __ldg(s4 + t);
+        const int e = 4 * t;
+        s_rows[(e / D) * stride + e % D] = v.x;
+        s_rows[((e + 1) / D) * stride + (e + 1) % D] = v.y;
+        s_rows[((e + 2) / D) * stride + (e + 2) % D] = v.z;
+        s_rows[((e + 3) / D) * stride + (e + 3) % D] = v.w;
+      }
+    } else {
+      for (int t = threadIdx.x; t < nf; t += blockDim.x) s_rows[(t / D) * stride + t % D] = __ldg(src + t);
+    }
+    // EMPTY top-k rows of the chunk: one contiguous block of nq * k keys
+    uint64_t* kp = keys + c0 * k;
+    for (int t = threadIdx.x; t < nq * k; t += blockDim.x) kp[t] = kEmptyKey;
+    __syncthreads();
+    if (threadIdx.x >= nq) continue;
+    const long long i = c0 + threadIdx.x;
+    const float* row = s_rows + threadIdx.x * stride;
+    auto qget = [row](int j) { return row[j]; };
     uint32_t leaf = 0, pend = 0;
-    descend(top, qget, leaf, pend, 0);
+    if (ntree) descend_with(top.h, top.d, [s_split](uint32_t node) { return s_split[node]; }, qget, leaf, pend, 0);
+    else descend(top, qget, leaf, pend, 0);
+    kth[i] = __int_as_float(0x7f800000);
     state[i] = (pend << 16) | leaf;
     next[i] = (int)leaf;
     visits[i] = 1;
@@ -85,7 +130,7 @@ __global__ void start_kernel(const float* __restrict__ q, int D, long long m, in
         int c = 0;
         for (;;) {
           const int4 v = __ldg(nd + c);
-          c = (__ldg(qp + v.y) >= __int_as_float(v.x)) ? v.w : v.z;
+          c = (row[v.y] >= __int_as_float(v.x)) ? v.w : v.z;
           if (c < 0) break;
         }
         sub = (~c) >> home_block_shift(nb, sub_w);
@@ -220,6 +265,11 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
                                 uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
                                 int* __restrict__ counts, int* seq_log, unsigned long long* seq_pos,
                                 long long seq_cap) {
+  // the top tree's split values in shared memory when they fit (dynamic smem)
+  extern __shared__ float s_fl_split[];
+  const int ntree = start_tree_smem(top.h);
+  for (int i = threadIdx.x; i < ntree; i += blockDim.x) s_fl_split[i] = __ldg(top.split + i);
+  __syncthreads();
   const int n = ctl->active;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int qi = work[i];
@@ -228,7 +278,9 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
     float kth = key_dist(keys[(long long)qi * k + k - 1]);
     uint32_t st = state[qi];
     uint32_t lf = st & 0xFFFFu, pend = st >> 16;
-    int nxt = find_next_leaf(top, qget, kth, lf, pend);
+    int nxt;
+    if (ntree) nxt = find_next_leaf_with(top.h, top.d, [](uint32_t node) { return s_fl_split[node]; }, qget, kth, lf, pend);
+    else nxt = find_next_leaf(top, qget, kth, lf, pend);
     state[qi] = (pend << 16) | lf;
     next[qi] = nxt;
     if (nxt >= 0) {

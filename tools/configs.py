@@ -4,6 +4,7 @@
     python tools/configs.py cfg3 [--m 2e8]       # n=2M refs, query stream of m queries in 10M chunks
     python tools/configs.py cfg4 [--m 10e6]      # d = 5 / 15 / 27 mixture, n=2M
     python tools/configs.py cfg5 [--m 1e6]       # n=8M host-resident leaf streaming, k in {1,10,50}, h in {8,11,14}
+    python tools/configs.py uniform2m [--m 1e7]  # uniform data at the headline size (n=2M, d=10, k=10)
 
 One JSON line per measurement on stdout.  Every run checks a sample of rows
 against the CPU oracle (exact mode: bit-identical keys).
@@ -114,6 +115,25 @@ def cfg4(a):
         dev.close()
 
 
+def uniform2m(a):
+    """The north star's second data family at the headline size: uniform
+    [0,1)^10 (reference gen_synthetic "uniform"), n=2M refs, m queries."""
+    n, m = 2_000_000, int(a.m)
+    rng = np.random.default_rng(0)
+    refs = rng.random((n, 10), dtype=np.float32)
+    queries = rng.random((m, 10), dtype=np.float32)
+    for h in (9, 11):
+        tree = bkt.build_buffer_tree(refs, h)
+        dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
+        dev.ensure_tree(tree)
+        dev.search(queries[:100000], 10)
+        keys, st, _ = dev.search(queries, 10, timing=True)
+        ok = oracle_check(tree, queries, keys, 10, rows=256)
+        emit({"config": f"uniform n=2M m={m} d=10 k=10 h={h}", "qps_device": m / (st["search_ms"] / 1e3),
+              "pairs_per_query": st["pairs"] / m, "rounds": st["rounds"], "sample_rows_match_oracle": ok})
+        dev.close()
+
+
 def cfg5(a):
     n, m = 8_000_000, int(a.m)
     pts, _ = gen_mixture(n + m, 10, seed=1)
@@ -138,11 +158,11 @@ def cfg5(a):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["cfg1", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("which", choices=["cfg1", "cfg3", "cfg4", "cfg5", "uniform2m"])
     ap.add_argument("--m", type=float, default=None)
     a = ap.parse_args()
     if a.m is None:
-        a.m = {"cfg1": 65536, "cfg3": 2e8, "cfg4": 10e6, "cfg5": 1e6}[a.which]
+        a.m = {"cfg1": 65536, "cfg3": 2e8, "cfg4": 10e6, "cfg5": 1e6, "uniform2m": 10e6}[a.which]
     globals()[a.which](a)
 
 

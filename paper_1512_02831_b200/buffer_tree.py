@@ -290,9 +290,7 @@ def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: Buffe
     keys, st, seq = dev.search(qarr, params.k, exact=exact, visited=visited, seq_cap=seq_cap,
                                timing=stats is not None, kernel=kernel)
     t2 = time.perf_counter()
-    counts = _native.host_empty((m,), np.int64)
-    counts.fill(params.k)
-    result = NeighborBatch.from_keys(keys, counts)
+    result = NeighborBatch.from_keys(keys, params.k)  # every row is full: counts built on first access
 
     if debug_audit:
         # query conservation (buffer_tree.py:632-637): every query finished

@@ -699,13 +699,13 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         const int s = g % kTcStages;
         const uint32_t b = g % kTcBufs;
         const long long te0 = kTcDiag ? clock64() : 0;
-        if (A.spin) {
-          mbar_wait_spin(&tfull[b], (g / kTcBufs) & 1u);
-          mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
-        } else {
-          mbar_wait(&tfull[b], (g / kTcBufs) & 1u);
-          mbar_wait(&full[s], (g / kTcStages) & 1u);
-        }
+        // Only the accumulator is waited for here.  The stage's ids and
+        // coordinates (TMA -> full[s]) are read by survivor re-evaluation
+        // alone, which waits for full[s] itself; most chunks have none.
+        // Skipping a phase is safe: the producer cannot refill stage s
+        // before this warp's empty[s] arrival below.
+        if (A.spin) mbar_wait_spin(&tfull[b], (g / kTcBufs) & 1u);
+        else mbar_wait(&tfull[b], (g / kTcBufs) & 1u);
         tc_fence_after();
         const long long te1 = kTcDiag ? clock64() : 0;
         const long long row0 = cu.r0 + (long long)c * kTcRows;
@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         }
         if (dbg_on) A.dbg[16 * g + 8] = clock64();
         if (__any_sync(0xffffffffu, mchunk <= thr)) {
+          mbar_wait(&full[s], (g / kTcStages) & 1u);
           if (NR == 64) {
             // both groups are still in registers
             process(va, 0, s);

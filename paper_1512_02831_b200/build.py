@@ -91,7 +91,7 @@ def _compile(cmd: list[str], src: Path, obj: Path, force: bool) -> bool:
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> Path:
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
     tag = _sources_hash("v1" + os.environ.get("BKT_BUILD_DIAG", "") + os.environ.get("BKT_BUILD_CROSS", "")
-                        + os.environ.get("BKT_BUILD_MARGIN", ""))
+                        + os.environ.get("BKT_BUILD_MARGIN", "") + os.environ.get("BKT_BUILD_DEFS", ""))
     stamp = LIB_DIR / "libbkt.stamp"
     if LIB.exists() and stamp.exists() and stamp.read_text() == tag and not force:
         return LIB
@@ -105,6 +105,8 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
         diag.append("-DBKT_TC_CROSS=1")
     if os.environ.get("BKT_BUILD_MARGIN"):
         diag.append(f"-DBKT_TC_MARGIN_LOG2={int(os.environ['BKT_BUILD_MARGIN'])}")
+    # experiments: extra -D flags for every CUDA unit, e.g. BKT_BUILD_DEFS="-DBKT_TC_LD4=1"
+    diag += [f for f in os.environ.get("BKT_BUILD_DEFS", "").split() if f.startswith("-D")]
     for kt, nr, cps in ((16, 64, 2), (16, 64, 3), (16, 128, 2), (16, 128, 3), (16, 256, 2), (32, 64, 2)):
         for fma in (0, 1):
             obj = OBJ_DIR / f"leafscan_tc_{kt}_{nr}_{cps}_{fma}.o"

@@ -909,10 +909,10 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.kth = ctx->kthv;
     t.d = ctx->d;
     t.qstride = ctx->D;
-    t.spin = 1;
+    t.spin = 0;  // measured: suspending waits beat spinning by 2.6% on config 2 (BKT_TC_SPIN: 1 MMA, 2 epilogue)
     t.ctr = R.counters ? ctx->tc_ctr : nullptr;
     t.sub_w = ctx->sub_w;
-    if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e) != 0;
+    if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e);
     if (std::getenv("BKT_TC_DEBUG") && R.leafscan_launches == 5) {
       // per-chunk timestamps of CTA 0 in the 6th leafscan launch (a steady-state round)
       static long long* dbg = nullptr;

@@ -92,7 +92,7 @@ struct TcArgs {
   float* kth;                  // per query: current k-th distance (== key_dist(keys[k-1]))
   int d;                       // real dimensionality
   int qstride;                 // row stride of the query block (kernel D of the direct path)
-  int spin;                    // 1: MMA/epilogue warps spin on mbarriers instead of suspending
+  int spin;                    // bit 0: the MMA warp, bit 1: the epilogue spins on mbarriers instead of suspending
   int tree_smem;               // 1: the top tree's split values are copied to shared memory
   int sub_w;                   // home-round sub-buckets per leaf (tile records carry the sub-bucket)
   long long* dbg;              // diagnostics (BKT_TC_DEBUG): per-chunk timestamps of CTA 0
@@ -442,13 +442,13 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
       for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x, ++tt) {
         const TcTile T = tc_tile_info<kTcRows>(A, t);
         const uint32_t ab = tt & 1u;
-        if (A.spin) mbar_wait_spin(&afull[ab], (tt >> 1) & 1u); else mbar_wait(&afull[ab], (tt >> 1) & 1u);
+        if (A.spin & 1) mbar_wait_spin(&afull[ab], (tt >> 1) & 1u); else mbar_wait(&afull[ab], (tt >> 1) & 1u);
         tc_fence_after();
         for (int i = 0; i < T.nchunks; ++i) {
           const int c = tc_chunk_at(i, T.c0, T.nchunks);
           const int s = g % kTcStages;
           const uint32_t b = g % kTcBufs, use = g / kTcBufs;
-          if (A.spin) {
+          if (A.spin & 1) {
             mbar_wait_spin(&full[s], (g / kTcStages) & 1u);
             if (use > 0) mbar_wait_spin(&tempty[b], (use - 1) & 1u);
           } else {
@@ -637,11 +637,10 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         }
       };
 
-      // filter one 32-column group of TMEM values, then re-evaluate survivors
+      // survivors of one 32-column group of TMEM values (the caller has seen a
+      // lane's group minimum pass the filter): bitmask, exact re-evaluation
       auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
-        const float mn = min32(v);
         if constexpr (kTcDiag) c_grp += 1;
-        if (!__any_sync(0xffffffffu, mn <= thr)) return;
         uint32_t mask = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) <= thr ? 1u : 0u) << j;
@@ -704,7 +703,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         // alone, which waits for full[s] itself; most chunks have none.
         // Skipping a phase is safe: the producer cannot refill stage s
         // before this warp's empty[s] arrival below.
-        if (A.spin) mbar_wait_spin(&tfull[b], (g / kTcBufs) & 1u);
+        if (A.spin & 2) mbar_wait_spin(&tfull[b], (g / kTcBufs) & 1u);
         else mbar_wait(&tfull[b], (g / kTcBufs) & 1u);
         tc_fence_after();
         const long long te1 = kTcDiag ? clock64() : 0;
@@ -747,35 +746,50 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         // here; a chunk with a candidate is re-read group by group (pass 2).
         first_chunk = false;
         const bool dbg_on = kTcDiag && A.dbg && blockIdx.x == 0 && tid == 0 && (int)g < A.dbg_cap;
-        float mchunk;
+        // per-group minima stay in registers: pass 2 re-reads only the groups
+        // in which some lane has a candidate (thr only decreases meanwhile)
+        constexpr int kGrp = NR / 32;
+        float gmn[kGrp];
         tmem_ld32_async(tbase, va);
         if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
         tmem_wait(va);
         tmem_touch(vb);
         if (dbg_on) A.dbg[16 * g + 7] = clock64();
-        mchunk = min32(va);
-        if (ngrp > 1) mchunk = fminf(mchunk, min32(vb));
-        if constexpr (NR > 64) {
-#pragma unroll 1
-          for (int gp = 2; gp < ngrp; gp += 2) {
+        const float kInf = __int_as_float(0x7f800000);
+        gmn[0] = min32(va);
+        gmn[1] = ngrp > 1 ? min32(vb) : kInf;
+#pragma unroll
+        for (int gp = 2; gp < kGrp; gp += 2) {
+          if (gp < ngrp) {
             tmem_ld32_async(tbase + 32 * gp, va);
             if (gp + 1 < ngrp) tmem_ld32_async(tbase + 32 * (gp + 1), vb);
             tmem_wait(va);
             tmem_touch(vb);
-            mchunk = fminf(mchunk, min32(va));
-            if (gp + 1 < ngrp) mchunk = fminf(mchunk, min32(vb));
+            gmn[gp] = min32(va);
+            gmn[gp + 1] = gp + 1 < ngrp ? min32(vb) : kInf;
+          } else {
+            gmn[gp] = kInf;
+            gmn[gp + 1] = kInf;
           }
         }
+        float mchunk = gmn[0];
+#pragma unroll
+        for (int gi = 1; gi < kGrp; ++gi) mchunk = fminf(mchunk, gmn[gi]);
         if (dbg_on) A.dbg[16 * g + 8] = clock64();
         if (__any_sync(0xffffffffu, mchunk <= thr)) {
           mbar_wait(&full[s], (g / kTcStages) & 1u);
           if (NR == 64) {
             // both groups are still in registers
-            process(va, 0, s);
-            if (ngrp > 1) process(vb, 32, s);
+            if (__any_sync(0xffffffffu, gmn[0] <= thr)) process(va, 0, s);
+            if (__any_sync(0xffffffffu, gmn[1] <= thr)) process(vb, 32, s);
           } else {
 #pragma unroll 1
             for (int gi = 0; gi < ngrp; ++gi) {
+              // static-index select (no local-memory array), one process() call site
+              float gv = gmn[0];
+#pragma unroll
+              for (int j = 1; j < kGrp; ++j) gv = gi == j ? gmn[j] : gv;
+              if (!__any_sync(0xffffffffu, gv <= thr)) continue;
               tmem_ld32_async(tbase + 32 * gi, va);
               tmem_wait(va);
               process(va, 32 * gi, s);

@@ -849,6 +849,8 @@ struct SearchRun {
   bool seq = false;
   long long seq_cap = 0;
   bool counters = false;
+  unsigned long long* ctr_rounds = nullptr;  // BKT_TRACE_ROUNDS + counters: a 16-counter snapshot per leafscan launch
+  int ctr_rounds_cap = 0;
   // early result drain (single batch, host results): when at most drain_at
   // queries remain active, snapshot them and start copying every row to the
   // host while the tail rounds run; drain_start() launches the copy
@@ -913,8 +915,9 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.ctr = R.counters ? ctx->tc_ctr : nullptr;
     t.sub_w = ctx->sub_w;
     if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e);
-    if (std::getenv("BKT_TC_DEBUG") && R.leafscan_launches == 5) {
-      // per-chunk timestamps of CTA 0 in the 6th leafscan launch (a steady-state round)
+    const char* dbg_env = std::getenv("BKT_TC_DEBUG");
+    if (dbg_env && R.leafscan_launches == (std::atoi(dbg_env) > 1 ? std::atoi(dbg_env) : 5)) {
+      // per-chunk timestamps of CTA 0 in one leafscan launch (BKT_TC_DEBUG=<launch>, default the 6th)
       static long long* dbg = nullptr;
       const int cap = 4096;
       if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * cap);
@@ -938,6 +941,9 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
       return BKT_OK;
     }
     CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows, R.tc_cps));
+    if (R.ctr_rounds && R.leafscan_launches < R.ctr_rounds_cap)
+      CU(cudaMemcpyAsync(R.ctr_rounds + 16 * R.leafscan_launches, ctx->tc_ctr, sizeof(unsigned long long) * 16,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
   } else {
     CU(launch_leafscan(ctx->D, R.kb, R.fma, R.grid_scan, ctx->stream, a, nullptr));
   }
@@ -1201,6 +1207,10 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     CU(cudaMemsetAsync(ctx->tc_ctr, 0, sizeof(unsigned long long) * 16, ctx->stream));
   }
   R.counters = counters;
+  if (counters && std::getenv("BKT_TRACE_ROUNDS")) {
+    R.ctr_rounds_cap = kHistCap;
+    CU(cudaMalloc(&R.ctr_rounds, sizeof(unsigned long long) * 16 * R.ctr_rounds_cap));
+  }
 
   // Host I/O pipeline: with host-resident queries or results and at least two
   // batches, batch b+1's queries stream in (io set 0, its own host thread and
@@ -1416,9 +1426,26 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     std::vector<int> hist(std::min<long long>(kHistCap, per_launch.size()));
     CU(cudaMemcpy(hist.data(), ctx->hist, sizeof(int) * hist.size(), cudaMemcpyDeviceToHost));
     size_t off = per_launch.size() - hist.size();
-    for (size_t r = 0; r < hist.size(); ++r)
-      std::fprintf(stderr, "round %zu active %d leafscan_ms %.4f\n", r, hist[r], per_launch[off + r]);
+    std::vector<unsigned long long> cr;
+    if (R.ctr_rounds) {
+      cr.resize(16 * (size_t)std::min<long long>(R.ctr_rounds_cap, R.leafscan_launches));
+      CU(cudaMemcpy(cr.data(), R.ctr_rounds, sizeof(unsigned long long) * cr.size(), cudaMemcpyDeviceToHost));
+    }
+    for (size_t r = 0; r < hist.size(); ++r) {
+      std::fprintf(stderr, "round %zu active %d leafscan_ms %.4f", r, hist[r], per_launch[off + r]);
+      if (off == 0 && 16 * (r + 1) <= cr.size()) {
+        // counter deltas of this round's launch (same fields as "tc counters")
+        const unsigned long long* c1 = &cr[16 * r];
+        unsigned long long c0[16] = {};
+        if (r > 0) std::copy(&cr[16 * (r - 1)], &cr[16 * r], c0);
+        std::fprintf(stderr, " groups %llu any %llu survivors %llu trips %llu merges %llu tiles %llu queries %llu first %llu inserted %llu",
+                     c1[0] - c0[0], c1[1] - c0[1], c1[2] - c0[2], c1[3] - c0[3], c1[4] - c0[4], c1[5] - c0[5],
+                     c1[6] - c0[6], c1[7] - c0[7], c1[8] - c0[8]);
+      }
+      std::fprintf(stderr, "\n");
+    }
   }
+  if (R.ctr_rounds) cudaFree(R.ctr_rounds);
   st.rounds = R.rounds;
   st.leaf_visits = R.scans;
   st.pairs = (int64_t)pairs;

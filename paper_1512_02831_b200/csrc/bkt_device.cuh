@@ -144,15 +144,8 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
 // ----------------------------------------------------------------------------
 // warp-aggregated atomics
 // ----------------------------------------------------------------------------
-// Add 1 to counter[key] for every active lane; lanes sharing a key are
-// combined into one atomic by their leader.
-__device__ __forceinline__ void warp_count(int* counter, int key) {
-  unsigned mask = __activemask();
-  unsigned peers = __match_any_sync(mask, key);
-  int leader = __ffs(peers) - 1;
-  if ((int)(threadIdx.x & 31) == leader) atomicAdd(counter + key, __popc(peers));
-}
-// Reserve one slot per lane in bucket `key`; returns this lane's slot.
+// Reserve one slot per lane in bucket `key` (lanes sharing a key are combined
+// into one atomic by their leader); returns this lane's slot.
 __device__ __forceinline__ int warp_reserve(int* cursor, int key) {
   unsigned mask = __activemask();
   unsigned peers = __match_any_sync(mask, key);

@@ -14,7 +14,7 @@
 //   pts        f32[total_quads * 4 * D]         quad g, dim j, point t at g*4D + 4j + t
 //   pidx       u32[total_quads * 4]             original row of each point (padding: 0xFFFFFFFF)
 //   per batch of m queries: q f32[m*D], keys u64[m*k], state u32[m], next i32[m],
-//   visits u32[m], two work lists i32[m]; per leaf: counts, cursor, leaf_off, tile_off.
+//   visits u32[m], bucket slot (rank) i32[m], two work lists i32[m]; per leaf: counts, leaf_off, tile_off.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -120,9 +120,9 @@ struct bkt_ctx {
   int cap_nl = 0;
   int cap_keys = 0;
   int* counts = nullptr;    // per bucket key
-  int* cursor = nullptr;    // per bucket key
   int* key_off = nullptr;   // nkeys + 1: first work-list slot of each key
   int* qkey = nullptr;      // per query: bucket key of its next leaf visit
+  int* rank = nullptr;      // per query: slot in its next bucket (taken when counted)
   int* leaf_off = nullptr;
   int* tile_off = nullptr;
   int4* tiles = nullptr;    // per-tile records (capacity tiles_cap)
@@ -250,6 +250,7 @@ void free_work(bkt_ctx* c) {
   c->tiles_cap = 0;
   dfree(c->kthv);
   dfree(c->qkey);
+  dfree(c->rank);
   dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
   dfree(c->work[0]); dfree(c->work[1]);
   c->cap_m = 0; c->cap_k = 0;
@@ -269,7 +270,7 @@ int ensure_alt(bkt_ctx* ctx, long long m, int k) {
 }
 
 void free_leafbufs(bkt_ctx* c) {
-  dfree(c->counts); dfree(c->cursor); dfree(c->key_off); dfree(c->leaf_off); dfree(c->tile_off);
+  dfree(c->counts); dfree(c->key_off); dfree(c->leaf_off); dfree(c->tile_off);
   hfree(c->h_tile_off);
   c->cap_nl = 0;
   c->cap_keys = 0;
@@ -280,10 +281,8 @@ int ensure_leafbufs(bkt_ctx* ctx, int nl, int nkeys) {
   if (ctx->cap_nl >= nl && ctx->cap_keys >= nkeys) return BKT_OK;
   free_leafbufs(ctx);
   CU(cudaMalloc(&ctx->counts, sizeof(int) * nkeys));
-  CU(cudaMalloc(&ctx->cursor, sizeof(int) * nkeys));
   CU(cudaMalloc(&ctx->key_off, sizeof(int) * (nkeys + 1)));
   CU(cudaMemset(ctx->counts, 0, sizeof(int) * nkeys));
-  CU(cudaMemset(ctx->cursor, 0, sizeof(int) * nkeys));
   CU(cudaMalloc(&ctx->leaf_off, sizeof(int) * (nl + 1)));
   CU(cudaMalloc(&ctx->tile_off, sizeof(int) * (nl + 1)));
   CU(cudaHostAlloc(&ctx->h_tile_off, sizeof(int) * (nl + 1), cudaHostAllocDefault));
@@ -305,6 +304,7 @@ int ensure_work(bkt_ctx* ctx, long long m, int k) {
   CU(cudaMalloc(&ctx->visits, sizeof(uint32_t) * M));
   CU(cudaMalloc(&ctx->kthv, sizeof(float) * M));
   CU(cudaMalloc(&ctx->qkey, sizeof(int) * M));
+  CU(cudaMalloc(&ctx->rank, sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[0], sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[1], sizeof(int) * M));
   ctx->tiles_cap = M / kNT + (1ll << ctx->h) + 1;
@@ -874,6 +874,7 @@ ScanArgs make_scan_args(bkt_ctx* ctx, SearchRun& R, int cur) {
   a.tile_hi = -1;
   a.tiles = ctx->tiles;
   a.counts = ctx->counts;
+  a.rank = ctx->rank;
   a.pts = ctx->pts;
   a.pidx = ctx->pidx;
   a.quad_origin = 0;
@@ -1017,7 +1018,7 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
   // FindLeaf after every chunk of the round has been scanned
   findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
       ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys, ctx->state,
-      ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+      ctx->next, ctx->visits, ctx->counts, ctx->rank, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
   CU(cudaGetLastError());
   R.launches++;
   return BKT_OK;
@@ -1031,12 +1032,11 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
   init.active = (int)m;
   CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
-  CU(cudaMemsetAsync(ctx->cursor, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
   start_kernel<<<R.grid_small, kStartQ, start_smem_bytes(ctx->h, ctx->D), ctx->stream>>>(
       ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
                                                        ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
                                                        R.seq_cap, ctx->kthv, ctx->blk_base, ctx->nodes, ctx->sub_w,
-                                                       ctx->qkey, ctx->counts);
+                                                       ctx->qkey, ctx->counts, ctx->rank);
   CU(cudaGetLastError());
   R.launches++;
 
@@ -1051,9 +1051,8 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
     // home visits (round 0) are sub-bucketed per block; later rounds key by leaf only
     const int sw = round == 0 ? ctx->sub_w : 1;
     plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, sw, ctx->nl * sw,
-                                                     ctx->leaf_off, ctx->tile_off, ctx->cursor, ctx->ctl, ctx->nl, kNT,
-                                                     ctx->hist, kHistCap, ctx->tiles,
-                                                     (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
+                                                     ctx->leaf_off, ctx->tile_off, ctx->ctl, ctx->nl, kNT,
+                                                     ctx->hist, kHistCap);
     CU(cudaGetLastError());
     R.launches++;
     const int slot = (int)(round % kRing);
@@ -1065,8 +1064,10 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       if (ctx->h_ctl[slot].active == 0) break;
     }
     scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->next,
-                                                           ctx->qkey, ctx->key_off, ctx->cursor, ctx->work[cur],
-                                                           ctx->ctl);
+                                                           ctx->qkey, ctx->key_off, ctx->rank, ctx->work[cur],
+                                                           ctx->ctl, ctx->leaf_off, ctx->tile_off, ctx->nl, sw, kNT,
+                                                           ctx->tiles,
+                                                           (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
     CU(cudaGetLastError());
     R.launches++;
     if (ooc) {
@@ -1083,7 +1084,8 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
         // then overlap across many warps instead of stalling the scan's epilogue
         findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
             ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys,
-            ctx->state, ctx->next, ctx->visits, ctx->counts, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+            ctx->state, ctx->next, ctx->visits, ctx->counts, ctx->rank, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
+            R.seq_cap);
         CU(cudaGetLastError());
         R.launches++;
       }

@@ -44,6 +44,7 @@ struct ScanArgs {
   int tile_lo, tile_hi;  // chunk mode: tile sub-range; tile_hi < 0 = [0, *num_tiles)
   const int4* tiles;     // per-tile {leaf, qbeg, qcnt} written by plan_kernel
   int* counts;           // nl: next-round histogram (fused epilogue)
+  int* rank;             // m: a query's slot in its next-round bucket (taken when counted)
   // leaf structure, quad-interleaved: quad g, dim j, point t at pts[(g - quad_origin)*4D + 4j + t]
   const float* pts;
   const uint32_t* pidx;  // original index of point (g - quad_origin)*4 + t (padding: 0xFFFFFFFF)
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, (ScanOcc<D, KB>::kMinBlocks)) leafsc
           uint32_t v = a.visits[qi] + 1;
           a.visits[qi] = v;
           log_visit(a, qi, v, nxt);
-          warp_count(a.counts, nxt);  // next round's bucket (key = leaf)
+          a.rank[qi] = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
         }
       }
     }

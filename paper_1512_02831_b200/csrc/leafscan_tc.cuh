@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
             const uint32_t vv = cu.vis + 1;
             a.visits[qi] = vv;
             log_visit(a, qi, vv, nxt);
-            warp_count(a.counts, nxt);  // next round's bucket (key = leaf)
+            a.rank[qi] = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
             }
         }
       }

@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(kStartQ) start_kernel(const float* __restrict_
                                                         unsigned long long* seq_pos, long long seq_cap,
                                                         float* __restrict__ kth, const int* __restrict__ blk_base,
                                                         const int4* __restrict__ nodes, int sub_w,
-                                                        int* __restrict__ qkey, int* __restrict__ counts) {
+                                                        int* __restrict__ qkey, int* __restrict__ counts,
+                                                        int* __restrict__ rank) {
   extern __shared__ float s_start[];
   const int ntree = start_tree_n(top.h, D);
   float* s_split = s_start;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kStartQ) start_kernel(const float* __restrict_
     }
     const int key = (int)leaf * sub_w + sub;
     qkey[i] = key;
-    warp_count(counts, key);
+    rank[i] = warp_reserve(counts, key);
   }
 }
 
@@ -174,15 +175,14 @@ __device__ __forceinline__ void block_scan2(long long& a, long long& b, long lon
   __syncthreads();
 }
 
-// counts -> key_off, leaf_off, tile_off + per-tile records; resets counts and
-// cursors; updates ctl.  One CTA of kPlanThreads threads; each thread owns a
-// contiguous run of keys (phase 1) and of leaves (phase 2).
+// counts -> key_off, leaf_off, tile_off; resets counts; updates ctl.  One CTA
+// of kPlanThreads threads; each thread owns a contiguous run of keys (phase 1)
+// and of leaves (phase 2).  The per-tile records are written by scatter_kernel.
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ counts, int* __restrict__ key_off,
                                                             int sub_w, int nkeys,
                                                             int* __restrict__ leaf_off, int* __restrict__ tile_off,
-                                                            int* __restrict__ cursor, RoundCtl* ctl, int nl,
-                                                            int tile_q, int* hist, int hist_cap, int4* tiles,
-                                                            int tiles_cap) {
+                                                            RoundCtl* ctl, int nl, int tile_q, int* hist,
+                                                            int hist_cap) {
   long long tot_c, tot_t;
   {
     const int per = (nkeys + kPlanThreads - 1) / kPlanThreads;
@@ -195,7 +195,6 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
       key_off[e] = (int)ec;
       ec += counts[e];
       counts[e] = 0;
-      cursor[e] = 0;
     }
     if (threadIdx.x == 0) key_off[nkeys] = (int)tot_c;
   }
@@ -214,18 +213,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
     const int c = key_off[(l + 1) * sub_w] - ec;
     leaf_off[l] = ec;
     tile_off[l] = (int)et;
-    // per-tile records {leaf, first work-list slot, query count, sub-bucket of
-    // the first query (its block for a home-leaf visit)}: one load per tile in
-    // the scan kernels
-    const int nt = (c + tile_q - 1) / tile_q;
-    const int kb0 = l * sub_w, kb1 = (l + 1) * sub_w;
-    int e = kb0;
-    for (int j = 0; j < nt && et + j < tiles_cap; ++j) {
-      const int p = ec + j * tile_q;
-      while (e + 1 < kb1 && key_off[e + 1] <= p) ++e;
-      tiles[et + j] = make_int4(l, p, min(tile_q, c - j * tile_q), e - kb0);
-    }
-    et += nt;
+    et += (c + tile_q - 1) / tile_q;
   }
   if (threadIdx.x == 0) {
     leaf_off[nl] = (int)tot_c;
@@ -242,19 +230,43 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
 }
 
 // Place every still-active query of the previous work list into its key's
-// slice of the new list.  identity: previous list is 0..prev_active-1.
+// slice of the new list, at the slot it took when it was counted (rank), and
+// write the round's per-tile records {leaf, first work-list slot, query
+// count, sub-bucket of the first query (its block for a home-leaf visit)}.
+// identity: previous list is 0..prev_active-1.  No atomics.
 __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const int* __restrict__ next,
                                const int* __restrict__ qkey, const int* __restrict__ key_off,
-                               int* __restrict__ cursor, int* __restrict__ work, const RoundCtl* ctl) {
+                               const int* __restrict__ rank, int* __restrict__ work, const RoundCtl* ctl,
+                               const int* __restrict__ leaf_off, const int* __restrict__ tile_off, int nl, int sub_w,
+                               int tile_q, int4* __restrict__ tiles, int tiles_cap) {
   const int n = ctl->prev_active;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    int qi = identity ? i : prev[i];
-    const int leaf = next[qi];
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    int qi = identity ? i : __ldg(prev + i);
+    const int leaf = __ldg(next + qi);
     if (leaf >= 0) {
-      const int key = identity ? qkey[qi] : leaf;  // home round: (leaf, block) keys
-      int pos = warp_reserve(cursor, key);
-      work[key_off[key] + pos] = qi;
+      const int key = identity ? __ldg(qkey + qi) : leaf;  // home round: (leaf, block) keys
+      work[__ldg(key_off + key) + __ldg(rank + qi)] = qi;
     }
+  }
+  const int nt = min(ctl->num_tiles, tiles_cap);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += stride) {
+    // leaf: last l with tile_off[l] <= t (binary search over nl + 1 offsets)
+    int lo = 0, hi = nl;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(tile_off + mid) <= t) lo = mid; else hi = mid;
+    }
+    const int l = lo, j = t - __ldg(tile_off + l);
+    const int ec = __ldg(leaf_off + l), c = __ldg(leaf_off + l + 1) - ec;
+    const int p = ec + j * tile_q;
+    // sub-bucket of slot p: last e in [l sub_w, (l + 1) sub_w) with key_off[e] <= p
+    int e0 = l * sub_w, e1 = e0 + sub_w;
+    while (e1 - e0 > 1) {
+      const int mid = (e0 + e1) >> 1;
+      if (__ldg(key_off + mid) <= p) e0 = mid; else e1 = mid;
+    }
+    tiles[t] = make_int4(l, p, min(tile_q, c - j * tile_q), e0 - l * sub_w);
   }
 }
 
@@ -263,8 +275,8 @@ __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const
 __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ctl, const float* __restrict__ q,
                                 int D, int k, TopTreeView top, const uint64_t* __restrict__ keys,
                                 uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
-                                int* __restrict__ counts, int* seq_log, unsigned long long* seq_pos,
-                                long long seq_cap) {
+                                int* __restrict__ counts, int* __restrict__ rank, int* seq_log,
+                                unsigned long long* seq_pos, long long seq_cap) {
   // the top tree's split values in shared memory when they fit (dynamic smem)
   extern __shared__ float s_fl_split[];
   const int ntree = start_tree_smem(top.h);
@@ -292,7 +304,7 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
           seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)v; seq_log[3 * p + 2] = nxt;
         }
       }
-      warp_count(counts, nxt);  // next round's bucket (key = leaf)
+      rank[qi] = warp_reserve(counts, nxt);  // next round's bucket (key = leaf) and slot
     }
   }
 }

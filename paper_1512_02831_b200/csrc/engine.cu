@@ -855,6 +855,7 @@ struct SearchRun {
   // queries remain active, snapshot them and start copying every row to the
   // host while the tail rounds run; drain_start() launches the copy
   long long drain_at = -1;
+  long long finish_at = -1;  // tail finisher: one launch once at most this many queries remain (-1: off)
   bool drain_fired = false;
   std::function<void()> drain_start;
 };
@@ -1097,6 +1098,24 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       const int chk = (int)((round - (kRing - 1)) % kRing);
       CU(cudaEventSynchronize(ring[chk]));
       if (ctx->h_ctl[chk].active == 0) break;
+      if (R.finish_at >= 0 && ctx->h_ctl[chk].active <= R.finish_at) {
+        // the list just scanned (work[cur ^ 1], ctl->active entries) holds
+        // every query that is still active; finish them in one launch
+        const int blocks = (int)std::max<long long>(1, (R.finish_at + kFinishWarps - 1) / kFinishWarps);
+        const TopTreeView top{ctx->split, ctx->h, ctx->d};
+        int* seq = R.seq ? ctx->seq_dev : nullptr;
+        if (R.fma)
+          finish_kernel<true><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
+              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        else
+          finish_kernel<false><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
+              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        CU(cudaGetLastError());
+        R.launches++;
+        break;
+      }
       if (R.drain_at >= 0 && !R.drain_fired && ctx->h_ctl[chk].active <= R.drain_at) {
         // the list just scanned holds every query that can still change
         snapshot_active<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], ctx->ctl, ctx->qkey);
@@ -1170,6 +1189,15 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     if (rc != BKT_OK) return rc;
   }
   R.grid_small = ctx->sm_count * 8;
+  // tail finisher (resident structure, d <= 32, k <= 64) for deep trees:
+  // one warp walks a query's remaining leaves in one launch, which beats a
+  // round per leaf when a tail of thousands of rounds over short leaves is
+  // left (config 5, h = 14: 3,751 rounds, 1.26 -> 2.02 M q/s) and loses
+  // where rounds are few or leaves long (config 1 h = 8: -2% at best;
+  // config 2: -1%; config 5 h = 11: -6%; tools/finish_sweep.py)
+  if (ctx->residency == 0 && ctx->d <= 32 && k <= 64 && ctx->h >= 12)
+    R.finish_at = std::min<long long>((long long)ctx->sm_count * 512, m / 8);
+  if (const char* e = std::getenv("BKT_FINISH_AT")) R.finish_at = std::atoll(e);
 
   // batch size: whatever fits comfortably in free memory (or the caller's choice)
   const long long per_query = 4ll * ctx->D + 4ll * ctx->d + 8ll * k + 4 * 5;

@@ -11,11 +11,14 @@
 //             "buffers" of QueryBuffers.drain_all, buffer_tree.py:420-430, in
 //             leaf order; inside a leaf, ordered by block).
 //   scatter : counting-sort placement of the still-active queries into their
-//             key's slice with warp-aggregated atomics (the reference's
+//             key's slice at the slot taken when counted (the reference's
 //             stable argsort + insert_many, buffer_tree.py:603-619).  DONE
 //             queries drop out (buffer_tree.py:482-485).
 //   findleaf: unfused FindLeaf for the out-of-core path (leafscan fuses it
 //             when the whole leaf structure is resident).
+//   finish  : the tail -- once few queries remain, one warp per query runs
+//             the rest of its traversal (leaf scan, top-k, FindLeaf) in a
+//             single launch instead of one round per remaining leaf.
 #pragma once
 #include "bkt_device.cuh"
 
@@ -316,6 +319,122 @@ __global__ void pad_rows_kernel(const float* __restrict__ src, int d, float* __r
     long long i = t / D;
     int j = (int)(t - i * D);
     dst[t] = (j < d) ? src[i * d + j] : 0.0f;
+  }
+}
+
+// Tail finisher.  Warp w takes the queries work[w], work[w + W], ... of the
+// round just scanned (length ctl->active); a query with a next leaf runs
+// the rest of its traversal here: scan the leaf (lanes stride over its
+// quads, reference arithmetic core.py:108-122, FMA variant when !exact),
+// insert every candidate whose key beats the current k-th key into the
+// warp's sorted top-k row (shared memory), then FindLeaf with the new k-th
+// distance (buffer_tree.py:330-349) -- the same per-visit semantics as a
+// round (the top-k after a visit is the best k of the list and the leaf), so
+// results, visit counts, pairs and leaf sequences are unchanged.
+constexpr int kFinishWarps = 8;
+template <bool FMA>
+__global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(
+    const int* __restrict__ work, RoundCtl* ctl, const float* __restrict__ q, int D, int k, TopTreeView top,
+    uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
+    const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base,
+    const int* __restrict__ leaf_size, unsigned long long* pairs, int* seq_log, unsigned long long* seq_pos,
+    long long seq_cap) {
+  __shared__ uint64_t s_row[kFinishWarps][64];
+  __shared__ float s_q[kFinishWarps][32];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int d = top.d;
+  uint64_t* row = s_row[wl];
+  float* sq = s_q[wl];
+  const int n = ctl->active;
+  const int nw = gridDim.x * kFinishWarps;
+  unsigned long long pairs_acc = 0, scans_acc = 0;
+  for (int i = blockIdx.x * kFinishWarps + wl; i < n; i += nw) {
+    const int qi = __ldg(work + i);
+    int leaf = next[qi];
+    if (leaf < 0) continue;
+    if (lane < d) sq[lane] = __ldg(q + (long long)qi * D + lane);
+    uint64_t* kp = keys + (long long)qi * k;
+    for (int j = lane; j < k; j += 32) row[j] = kp[j];
+    __syncwarp();
+    float qv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) qv[j] = j < d ? sq[j] : 0.0f;
+    uint32_t st = state[qi];
+    uint32_t lf = st & 0xFFFFu, pend = st >> 16;
+    uint32_t vis = visits[qi];
+    while (leaf >= 0) {
+      const long long g0 = __ldg(quad_base + leaf), g1 = __ldg(quad_base + leaf + 1);
+      uint64_t kkey = row[k - 1];
+      for (long long gb = g0; gb < g1; gb += 32) {
+        const long long g = gb + lane;
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        bool has = g < g1;
+        if (has) {
+          const float4* pq = reinterpret_cast<const float4*>(pts + g * 4 * D);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j < d) {
+              const float4 p = __ldg(pq + j);
+              const float e[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float df = __fsub_rn(qv[j], e[t]);
+                if constexpr (FMA) acc[t] = __fmaf_rn(df, df, acc[t]);
+                else acc[t] = __fadd_rn(acc[t], __fmul_rn(df, df));
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          // candidates: keys below the current k-th key (ties by original index)
+          const uint64_t key = has ? pack_key(acc[t], __ldg(pidx + g * 4 + t)) : ~0ull;
+          unsigned bal = __ballot_sync(0xffffffffu, key < kkey);
+          while (bal) {
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const uint64_t c = __shfl_sync(0xffffffffu, key, src);
+            if (lane == 0 && c < row[k - 1]) {
+              int j = k - 1;
+              while (j > 0 && row[j - 1] > c) {
+                row[j] = row[j - 1];
+                --j;
+              }
+              row[j] = c;
+            }
+            __syncwarp();
+            kkey = row[k - 1];
+          }
+        }
+      }
+      pairs_acc += (unsigned long long)__ldg(leaf_size + leaf);
+      scans_acc += 1;
+      // FindLeaf with the k-th distance after this leaf (every lane computes it)
+      const float kth = key_dist(row[k - 1]);
+      const float* sp = top.split;
+      leaf = find_next_leaf_with(top.h, d, [sp](uint32_t node) { return __ldg(sp + node); },
+                                 [sq](int j) { return sq[j]; }, kth, lf, pend);
+      if (leaf >= 0) {
+        ++vis;
+        if (seq_log && lane == 0) {
+          const unsigned long long p = atomicAdd(seq_pos, 1ull);
+          if ((long long)p < seq_cap) {
+            seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)vis; seq_log[3 * p + 2] = leaf;
+          }
+        }
+      }
+    }
+    for (int j = lane; j < k; j += 32) kp[j] = row[j];
+    if (lane == 0) {
+      state[qi] = (pend << 16) | lf;
+      next[qi] = -1;
+      visits[qi] = vis;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && (pairs_acc || scans_acc)) {
+    if (pairs) atomicAdd(pairs, pairs_acc);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->scans), scans_acc);
   }
 }
 

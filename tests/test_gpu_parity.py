@@ -361,3 +361,47 @@ def test_tensor_core_variants_exact(knn_golden, gpu_device, env, monkeypatch):
         tree = bkt.build_buffer_tree(c["refs"], s["h"])
         res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, kernel="tc")
         assert np.array_equal(res.keys, c["keys"]), (env, s)
+
+
+@pytest.mark.parametrize("finish_at", ["-1", "1000000000"])
+@pytest.mark.parametrize("kernel", ["direct", "tc"])
+def test_tail_finisher_on_and_off_exact(knn_golden, gpu_device, kernel, finish_at, monkeypatch):
+    """The tail finisher (one warp per remaining query, one launch) and the
+    plain round loop give the reference's keys, visit counts, leaf sequences
+    and scan events: off entirely (-1) and taking over from the first
+    round check (1e9)."""
+    monkeypatch.setenv("BKT_FINISH_AT", finish_at)
+    for c in knn_golden:
+        s = c["spec"]
+        tree = bkt.build_buffer_tree(c["refs"], s["h"])
+        stats = bkt.SearchStats(record_sequences=True)
+        res = bkt.lazy_search(tree, c["queries"], bkt.SearchParams(k=s["k"]), device=gpu_device, stats=stats,
+                              kernel=kernel)
+        assert np.array_equal(res.keys, c["keys"]), (finish_at, s)
+        assert np.array_equal(stats.visited_per_query, c["visited"]), (finish_at, s)
+        flat = np.concatenate([np.asarray(x, np.int64) for x in stats.leaf_sequences])
+        assert np.array_equal(flat, c["seq"]), (finish_at, s)
+        assert stats.leaf_scan_events == int(c["visited"].sum())
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_tail_finisher_mixture(gpu_device, exact, monkeypatch):
+    """A config-2-like mixture: the finisher taking over at different points
+    gives the same keys, visit counts and scan events as the round loop
+    without it, in both arithmetic modes."""
+    rng = np.random.default_rng(5)
+    centers = rng.random((8, 10))
+    pts = (centers[rng.integers(0, 8, 220_000)] + rng.normal(0, 0.05, (220_000, 10))).astype(np.float32)
+    refs, queries = pts[:200_000], pts[200_000:]
+    tree = bkt.build_buffer_tree(refs, 7)
+    out = []
+    for fa in ("-1", "5000", "1000000000"):
+        monkeypatch.setenv("BKT_FINISH_AT", fa)
+        stats = bkt.SearchStats()
+        res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=10), device=gpu_device, stats=stats, exact=exact)
+        out.append((res.keys, stats.visited_per_query, stats.leaf_scan_events))
+    for keys, vis, ev in out[1:]:
+        assert np.array_equal(keys, out[0][0]) and np.array_equal(vis, out[0][1]) and ev == out[0][2]
+    if exact:
+        sample = np.arange(0, queries.shape[0], 97)
+        assert np.array_equal(out[0][0][sample], O.brute_keys(refs, queries[sample], 10))

@@ -278,6 +278,8 @@ def main() -> None:
             barrier()
             if i >= e2e_warm:
                 tot += w1 - w0
+            if os.environ.get("BKT_BENCH_DEBUG"):
+                print(f"e2e call {i}: {1e3 * (w1 - w0):.1f} ms", file=sys.stderr, flush=True)
         e2e_local = e2e_steps * m / tot
         e2e = {"value": e2e_local, "unit": UNIT, "h2d_bytes_per_step": int(m * DIM * 4),
                "d2h_bytes_per_step": int(m * K * 8)}

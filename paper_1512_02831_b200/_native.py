@@ -148,13 +148,21 @@ class _PinnedPool:
         self._filling: set[int] = set()
 
     def _fill(self, nbytes: int) -> None:
-        try:
-            addr = lib().bkt_host_alloc(nbytes)
-        except Exception:  # pragma: no cover - no driver
-            addr = None
-        with self._lock:
-            self._filling.discard(nbytes)
-            if addr:
+        # page-lock buffers of this size one after another up to `per_size`
+        # (a caller that keeps its previous result alive needs two)
+        while True:
+            with self._lock:
+                if self._held + nbytes > self._max or self._count.get(nbytes, 0) >= self._per_size:
+                    self._filling.discard(nbytes)
+                    return
+            try:
+                addr = lib().bkt_host_alloc(nbytes)
+            except Exception:  # pragma: no cover - no driver
+                addr = None
+            with self._lock:
+                if not addr:
+                    self._filling.discard(nbytes)
+                    return
                 self._held += nbytes
                 self._count[nbytes] = self._count.get(nbytes, 0) + 1
                 self._free.setdefault(nbytes, []).append(addr)
@@ -162,9 +170,9 @@ class _PinnedPool:
     def take(self, nbytes: int):
         # A free buffer of this size is handed out at once.  Otherwise the
         # caller gets ordinary memory now and a buffer is page-locked in the
-        # background (cudaHostAlloc costs ~0.4 s per 800 MB), at most
-        # `per_size` per size: a caller that keeps many results alive (a
-        # stream) never waits for the allocation.
+        # background (cudaHostAlloc costs ~0.4 s per 800 MB), up to
+        # `per_size` per size in one go: a caller that keeps many results
+        # alive (a stream) never waits for the allocation.
         with self._lock:
             lst = self._free.get(nbytes)
             if lst:

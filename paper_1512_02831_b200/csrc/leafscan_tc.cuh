@@ -637,6 +637,13 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         }
       };
 
+      // this query's coordinates for survivor re-evaluation: loaded once per
+      // chunk that has survivors (pass 2), not once per survivor
+      float qv[KT - 1];
+      auto load_qv = [&]() {
+#pragma unroll
+        for (int jj = 0; jj < KT - 1; ++jj) qv[jj] = jj < d ? sq[jj * 128] : 0.0f;
+      };
       // survivors of one 32-column group of TMEM values (the caller has seen a
       // lane's group minimum pass the filter): bitmask, exact re-evaluation
       auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
@@ -659,12 +666,9 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
             const float* pp = prow + j * d;
             // unrolled to KT - 1 >= d with predication: every shared load issues
             // up front, only the (ordered) accumulation chain stays serial
-            float qv[KT - 1], pv[KT - 1];
+            float pv[KT - 1];
 #pragma unroll
-            for (int jj = 0; jj < KT - 1; ++jj) {
-              qv[jj] = jj < d ? sq[jj * 128] : 0.0f;
-              pv[jj] = jj < d ? pp[jj] : 0.0f;
-            }
+            for (int jj = 0; jj < KT - 1; ++jj) pv[jj] = jj < d ? pp[jj] : 0.0f;
             float acc = 0.0f;
 #pragma unroll
             for (int jj = 0; jj < KT - 1; ++jj) {
@@ -778,6 +782,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         if (dbg_on) A.dbg[16 * g + 8] = clock64();
         if (__any_sync(0xffffffffu, mchunk <= thr)) {
           mbar_wait(&full[s], (g / kTcStages) & 1u);
+          load_qv();
           if (NR == 64) {
             // both groups are still in registers
             if (__any_sync(0xffffffffu, gmn[0] <= thr)) process(va, 0, s);

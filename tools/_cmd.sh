@@ -1,1 +1,5 @@
-BKT_BENCH_DEBUG=1 timeout 600 python bench.py --no-cpu 2>&1 | grep -E "e2e call|^\{" | cut -c1-120; timeout 300 python -m pytest tests -m gpu -q -k "pinned or pool" 2>&1 | tail -2
+for r in 1 2; do
+bash tools/quickbench.sh base$r BKT_LIB_NAME=libbkt_base.so
+bash tools/quickbench.sh qv$r
+done
+timeout 600 python -m pytest tests -m gpu -x -q -k "golden or tensor_core or config2 or mixture" 2>&1 | tail -2

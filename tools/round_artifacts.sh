@@ -16,6 +16,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:leaf
   python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > /dev/null 2>&1
 python tools/ncu_summary.py $out/leafscan_full.ncu-rep > $out/ncu_leafscan_full.txt 2>&1
 for c in cfg1 cfg4; do timeout 900 python tools/configs.py $c > $out/$c.jsonl 2> $out/$c.err; done
+timeout 600 python tools/finish_sweep.py --at=-1,default > $out/finish_sweep.jsonl 2>&1
 timeout 900 python tools/configs.py cfg3 --m 1e8 > $out/cfg3.jsonl 2> $out/cfg3.err
 timeout 1200 python tools/configs.py cfg5 --m 1e6 > $out/cfg5.jsonl 2> $out/cfg5.err
 echo done

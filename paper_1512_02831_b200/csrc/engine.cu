@@ -856,6 +856,7 @@ struct SearchRun {
   // host while the tail rounds run; drain_start() launches the copy
   long long drain_at = -1;
   long long finish_at = -1;  // tail finisher: one launch once at most this many queries remain (-1: off)
+  bool finish_cta = false;   // finisher with one CTA per query (else one warp per query)
   bool drain_fired = false;
   std::function<void()> drain_start;
 };
@@ -1104,7 +1105,16 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
         const int blocks = (int)std::max<long long>(1, (R.finish_at + kFinishWarps - 1) / kFinishWarps);
         const TopTreeView top{ctx->split, ctx->h, ctx->d};
         int* seq = R.seq ? ctx->seq_dev : nullptr;
-        if (R.fma)
+        const int cta_blocks = (int)std::max<long long>(1, std::min<long long>(R.finish_at, ctx->sm_count * 8ll));
+        if (R.finish_cta && R.fma)
+          finish_cta_kernel<true><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
+              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        else if (R.finish_cta)
+          finish_cta_kernel<false><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
+              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        else if (R.fma)
           finish_kernel<true><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
               ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
               ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
@@ -1189,15 +1199,24 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     if (rc != BKT_OK) return rc;
   }
   R.grid_small = ctx->sm_count * 8;
-  // tail finisher (resident structure, d <= 32, k <= 64) for deep trees:
-  // one warp walks a query's remaining leaves in one launch, which beats a
-  // round per leaf when a tail of thousands of rounds over short leaves is
-  // left (config 5, h = 14: 3,751 rounds, 1.26 -> 2.02 M q/s) and loses
-  // where rounds are few or leaves long (config 1 h = 8: -2% at best;
-  // config 2: -1%; config 5 h = 11: -6%; tools/finish_sweep.py)
-  if (ctx->residency == 0 && ctx->d <= 32 && k <= 64 && ctx->h >= 12)
-    R.finish_at = std::min<long long>((long long)ctx->sm_count * 512, m / 8);
+  // Tail finisher (resident structure, d <= 32, k <= 64): the last queries
+  // walk the rest of their traversals in one launch instead of one round per
+  // leaf (tools/finish_sweep.py, profiles/r1d/finish_sweep*.txt):
+  //  * leaves of >= 512 points: one CTA per query once <= 48 per SM remain
+  //    (config 2 27.8 -> 28.3 M q/s; config 5 h = 11 +8%; uniform h = 11 +3%);
+  //  * deeper trees of short leaves (h >= 12): one warp per query once
+  //    <= min(512 per SM, m / 8) remain (config 5 h = 14: 1.27 -> 2.0 M q/s);
+  //  * otherwise off (config 1, 256-point leaves: no gain).
+  if (ctx->residency == 0 && ctx->d <= 32 && k <= 64) {
+    if (ctx->n >= 512ll * ctx->nl) {
+      R.finish_at = (long long)ctx->sm_count * 48;
+      R.finish_cta = true;
+    } else if (ctx->h >= 12) {
+      R.finish_at = std::min<long long>((long long)ctx->sm_count * 512, m / 8);
+    }
+  }
   if (const char* e = std::getenv("BKT_FINISH_AT")) R.finish_at = std::atoll(e);
+  if (const char* e = std::getenv("BKT_FINISH_CTA")) R.finish_cta = std::atoi(e) != 0;
 
   // batch size: whatever fits comfortably in free memory (or the caller's choice)
   const long long per_query = 4ll * ctx->D + 4ll * ctx->d + 8ll * k + 4 * 5;

@@ -438,4 +438,127 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(
   }
 }
 
+// Tail finisher, one CTA per query: the leaf's quads are spread over the
+// CTA's threads (one quad each per slice), candidates below the current k-th
+// key are appended to a shared list and inserted by thread 0 after each
+// slice; thread 0 runs FindLeaf.  Same per-visit semantics as finish_kernel,
+// a quarter of its per-leaf latency for long leaves.
+constexpr int kFinishT = 256;
+template <bool FMA>
+__global__ void __launch_bounds__(kFinishT) finish_cta_kernel(
+    const int* __restrict__ work, RoundCtl* ctl, const float* __restrict__ q, int D, int k, TopTreeView top,
+    uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
+    const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base,
+    const int* __restrict__ leaf_size, unsigned long long* pairs, int* seq_log, unsigned long long* seq_pos,
+    long long seq_cap) {
+  __shared__ uint64_t s_row[64];
+  __shared__ float s_q[32];
+  __shared__ uint64_t s_cand[kFinishT * 4];
+  __shared__ int s_nc, s_leaf;
+  const int tid = threadIdx.x;
+  const int d = top.d;
+  const int n = ctl->active;
+  unsigned long long pairs_acc = 0, scans_acc = 0;
+  if (tid == 0) s_nc = 0;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int qi = __ldg(work + i);
+    int leaf = next[qi];
+    __syncthreads();  // the previous query's shared state is no longer read
+    if (leaf < 0) continue;
+    if (tid < d) s_q[tid] = __ldg(q + (long long)qi * D + tid);
+    uint64_t* kp = keys + (long long)qi * k;
+    if (tid < k) s_row[tid] = kp[tid];
+    __syncthreads();
+    float qv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) qv[j] = j < d ? s_q[j] : 0.0f;
+    uint32_t lf = 0, pend = 0, vis = 0;
+    if (tid == 0) {
+      const uint32_t st = state[qi];
+      lf = st & 0xFFFFu;
+      pend = st >> 16;
+      vis = visits[qi];
+    }
+    while (leaf >= 0) {
+      const long long g0 = __ldg(quad_base + leaf), g1 = __ldg(quad_base + leaf + 1);
+      for (long long gb = g0; gb < g1; gb += kFinishT) {
+        const uint64_t kkey = s_row[k - 1];
+        const long long g = gb + tid;
+        if (g < g1) {
+          float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          const float4* pq = reinterpret_cast<const float4*>(pts + g * 4 * D);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j < d) {
+              const float4 p = __ldg(pq + j);
+              const float e[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float df = __fsub_rn(qv[j], e[t]);
+                if constexpr (FMA) acc[t] = __fmaf_rn(df, df, acc[t]);
+                else acc[t] = __fadd_rn(acc[t], __fmul_rn(df, df));
+              }
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint64_t key = pack_key(acc[t], __ldg(pidx + g * 4 + t));
+            if (key < kkey) s_cand[atomicAdd(&s_nc, 1)] = key;
+          }
+        }
+        __syncthreads();
+        if (tid == 0) {
+          // insert every candidate that beats the current k-th key (any order:
+          // the result is the best k of the list and the candidates)
+          const int nc = s_nc;
+          for (int c = 0; c < nc; ++c) {
+            const uint64_t ck = s_cand[c];
+            if (ck < s_row[k - 1]) {
+              int j = k - 1;
+              while (j > 0 && s_row[j - 1] > ck) {
+                s_row[j] = s_row[j - 1];
+                --j;
+              }
+              s_row[j] = ck;
+            }
+          }
+          s_nc = 0;
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        pairs_acc += (unsigned long long)__ldg(leaf_size + leaf);
+        scans_acc += 1;
+        // FindLeaf with the k-th distance after this leaf
+        const float kth = key_dist(s_row[k - 1]);
+        const float* sp = top.split;
+        const int nxt = find_next_leaf_with(top.h, d, [sp](uint32_t node) { return __ldg(sp + node); },
+                                            [](int j) { return s_q[j]; }, kth, lf, pend);
+        if (nxt >= 0) {
+          ++vis;
+          if (seq_log) {
+            const unsigned long long p = atomicAdd(seq_pos, 1ull);
+            if ((long long)p < seq_cap) {
+              seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)vis; seq_log[3 * p + 2] = nxt;
+            }
+          }
+        }
+        s_leaf = nxt;
+      }
+      __syncthreads();
+      leaf = s_leaf;
+    }
+    if (tid < k) kp[tid] = s_row[tid];
+    if (tid == 0) {
+      state[qi] = (pend << 16) | lf;
+      next[qi] = -1;
+      visits[qi] = vis;
+    }
+  }
+  if (tid == 0 && (pairs_acc || scans_acc)) {
+    if (pairs) atomicAdd(pairs, pairs_acc);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->scans), scans_acc);
+  }
+}
+
 }  // namespace bkt

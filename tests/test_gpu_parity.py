@@ -363,14 +363,15 @@ def test_tensor_core_variants_exact(knn_golden, gpu_device, env, monkeypatch):
         assert np.array_equal(res.keys, c["keys"]), (env, s)
 
 
-@pytest.mark.parametrize("finish_at", ["-1", "1000000000"])
+@pytest.mark.parametrize("finish_at,cta", [("-1", "0"), ("1000000000", "0"), ("1000000000", "1")])
 @pytest.mark.parametrize("kernel", ["direct", "tc"])
-def test_tail_finisher_on_and_off_exact(knn_golden, gpu_device, kernel, finish_at, monkeypatch):
-    """The tail finisher (one warp per remaining query, one launch) and the
-    plain round loop give the reference's keys, visit counts, leaf sequences
-    and scan events: off entirely (-1) and taking over from the first
-    round check (1e9)."""
+def test_tail_finisher_on_and_off_exact(knn_golden, gpu_device, kernel, finish_at, cta, monkeypatch):
+    """The tail finisher (one warp or one CTA per remaining query, one
+    launch) and the plain round loop give the reference's keys, visit
+    counts, leaf sequences and scan events: off entirely (-1) and taking
+    over from the first round check (1e9)."""
     monkeypatch.setenv("BKT_FINISH_AT", finish_at)
+    monkeypatch.setenv("BKT_FINISH_CTA", cta)
     for c in knn_golden:
         s = c["spec"]
         tree = bkt.build_buffer_tree(c["refs"], s["h"])
@@ -395,8 +396,9 @@ def test_tail_finisher_mixture(gpu_device, exact, monkeypatch):
     refs, queries = pts[:200_000], pts[200_000:]
     tree = bkt.build_buffer_tree(refs, 7)
     out = []
-    for fa in ("-1", "5000", "1000000000"):
+    for fa, cta in (("-1", "0"), ("5000", "0"), ("1000000000", "0"), ("5000", "1"), ("1000000000", "1")):
         monkeypatch.setenv("BKT_FINISH_AT", fa)
+        monkeypatch.setenv("BKT_FINISH_CTA", cta)
         stats = bkt.SearchStats()
         res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=10), device=gpu_device, stats=stats, exact=exact)
         out.append((res.keys, stats.visited_per_query, stats.leaf_scan_events))

@@ -14,7 +14,7 @@
 //   pts        f32[total_quads * 4 * D]         quad g, dim j, point t at g*4D + 4j + t
 //   pidx       u32[total_quads * 4]             original row of each point (padding: 0xFFFFFFFF)
 //   per batch of m queries: q f32[m*D], keys u64[m*k], state u32[m], next i32[m],
-//   visits u32[m], bucket slot (rank) i32[m], two work lists i32[m]; per leaf: counts, leaf_off, tile_off.
+//   visits u32[m], bucket slot per work-list position int2[m], two work lists i32[m]; per leaf: counts, leaf_off, tile_off.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -122,7 +122,7 @@ struct bkt_ctx {
   int* counts = nullptr;    // per bucket key
   int* key_off = nullptr;   // nkeys + 1: first work-list slot of each key
   int* qkey = nullptr;      // per query: bucket key of its next leaf visit
-  int* rank = nullptr;      // per query: slot in its next bucket (taken when counted)
+  int2* pos = nullptr;      // per work-list position: {next leaf or -1, slot in its next bucket}
   int* leaf_off = nullptr;
   int* tile_off = nullptr;
   int4* tiles = nullptr;    // per-tile records (capacity tiles_cap)
@@ -250,7 +250,7 @@ void free_work(bkt_ctx* c) {
   c->tiles_cap = 0;
   dfree(c->kthv);
   dfree(c->qkey);
-  dfree(c->rank);
+  dfree(c->pos);
   dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
   dfree(c->work[0]); dfree(c->work[1]);
   c->cap_m = 0; c->cap_k = 0;
@@ -304,7 +304,7 @@ int ensure_work(bkt_ctx* ctx, long long m, int k) {
   CU(cudaMalloc(&ctx->visits, sizeof(uint32_t) * M));
   CU(cudaMalloc(&ctx->kthv, sizeof(float) * M));
   CU(cudaMalloc(&ctx->qkey, sizeof(int) * M));
-  CU(cudaMalloc(&ctx->rank, sizeof(int) * M));
+  CU(cudaMalloc(&ctx->pos, sizeof(int2) * M));
   CU(cudaMalloc(&ctx->work[0], sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[1], sizeof(int) * M));
   ctx->tiles_cap = M / kNT + (1ll << ctx->h) + 1;
@@ -876,7 +876,7 @@ ScanArgs make_scan_args(bkt_ctx* ctx, SearchRun& R, int cur) {
   a.tile_hi = -1;
   a.tiles = ctx->tiles;
   a.counts = ctx->counts;
-  a.rank = ctx->rank;
+  a.pos = ctx->pos;
   a.pts = ctx->pts;
   a.pidx = ctx->pidx;
   a.quad_origin = 0;
@@ -1020,7 +1020,7 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
   // FindLeaf after every chunk of the round has been scanned
   findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
       ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys, ctx->state,
-      ctx->next, ctx->visits, ctx->counts, ctx->rank, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
+      ctx->next, ctx->visits, ctx->counts, ctx->pos, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap);
   CU(cudaGetLastError());
   R.launches++;
   return BKT_OK;
@@ -1038,7 +1038,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
                                                        ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
                                                        R.seq_cap, ctx->kthv, ctx->blk_base, ctx->nodes, ctx->sub_w,
-                                                       ctx->qkey, ctx->counts, ctx->rank);
+                                                       ctx->qkey, ctx->counts, ctx->pos);
   CU(cudaGetLastError());
   R.launches++;
 
@@ -1065,8 +1065,8 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
       CU(cudaEventSynchronize(ring[slot]));
       if (ctx->h_ctl[slot].active == 0) break;
     }
-    scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->next,
-                                                           ctx->qkey, ctx->key_off, ctx->rank, ctx->work[cur],
+    scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->pos,
+                                                           ctx->qkey, ctx->key_off, ctx->work[cur],
                                                            ctx->ctl, ctx->leaf_off, ctx->tile_off, ctx->nl, sw, kNT,
                                                            ctx->tiles,
                                                            (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
@@ -1086,7 +1086,7 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
         // then overlap across many warps instead of stalling the scan's epilogue
         findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
             ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys,
-            ctx->state, ctx->next, ctx->visits, ctx->counts, ctx->rank, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
+            ctx->state, ctx->next, ctx->visits, ctx->counts, ctx->pos, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
             R.seq_cap);
         CU(cudaGetLastError());
         R.launches++;

@@ -44,7 +44,7 @@ struct ScanArgs {
   int tile_lo, tile_hi;  // chunk mode: tile sub-range; tile_hi < 0 = [0, *num_tiles)
   const int4* tiles;     // per-tile {leaf, qbeg, qcnt} written by plan_kernel
   int* counts;           // nl: next-round histogram (fused epilogue)
-  int* rank;             // m: a query's slot in its next-round bucket (taken when counted)
+  int2* pos;             // m: per work-list position {next leaf or -1, slot in that leaf's next-round bucket}
   // leaf structure, quad-interleaved: quad g, dim j, point t at pts[(g - quad_origin)*4D + 4j + t]
   const float* pts;
   const uint32_t* pidx;  // original index of point (g - quad_origin)*4 + t (padding: 0xFFFFFFFF)
@@ -279,12 +279,14 @@ __global__ void __launch_bounds__(kThreads, (ScanOcc<D, KB>::kMinBlocks)) leafsc
         int nxt = find_next_leaf(a.top, qget, key_dist(arr[0]), lf, pend);
         a.state[qi] = (pend << 16) | lf;
         a.next[qi] = nxt;
+        int rk = 0;
         if (nxt >= 0) {
           uint32_t v = a.visits[qi] + 1;
           a.visits[qi] = v;
           log_visit(a, qi, v, nxt);
-          a.rank[qi] = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
+          rk = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
         }
+        a.pos[T.qbeg + tid] = make_int2(nxt, rk);  // coalesced: read back by position in scatter
       }
     }
   }

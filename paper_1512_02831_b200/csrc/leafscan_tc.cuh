@@ -851,12 +851,14 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
           const int nxt = find_next_leaf_with(th, d, [sp](uint32_t node) { return sp[node]; }, qget, kth, lf, pend);
           a.state[qi] = (pend << 16) | lf;
           a.next[qi] = nxt;
+          int rk = 0;
           if (nxt >= 0) {
             const uint32_t vv = cu.vis + 1;
             a.visits[qi] = vv;
             log_visit(a, qi, vv, nxt);
-            a.rank[qi] = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
-            }
+            rk = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
+          }
+          a.pos[cu.qbeg + tid] = make_int2(nxt, rk);  // coalesced: read back by position in scatter
         }
       }
     }

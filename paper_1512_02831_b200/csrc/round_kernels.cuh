@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kStartQ) start_kernel(const float* __restrict_
                                                         float* __restrict__ kth, const int* __restrict__ blk_base,
                                                         const int4* __restrict__ nodes, int sub_w,
                                                         int* __restrict__ qkey, int* __restrict__ counts,
-                                                        int* __restrict__ rank) {
+                                                        int2* __restrict__ pos) {
   extern __shared__ float s_start[];
   const int ntree = start_tree_n(top.h, D);
   float* s_split = s_start;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kStartQ) start_kernel(const float* __restrict_
     }
     const int key = (int)leaf * sub_w + sub;
     qkey[i] = key;
-    rank[i] = warp_reserve(counts, key);
+    pos[i] = make_int2((int)leaf, warp_reserve(counts, key));  // position i = query i in the home round
   }
 }
 
@@ -233,23 +233,25 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
 }
 
 // Place every still-active query of the previous work list into its key's
-// slice of the new list, at the slot it took when it was counted (rank), and
+// slice of the new list, at the slot it took when it was counted, and
 // write the round's per-tile records {leaf, first work-list slot, query
 // count, sub-bucket of the first query (its block for a home-leaf visit)}.
 // identity: previous list is 0..prev_active-1.  No atomics.
-__global__ void scatter_kernel(const int* __restrict__ prev, int identity, const int* __restrict__ next,
+__global__ void scatter_kernel(const int* __restrict__ prev, int identity, const int2* __restrict__ pos,
                                const int* __restrict__ qkey, const int* __restrict__ key_off,
-                               const int* __restrict__ rank, int* __restrict__ work, const RoundCtl* ctl,
+                               int* __restrict__ work, const RoundCtl* ctl,
                                const int* __restrict__ leaf_off, const int* __restrict__ tile_off, int nl, int sub_w,
                                int tile_q, int4* __restrict__ tiles, int tiles_cap) {
   const int n = ctl->prev_active;
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    int qi = identity ? i : __ldg(prev + i);
-    const int leaf = __ldg(next + qi);
-    if (leaf >= 0) {
-      const int key = identity ? __ldg(qkey + qi) : leaf;  // home round: (leaf, block) keys
-      work[__ldg(key_off + key) + __ldg(rank + qi)] = qi;
+    // position i of the list just scanned: its next leaf and bucket slot were
+    // written by position (coalesced), only the store into the new list scatters
+    const int2 pr = __ldg(pos + i);
+    if (pr.x >= 0) {
+      const int qi = identity ? i : __ldg(prev + i);
+      const int key = identity ? __ldg(qkey + i) : pr.x;  // home round: (leaf, block) keys
+      work[__ldg(key_off + key) + pr.y] = qi;
     }
   }
   const int nt = min(ctl->num_tiles, tiles_cap);
@@ -278,7 +280,7 @@ __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const
 __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ctl, const float* __restrict__ q,
                                 int D, int k, TopTreeView top, const uint64_t* __restrict__ keys,
                                 uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
-                                int* __restrict__ counts, int* __restrict__ rank, int* seq_log,
+                                int* __restrict__ counts, int2* __restrict__ pos, int* seq_log,
                                 unsigned long long* seq_pos, long long seq_cap) {
   // the top tree's split values in shared memory when they fit (dynamic smem)
   extern __shared__ float s_fl_split[];
@@ -298,6 +300,7 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
     else nxt = find_next_leaf(top, qget, kth, lf, pend);
     state[qi] = (pend << 16) | lf;
     next[qi] = nxt;
+    int rk = 0;
     if (nxt >= 0) {
       uint32_t v = visits[qi] + 1;
       visits[qi] = v;
@@ -307,8 +310,9 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
           seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)v; seq_log[3 * p + 2] = nxt;
         }
       }
-      rank[qi] = warp_reserve(counts, nxt);  // next round's bucket (key = leaf) and slot
+      rk = warp_reserve(counts, nxt);  // next round's bucket (key = leaf) and slot
     }
+    pos[i] = make_int2(nxt, rk);
   }
 }
 

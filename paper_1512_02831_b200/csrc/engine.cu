@@ -134,7 +134,8 @@ struct bkt_ctx {
   int* seq_dev = nullptr;
   long long seq_dev_cap = 0;
   // pinned host mirrors
-  RoundCtl* h_ctl = nullptr;  // ring of kRing slots
+  RoundCtl* h_ctl = nullptr;  // ring of kRing slots (mapped page-locked memory)
+  RoundCtl* d_ctl_mirror = nullptr;  // device address of h_ctl (plan_kernel writes its slot)
   int* h_tile_off = nullptr;
   int h_tile_off_cap = 0;
   uint64_t* h_stage = nullptr;  // pinned staging for D2H / H2D
@@ -614,7 +615,8 @@ int bkt_open(int cuda_device, bkt_ctx** out) {
   CU(cudaMalloc(&ctx->pairs, sizeof(unsigned long long)));
   CU(cudaMalloc(&ctx->seq_pos, sizeof(unsigned long long)));
   CU(cudaMalloc(&ctx->hist, sizeof(int) * kHistCap));
-  CU(cudaHostAlloc(&ctx->h_ctl, sizeof(RoundCtl) * kRing, cudaHostAllocDefault));
+  CU(cudaHostAlloc(&ctx->h_ctl, sizeof(RoundCtl) * kRing, cudaHostAllocMapped));
+  CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_ctl_mirror), ctx->h_ctl, 0));
   for (int i = 0; i < kRing; ++i) CU(cudaEventCreateWithFlags(&ctx->ring_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) CU(cudaEventCreate(&ctx->t_ev[i]));
   CU(cudaEventCreateWithFlags(&ctx->t_ev[2], cudaEventDisableTiming));
@@ -1054,11 +1056,10 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
     const int sw = round == 0 ? ctx->sub_w : 1;
     plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, sw, ctx->nl * sw,
                                                      ctx->leaf_off, ctx->tile_off, ctx->ctl, ctx->nl, kNT,
-                                                     ctx->hist, kHistCap);
+                                                     ctx->hist, kHistCap, ctx->d_ctl_mirror + round % kRing);
     CU(cudaGetLastError());
     R.launches++;
     const int slot = (int)(round % kRing);
-    CU(cudaMemcpyAsync(&ctx->h_ctl[slot], ctx->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaEventRecord(ring[slot], ctx->stream));
     if (ooc) {
       // out-of-core needs the plan on the host anyway; check synchronously

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
                                                             int sub_w, int nkeys,
                                                             int* __restrict__ leaf_off, int* __restrict__ tile_off,
                                                             RoundCtl* ctl, int nl, int tile_q, int* hist,
-                                                            int hist_cap) {
+                                                            int hist_cap, RoundCtl* mirror) {
   long long tot_c, tot_t;
   {
     const int per = (nkeys + kPlanThreads - 1) / kPlanThreads;
@@ -228,6 +228,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
       if (hist && ctl->rounds < hist_cap) hist[ctl->rounds] = (int)tot_c;
       ctl->rounds += 1;
       ctl->scans += tot_c;
+    }
+    // the host's copy of this round's control block, written straight into
+    // mapped page-locked memory (no copy-engine operation between the round's
+    // kernels); the host reads it after the round's event completes
+    if (mirror) {
+      *mirror = *ctl;
+      __threadfence_system();
     }
   }
 }

@@ -64,7 +64,10 @@ struct ScanArgs {
 
 constexpr int kConsumerWarps = kNT / 32;
 constexpr int kThreads = kNT + 32;  // + one TMA producer warp
-constexpr int kQueue = 8;           // per-thread candidate queue (shared memory)
+#ifndef BKT_QUEUE
+#define BKT_QUEUE 8
+#endif
+constexpr int kQueue = BKT_QUEUE;   // per-thread candidate queue (shared memory)
 
 template <int D>
 struct ScanSmem {

@@ -919,6 +919,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.spin = 0;  // measured: suspending waits beat spinning by 2.6% on config 2 (BKT_TC_SPIN: 1 MMA, 2 epilogue)
     t.ctr = R.counters ? ctx->tc_ctr : nullptr;
     t.sub_w = ctx->sub_w;
+    t.tile_next = &ctx->ctl->tile_next;
     if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e);
     const char* dbg_env = std::getenv("BKT_TC_DEBUG");
     if (dbg_env && R.leafscan_launches == (std::atoi(dbg_env) > 1 ? std::atoi(dbg_env) : 5)) {

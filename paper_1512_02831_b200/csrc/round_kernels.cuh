@@ -31,7 +31,7 @@ struct RoundCtl {
   int rounds;       // rounds with active > 0
   long long scans;  // (query, leaf) scans so far (SearchStats.leaf_scan_events)
   int late_n;       // early result drain: queries still active when it started
-  int pad_;
+  int tile_next;    // dynamic tile counter of the round's leaf scan (reset by plan_kernel)
 };
 
 // Early result drain: remember the queries of the round just scanned (every
@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
     ctl->prev_active = ctl->active;
     ctl->active = (int)tot_c;
     ctl->num_tiles = (int)tot_t;
+    ctl->tile_next = 0;
     if (tot_c > 0) {
       if (hist && ctl->rounds < hist_cap) hist[ctl->rounds] = (int)tot_c;
       ctl->rounds += 1;

@@ -315,7 +315,7 @@ def main() -> None:
     tc_used = a.kernel in ("auto", "tc") and DIM <= 31
     kernel_name = "leafscan_tc_kernel" if tc_used else "leafscan_kernel"
     traffic = None
-    tf = ROOT / "profiles" / "r1e" / "ncu_traffic.json"
+    tf = ROOT / "profiles" / "r1f" / "ncu_traffic.json"
     if tf.exists() and tc_used and scan_launches:
         t = json.load(open(tf))
         # dram bytes of the captured launch per pair, times this run's mean pairs per launch
@@ -324,7 +324,7 @@ def main() -> None:
         ach = 2.0 * 16 * pairs / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
         roofline = {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": (ach / tf32_peak) if ach else None, "traffic": traffic,
-                    "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1e/ncu_traffic.json)",
+                    "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1f/ncu_traffic.json)",
                     "kernel": kernel_name, "peak_source": peak_src, "flops_per_pair": 32,
                     "leafscan_ms_per_step": scan_ms / a.steps,
                     "leafscan_share": scan_ms / dev_ms if dev_ms else None, "leafscan_launches": scan_launches}

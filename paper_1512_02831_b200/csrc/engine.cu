@@ -879,6 +879,10 @@ ScanArgs make_scan_args(bkt_ctx* ctx, SearchRun& R, int cur) {
   a.tiles = ctx->tiles;
   a.counts = ctx->counts;
   a.pos = ctx->pos;
+  // dynamic tile order for the CUDA-core scan when leaves are long (config 4
+  // d = 5: +10%); with leaves of a few chunks (config 1: 2 chunks per tile)
+  // the producer's shorter lookahead costs more than the balance gains (-14%)
+  a.tile_next = ctx->n >= 1024ll * ctx->nl ? &ctx->ctl->tile_next : nullptr;
   a.pts = ctx->pts;
   a.pidx = ctx->pidx;
   a.quad_origin = 0;

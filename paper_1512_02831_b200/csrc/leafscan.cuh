@@ -45,6 +45,7 @@ struct ScanArgs {
   const int4* tiles;     // per-tile {leaf, qbeg, qcnt} written by plan_kernel
   int* counts;           // nl: next-round histogram (fused epilogue)
   int2* pos;             // m: per work-list position {next leaf or -1, slot in that leaf's next-round bucket}
+  int* tile_next;        // round's tile counter for dynamic tile scheduling (zeroed by plan_kernel), or null
   // leaf structure, quad-interleaved: quad g, dim j, point t at pts[(g - quad_origin)*4D + 4j + t]
   const float* pts;
   const uint32_t* pidx;  // original index of point (g - quad_origin)*4 + t (padding: 0xFFFFFFFF)
@@ -75,7 +76,8 @@ struct ScanSmem {
   static constexpr int kStagePts = kChunkQuads * kQuadBytes;
   static constexpr int kStageIdx = kChunkQuads * 16;
   static constexpr int kQueueBytes = kQueue * kNT * 8;
-  static constexpr int kBytes = kStages * (kStagePts + kStageIdx) + kQueueBytes + 2 * kStages * 8 + 64;
+  // + full/empty barriers, 8 tile-publication barriers and 8 tile slots
+  static constexpr int kBytes = kStages * (kStagePts + kStageIdx) + kQueueBytes + 2 * kStages * 8 + 8 * 8 + 8 * 4 + 64;
 };
 
 __device__ __forceinline__ void log_visit(const ScanArgs& a, int qi, uint32_t visit, int leaf) {
@@ -144,6 +146,8 @@ __global__ void __launch_bounds__(kThreads, (ScanOcc<D, KB>::kMinBlocks)) leafsc
   uint64_t* s_queue = reinterpret_cast<uint64_t*>(smem + kStages * (S::kStagePts + S::kStageIdx));
   uint64_t* s_full = reinterpret_cast<uint64_t*>(smem + kStages * (S::kStagePts + S::kStageIdx) + S::kQueueBytes);
   uint64_t* s_empty = s_full + kStages;
+  uint64_t* s_tready = s_empty + kStages;                                // [8]
+  volatile int* s_tile = reinterpret_cast<volatile int*>(s_tready + 8);  // [8]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -152,18 +156,34 @@ __global__ void __launch_bounds__(kThreads, (ScanOcc<D, KB>::kMinBlocks)) leafsc
       mbar_init(&s_full[s], 1);
       mbar_init(&s_empty[s], kConsumerWarps);
     }
+    for (int s = 0; s < 8; ++s) mbar_init(&s_tready[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
   const int tiles_end = a.tile_hi >= 0 ? a.tile_hi : *a.num_tiles;
+  // Tile order (see leafscan_tc.cuh): dynamic from the round's counter when
+  // the launch covers the whole round -- consumer thread 0 publishes the j-th
+  // tile of this CTA two tiles ahead in s_tile[j & 7] (the consumer warps
+  // drift apart by at most kStages chunks, so eight slots never collide) --
+  // static striding for a chunk's tile sub-range (out-of-core rounds).
+  const bool dyn = a.tile_next != nullptr && a.tile_hi < 0;
+  auto seq_tile = [&](uint32_t j) -> int {
+    if (dyn) {
+      mbar_wait(&s_tready[j & 7u], (j >> 3) & 1u);
+      return s_tile[j & 7u];
+    }
+    return a.tile_lo + (int)blockIdx.x + (int)j * (int)gridDim.x;
+  };
 
   if (warp == kConsumerWarps) {
     // ===== TMA producer: streams every tile's leaf chunks through the ring,
     // running ahead across tile boundaries =====
     if (lane == 0) {
       uint32_t g = 0;
-      for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x) {
+      for (uint32_t j = 0;; ++j) {
+        const int t = seq_tile(j);
+        if (t >= tiles_end) break;
         const TileInfo T = tile_info(a, t);
         const int nquads = (int)(T.g1 - T.g0);
         for (int c = 0; c < T.nchunks; ++c, ++g) {
@@ -185,7 +205,21 @@ __global__ void __launch_bounds__(kThreads, (ScanOcc<D, KB>::kMinBlocks)) leafsc
   uint64_t* qslot = s_queue + tid;  // this thread's queue: qslot[j * kNT]
   const uint64_t zero = a.zero;
   uint32_t g = 0;
-  for (int t = a.tile_lo + blockIdx.x; t < tiles_end; t += gridDim.x) {
+  int grabbed = 0;
+  auto publish = [&](uint32_t j) {  // consumer thread 0
+    s_tile[j & 7u] = grabbed;
+    mbar_arrive(&s_tready[j & 7u]);
+    if (grabbed < tiles_end) grabbed = a.tile_lo + atomicAdd(a.tile_next, 1);
+  };
+  if (dyn && tid == 0) {
+    grabbed = a.tile_lo + atomicAdd(a.tile_next, 1);
+    publish(0);
+    publish(1);
+  }
+  for (uint32_t j = 0;; ++j) {
+    if (dyn && tid == 0) publish(j + 2);
+    const int t = seq_tile(j);
+    if (t >= tiles_end) break;
     const TileInfo T = tile_info(a, t);
     const int nquads = (int)(T.g1 - T.g0);
     const bool valid = tid < T.qcnt;

@@ -17,6 +17,7 @@
 //   visits u32[m], bucket slot per work-list position int2[m], two work lists i32[m]; per leaf: counts, leaf_off, tile_off.
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -930,14 +931,30 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
       // per-chunk timestamps of CTA 0 in one leafscan launch (BKT_TC_DEBUG=<launch>, default the 6th)
       static long long* dbg = nullptr;
       const int cap = 4096;
-      if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * cap);
-      cudaMemsetAsync(dbg, 0, sizeof(long long) * 16 * cap, ctx->stream);
+      const int extra = 2048;  // per-CTA start / end stamps
+      if (!dbg) cudaMalloc(&dbg, sizeof(long long) * (16 * cap + extra));
+      cudaMemsetAsync(dbg, 0, sizeof(long long) * (16 * cap + extra), ctx->stream);
       t.dbg = dbg;
       t.dbg_cap = cap;
       CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows, R.tc_cps));
-      std::vector<long long> h(16 * cap);
-      CU(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * 16 * cap, cudaMemcpyDeviceToHost, ctx->stream));
+      std::vector<long long> h(16 * cap + extra);
+      CU(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * (16 * cap + extra), cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
+      {
+        // load balance: per-CTA end of the epilogue's tile loop, from the earliest CTA start
+        long long s0 = LLONG_MAX, e_min = LLONG_MAX, e_max = 0;
+        double e_sum = 0;
+        const int nct = std::min(R.grid_scan, 1024);
+        for (int c = 0; c < nct; ++c) s0 = std::min(s0, h[16 * cap + c]);
+        for (int c = 0; c < nct; ++c) {
+          const long long e = h[16 * cap + 1024 + c] - s0;
+          e_min = std::min(e_min, e);
+          e_max = std::max(e_max, e);
+          e_sum += e;
+        }
+        std::fprintf(stderr, "cta balance: %d CTAs, end min %.1f us mean %.1f us max %.1f us (max/mean %.3f)\n", nct,
+                     e_min / 1e3, e_sum / nct / 1e3, e_max / 1e3, e_max / (e_sum / nct));
+      }
       long long base = h[0];
       auto rel = [&](long long v) { return v ? v - base : -1; };
       for (int g = 0; g < cap && h[16 * g + 5]; ++g)

@@ -290,6 +290,15 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int nsplit = (1 << a.top.h) - 1;
+  auto gtimer = []() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return (long long)v;
+  };
+  if constexpr (kTcDiag) {
+    // load balance of the launch (BKT_TC_DEBUG): per-CTA start / end of the epilogue's tile loop
+    if (A.dbg && tid == 0 && blockIdx.x < 1024) A.dbg[16 * A.dbg_cap + blockIdx.x] = gtimer();
+  }
   if (A.tree_smem)
     for (int i = tid; i < nsplit; i += tc_threads(CPS)) sSplit[i] = __ldg(a.top.split + i);
   if (tid == 0) {
@@ -902,6 +911,9 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
           a.pos[cu.qbeg + tid] = make_int2(nxt, rk);  // coalesced: read back by position in scatter
         }
       }
+    }
+    if constexpr (kTcDiag) {
+      if (A.dbg && tid == 0 && blockIdx.x < 1024) A.dbg[16 * A.dbg_cap + 1024 + blockIdx.x] = gtimer();
     }
     if constexpr (kTcDiag) {
       if (A.ctr) {

@@ -114,7 +114,11 @@ template <int KT, int NR, int CPS>
 struct TcSmem {
   static constexpr int kRows = NR;
   static constexpr int kBufs = tc_tmem_cols(CPS) / NR;
+#ifdef BKT_TC_STAGES
+  static constexpr int kStages = BKT_TC_STAGES;  // experiments
+#else
   static constexpr int kStages = CPS >= 3 ? (NR == 128 ? 2 : 3) : ((KT <= 16 ? 512 : 128) / NR < 2 ? 2 : (KT <= 16 ? 512 : 128) / NR);
+#endif
   static constexpr int kStageB = NR * KT * 4;
   static constexpr int kStageIdx = NR * 4;
   static constexpr int kStageRows = NR * (KT - 1) * 4;  // original coordinates (d <= KT - 1)

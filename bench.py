@@ -6,11 +6,14 @@
 
 Workload (BASELINE.json configs[1], "astronomy-like synthetic n=2M refs, m=10M
 queries, d=10, k=10, single B200 in-memory"): gen_mixture(n+m, 10, seed=1)
-drawn jointly, refs = first 2M rows, queries = the other 10M (rank 0).  With
-N GPUs each rank searches its own 10M queries (weak scaling): rank r>0 uses
-config 3's per-chunk query recipe with chunk r.  The tree (replicated per
-GPU) is built once before timing.  One step = one lazy_search over the
-rank's 10M queries.
+drawn jointly, refs = first 2M rows, queries = the other 10M.  With N GPUs
+(one process per GPU, torchrun) the tree is replicated and queries shard with
+no data-path collective:
+  --scaling weak (default): every rank searches its own 10M queries; rank 0
+      the config-2 queries, rank r>0 config 3's per-chunk recipe with chunk r;
+  --scaling strong: the config-2 10M queries split with shard_range.
+The tree is built once before timing.  One step = one search over the rank's
+queries.  Every rank checks --check-rows of its rows against the CPU oracle.
 
 value: queries/sec of the whole job, inputs resident in HBM, device time of
 the search (CUDA events on the engine's stream), max over ranks.
@@ -42,7 +45,7 @@ METRIC = "kNN queries/sec (k=10,d=10,n=2M) at 1/2/4/8 B200; % FP32/HBM roofline"
 UNIT = "queries/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -53,12 +56,16 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "tc"],
                     help="leaf scan: tensor-core filter (auto/tc) or CUDA-core direct scan")
     ap.add_argument("--height", type=int, default=9, help="tree height (results do not depend on it)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank searches its own m queries; strong: m queries sharded over the ranks")
     ap.add_argument("--m", type=int, default=M_QUERIES)
     ap.add_argument("--n", type=int, default=N_REFS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="queries in the CPU baseline sample (0 = auto)")
-    return ap.parse_args()
+    ap.add_argument("--check-rows", type=int, default=1000,
+                    help="rows of every rank's result checked against the CPU oracle (0 = off)")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -68,15 +75,65 @@ def dist_env():
     return world, rank, local
 
 
-def workload(rank: int, n: int, m: int):
-    from paper_1512_02831_b200.datasets import gen_mixture, gen_query_chunk
-    pts, _ = gen_mixture(n + m, DIM, components=8, spread=0.05, seed=1)
-    refs = pts.data[:n]
+def shard_range(m: int, rank: int, world: int) -> tuple[int, int]:
+    """Even split, remainder to the front ranks (reference scheduler.py:172-183).
+    Same rule as paper_1512_02831_b200.dist.shard_range; restated here so the
+    reference arm never imports the product package."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank must be in [0, world)")
+    base, rem = divmod(m, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def mixture_rows(n: int, m: int, lo: int, hi: int, d: int = DIM, seed: int = 1):
+    """refs = rows [0, n) and queries = rows [n+lo, n+hi) of the reference's
+    gen_mixture(n+m, d, components=8, spread=0.05, seed) (datasets.py:127-136),
+    drawn jointly as the reference does but only up to row n+hi: the normal
+    stream is consumed in order, so rows drawn in pieces equal the joint draw."""
+    rng = np.random.default_rng(seed)
+    centers = rng.random((8, d))
+    labels = rng.integers(0, 8, size=n + m)
+    refs = (centers[labels[:n]] + rng.normal(0.0, 0.05, size=(n, d))).astype(np.float32)
+    skip = lo
+    while skip > 0:  # rows before the shard: drawn and dropped, 1M at a time
+        t = min(skip, 1 << 20)
+        rng.normal(0.0, 0.05, size=(t, d))
+        skip -= t
+    q = (centers[labels[n + lo:n + hi]] + rng.normal(0.0, 0.05, size=(hi - lo, d))).astype(np.float32)
+    return np.ascontiguousarray(refs), np.ascontiguousarray(q)
+
+
+def query_chunk(chunk: int, size: int, d: int = DIM, seed: int = 1) -> np.ndarray:
+    """Config 3's per-chunk query recipe: the config-2 mixture
+    centres with default_rng(1000 + chunk)."""
+    centers = np.random.default_rng(seed).random((8, d))
+    r = np.random.default_rng(1000 + chunk)
+    return (centers[r.integers(0, 8, size=size)] + r.normal(0.0, 0.05, (size, d))).astype(np.float32)
+
+
+def rank_work(scaling: str, rank: int, world: int, n: int, m: int) -> dict:
+    """Which queries a rank searches.  weak: rank 0 the config-2 queries, rank
+    r > 0 config 3's query chunk r (m each); strong: rows shard_range(m) of
+    the config-2 queries."""
+    if scaling == "strong":
+        lo, hi = shard_range(m, rank, world)
+        return {"kind": "cfg2", "lo": lo, "hi": hi, "total": m}
     if rank == 0:
-        queries = pts.data[n:]
-    else:
-        queries = gen_query_chunk(rank, m, DIM)
-    return np.ascontiguousarray(refs), np.ascontiguousarray(queries)
+        return {"kind": "cfg2", "lo": 0, "hi": m, "total": m * world}
+    return {"kind": "chunk", "chunk": rank, "size": m, "total": m * world}
+
+
+def workload(w: dict, n: int, m: int):
+    if w["kind"] == "cfg2":
+        return mixture_rows(n, m, w["lo"], w["hi"])
+    refs, _ = mixture_rows(n, m, 0, 0)
+    return refs, np.ascontiguousarray(query_chunk(w["chunk"], w["size"]))
+
+
+def job_value(total_queries: int, steps: int, rank_seconds: list[float]) -> float:
+    """Whole-job throughput: every query all ranks searched / the slowest rank's time."""
+    return steps * total_queries / max(rank_seconds)
 
 
 class ClockSampler:
@@ -127,22 +184,43 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def cpu_baseline(tree, queries, sample: int, threads: int) -> dict:
+def oracle_tree_of(tree):
+    """The CPU oracle's view of a built tree (checker input; no product code runs)."""
+    from oracle import oracle as O
+    return O.OracleTree(tree.top.height, tree.d, tree.top.split_values,
+                        np.ascontiguousarray(np.asarray(tree.leaves.points)), tree.leaves.original_index,
+                        tree.leaves.leaf_starts)
+
+
+def cpu_baseline(otree, queries, sample: int, threads: int, label: str) -> dict:
     """The reference CPU path restated in C (oracle/, kind "port"): classic
     per-query traversal with the reference pruning rule == lazy_search's
     per-query leaf order, float32 two roundings per dimension."""
     from oracle import oracle as O
-    ot = O.OracleTree(tree.top.height, tree.d, tree.top.split_values,
-                      np.ascontiguousarray(np.asarray(tree.leaves.points)), tree.leaves.original_index,
-                      tree.leaves.leaf_starts)
     q = np.ascontiguousarray(queries[:sample])
     t0 = time.perf_counter()
-    r = O.knn_tree(ot, q, K, threads=threads)
+    r = O.knn_tree(otree, q, K, threads=threads)
     secs = time.perf_counter() - t0
     return {"value": sample / secs, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {sample} of the rank-0 config-2 queries (h={tree.top.height}), "
-                      f"C restatement of the reference traversal, {threads} threads, {secs:.1f}s",
+            "sample": f"{sample} {label} (h={otree.h}), C restatement of the reference traversal, "
+                      f"{threads} threads, {secs:.1f}s",
             "keys": r["keys"], "seconds": secs}
+
+
+def check_rows(otree, queries, got_keys, rows: int, threads: int, exact: bool) -> bool:
+    """Parity of a sample of one rank's result rows against the CPU oracle:
+    exact mode bit-identical keys; fma mode distances within 1e-5 relative."""
+    from oracle import oracle as O
+    rows = min(rows, queries.shape[0])
+    if rows <= 0:
+        return True
+    want = O.knn_tree(otree, np.ascontiguousarray(queries[:rows]), K, threads=threads)["keys"]
+    got = np.asarray(got_keys[:rows]).view(np.uint64)
+    if exact:
+        return bool(np.array_equal(got, want))
+    gd = (got >> np.uint64(32)).astype(np.uint32).view(np.float32).astype(np.float64)
+    wd = (want >> np.uint64(32)).astype(np.uint32).view(np.float32).astype(np.float64)
+    return bool(np.all(np.abs(gd - wd) <= 1e-5 * np.maximum(wd, 1e-30)))
 
 
 def cpu_model() -> str:
@@ -156,32 +234,43 @@ def cpu_model() -> str:
 
 
 def run_reference_arm(a) -> None:
+    """The reference's CPU path on the box's host cores: the oracle's C
+    restatement of the reference build (buffer_tree.py:149-197) and traversal
+    (kdtree.py:157-204 == lazy_search's per-query order), all host threads.
+    Nothing from paper_1512_02831_b200 is imported or loaded here.  Each step
+    times a bounded sample of the config-2 queries (the whole 10M would take
+    ~10 min per step), so the line's workload is a sample of the B200 arm's."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import paper_1512_02831_b200 as bkt
     from oracle import oracle as O
     O.build()
     threads = os.cpu_count() or 1
-    refs, queries = workload(0, a.n, a.m)
     h = a.height
-    tree = bkt.build_buffer_tree(refs, h)
     sample = a.cpu_sample or max(2000, 1500 * threads)
+    nsteps = a.warmup + a.steps
+    rows = min(a.m, sample * nsteps)
+    refs, queries = mixture_rows(a.n, a.m, 0, rows)
+    t0 = time.perf_counter()
+    otree = O.build_tree(refs, h)
+    build_s = time.perf_counter() - t0
     vals = []
-    for step in range(a.warmup + a.steps):
-        lo = (step * sample) % max(1, queries.shape[0] - sample)
-        r = cpu_baseline(tree, queries[lo:], sample, threads)
+    for step in range(nsteps):
+        lo = (step * sample) % max(1, rows - sample + 1)
+        r = cpu_baseline(otree, queries[lo:], sample, threads, "config-2 queries per step")
         if step >= a.warmup:
             vals.append(r["value"])
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * sample / v, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": a.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"cfg2 mixture n={a.n} refs, d={DIM}, k={K}, h={h}; bounded sample of "
-                                   f"{sample} queries per step", "model": "bufferkdtree-cpu-port"},
+                                   f"{sample} queries per step (same_config: a sample of the B200 arm's "
+                                   f"{a.m} queries, by design: the full set takes minutes per step on the CPU)",
+                       "model": "bufferkdtree-cpu-port", "build_seconds": build_s},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": f"{sample} queries/step of the config-2 queries, C port of the reference "
-                                       f"traversal, {threads} threads ({cpu_model()})"},
+                                       f"build and traversal (oracle/bkt_oracle.c), {threads} threads ({cpu_model()})"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -209,20 +298,24 @@ def main() -> None:
     red_t = torch.device("cpu") if shared else dev_t
 
     import paper_1512_02831_b200 as bkt
-    refs, queries = workload(rank, a.n, a.m)
+    from paper_1512_02831_b200.dist import max_over_ranks
+    w = rank_work(a.scaling, rank, world, a.n, a.m)
+    refs, queries = workload(w, a.n, a.m)
     m = queries.shape[0]
     h = a.height
     t0 = time.perf_counter()
     tree = bkt.build_buffer_tree(refs, h)
     build_s = time.perf_counter() - t0
     gpu = bkt.device_init(bkt.DeviceSpec(cuda_device=local))
+    t0 = time.perf_counter()
     gpu.ensure_tree(tree)
+    load_s = time.perf_counter() - t0
     exact = a.mode == "exact"
     peak_measured = gpu.fp32_peak_tflops()
     info = gpu.info()
 
     q_dev = torch.from_numpy(queries).to(dev_t)
-    keys_dev = torch.empty((m, K), dtype=torch.int64, device=dev_t)
+    keys_dev = torch.empty((max(m, 1), K), dtype=torch.int64, device=dev_t)
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev_t)
 
     def barrier():
@@ -247,9 +340,9 @@ def main() -> None:
     clocks.start()
     sts, walls = [], []
     for _ in range(a.steps):
-        st, w = step_device()
+        st, wt = step_device()
         sts.append(st)
-        walls.append(w)
+        walls.append(wt)
     clk = clocks.stop()
 
     dev_ms = sum(s["search_ms"] for s in sts)
@@ -280,26 +373,28 @@ def main() -> None:
                 tot += w1 - w0
             if os.environ.get("BKT_BENCH_DEBUG"):
                 print(f"e2e call {i}: {1e3 * (w1 - w0):.1f} ms", file=sys.stderr, flush=True)
-        e2e_local = e2e_steps * m / tot
-        e2e = {"value": e2e_local, "unit": UNIT, "h2d_bytes_per_step": int(m * DIM * 4),
-               "d2h_bytes_per_step": int(m * K * 8)}
         # device and host paths must agree
-        if not np.array_equal(res.keys, keys_dev.cpu().numpy().view(np.uint64)):
+        if not np.array_equal(res.keys, keys_dev[:m].cpu().numpy().view(np.uint64)):
             raise RuntimeError("device-resident and host API results differ")
+        e2e_time_max = max_over_ranks(tot, device=red_t)
+        e2e = {"value": job_value(w["total"], e2e_steps, [e2e_time_max]), "unit": UNIT,
+               "h2d_bytes_per_step": int(m * DIM * 4), "d2h_bytes_per_step": int(m * K * 8)}
 
-    # reductions across ranks: max time, sum of queries
-    def allmax(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=red_t)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    # reductions across ranks: the slowest rank's device time
+    dev_ms_max = max_over_ranks(dev_ms, device=red_t)
+    value = job_value(w["total"], a.steps, [dev_ms_max / 1e3])
 
-    dev_ms_max = allmax(dev_ms)
-    if e2e is not None:
-        e2e_time_max = allmax(e2e_steps * m / e2e["value"])
-        e2e["value"] = world * e2e_steps * m / e2e_time_max
-    value = world * a.steps * m / (dev_ms_max / 1e3)
+    # every rank checks a sample of its own rows against the CPU oracle
+    threads = os.cpu_count() or 1
+    otree = None
+    parity = None
+    if a.check_rows > 0:
+        otree = oracle_tree_of(tree)
+        ok = check_rows(otree, queries, keys_dev[:m].cpu().numpy(), a.check_rows,
+                        max(1, threads // max(1, world)), exact)
+        ok_all = -max_over_ranks(-float(ok), device=red_t)  # min over ranks
+        parity = {"rows_per_rank": min(a.check_rows, m), "ranks": world, "all_match": bool(ok_all >= 1.0),
+                  "rule": "exact: bit-identical keys" if exact else "fma: distances within 1e-5 relative"}
 
     # Roofline of the dominant kernel (the leaf scan).  It runs on the tensor
     # cores: per (query, reference point) pair the TF32 MMA does 2*KT = 32 FLOPs
@@ -315,8 +410,9 @@ def main() -> None:
     tc_used = a.kernel in ("auto", "tc") and DIM <= 31
     kernel_name = "leafscan_tc_kernel" if tc_used else "leafscan_kernel"
     traffic = None
-    tf = ROOT / "profiles" / "r1f" / "ncu_traffic.json"
-    if tf.exists() and tc_used and scan_launches:
+    tfs = sorted(ROOT.glob("profiles/r*/ncu_traffic.json"))  # the latest round's capture
+    tf = tfs[-1] if tfs else None
+    if tf is not None and tc_used and scan_launches:
         t = json.load(open(tf))
         # dram bytes of the captured launch per pair, times this run's mean pairs per launch
         traffic = t["dram_bytes_per_pair"] * pairs / scan_launches
@@ -324,7 +420,7 @@ def main() -> None:
         ach = 2.0 * 16 * pairs / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
         roofline = {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": (ach / tf32_peak) if ach else None, "traffic": traffic,
-                    "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1f/ncu_traffic.json)",
+                    "traffic_unit": f"bytes per launch (ncu dram read+write, {tf.relative_to(ROOT) if tf else None})",
                     "kernel": kernel_name, "peak_source": peak_src, "flops_per_pair": 32,
                     "leafscan_ms_per_step": scan_ms / a.steps,
                     "leafscan_share": scan_ms / dev_ms if dev_ms else None, "leafscan_launches": scan_launches}
@@ -343,38 +439,41 @@ def main() -> None:
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        threads = os.cpu_count() or 1
         sample = a.cpu_sample or max(2000, 1500 * threads)
-        cb = cpu_baseline(tree, queries, sample, threads)
+        if otree is None:
+            otree = oracle_tree_of(tree)
+        cb = cpu_baseline(otree, queries, sample, threads, "first rank-0 config-2 queries")
         got = keys_dev[:sample].cpu().numpy().view(np.uint64)
         if exact:
-            parity = bool(np.array_equal(got, cb["keys"]))
+            match = bool(np.array_equal(got, cb["keys"]))
         else:
             gd, gi = bkt.unpack_keys(got)
             wd, wi = bkt.unpack_keys(cb["keys"])
-            parity = bool(np.all(np.abs(gd.astype(np.float64) - wd) <= 1e-5 * np.maximum(wd, 1e-30)))
+            match = bool(np.all(np.abs(gd.astype(np.float64) - wd) <= 1e-5 * np.maximum(wd, 1e-30)))
         cpu = {k_: v_ for k_, v_ in cb.items() if k_ not in ("keys", "seconds")}
-        cpu["sample"] += f" ({cpu_model()}); GPU rows match: {parity}"
+        cpu["sample"] += f" ({cpu_model()}); GPU rows match: {match}"
 
     if rank == 0:
+        per_gpu = f"{m} queries per GPU" if a.scaling == "weak" else f"{a.m} queries sharded over {world} GPU(s)"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": dev_ms_max / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": a.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference gen_mixture recipe, seed 1; 8 gaussians, spread 0.05)",
-            "config": {"workload": f"cfg2: mixture n={a.n} refs, m={m} queries per GPU, d={DIM}, k={K}, "
+            "config": {"workload": f"cfg2: mixture n={a.n} refs, {per_gpu}, d={DIM}, k={K}, "
                                    + ("ranks sharing GPUs (smoke test), " if shared else "")
-                                   + 
-                                   f"in-memory", "height": h, "mode": a.mode, "kernel": a.kernel,
+                                   + "in-memory", "height": h, "mode": a.mode, "kernel": a.kernel,
                        "parallelism": f"query-sharded x{world} (tree replicated, no collective)",
                        "l2": "256 MiB write between steps; per-step inputs (1.2 GB) > L2",
-                       "rounds": rounds, "pairs_per_query": pairs / (a.steps * m),
-                       "build_seconds": build_s, "wall_ms_per_step": wall_ms / a.steps},
+                       "rounds": rounds, "pairs_per_query": pairs / (a.steps * max(m, 1)),
+                       "build_seconds": build_s, "load_tree_seconds": load_s,
+                       "wall_ms_per_step": wall_ms / a.steps},
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": roofline,
             "roofline_fp32_equiv": roofline_fp32,
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

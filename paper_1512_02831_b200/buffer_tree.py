@@ -256,6 +256,7 @@ def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: Buffe
     scan), "direct" (CUDA-core scan) or "tc"; all give identical results.
     """
     from .device import DeviceConfigError, chunk_required, default_device
+    from .scheduler import ChunkPlan
 
     t0 = time.perf_counter()
     qarr = np.ascontiguousarray(queries.data if hasattr(queries, "data") else queries, dtype=np.float32)
@@ -270,25 +271,33 @@ def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: Buffe
     if plan is not None and plan.n != tree.n:
         raise ValueError(f"plan covers {plan.n} points, structure has {tree.n}")
     dev = device if device is not None else default_device(0)
-    if plan is not None and dev.chunk_bytes is not None:
-        need = chunk_required(plan.max_len, tree.d)
+    # chunk capacity (device.py:384-392): with no plan the reference builds a
+    # one-chunk plan, so the whole structure must fit one chunk buffer
+    eff_plan = plan if plan is not None else ChunkPlan.build(tree.n, 1)
+    if dev.chunk_bytes is not None:
+        need = chunk_required(eff_plan.max_len, tree.d)
         if need > dev.chunk_bytes:
             per_point = 4 * tree.d + 8
             fit = max(1, (dev.chunk_bytes - 7) // per_point)
-            suggest = -(-plan.n // fit)
+            suggest = -(-eff_plan.n // fit)
             raise DeviceConfigError(
-                f"largest chunk ({plan.max_len} points) needs {need} bytes but chunk "
+                f"largest chunk ({eff_plan.max_len} points) needs {need} bytes but chunk "
                 f"buffers hold {dev.chunk_bytes}; use at least {suggest} chunks")
-    dev.ensure_tree(tree, plan if (plan is not None and plan.num_chunks > 1) else None)
-
     record = stats is not None and stats.record_sequences
     visited = np.empty(m, np.int32) if (stats is not None or debug_audit) else None
-    seq_cap = 0
-    if record:
-        seq_cap = m * tree.n_leaves
-    t1 = time.perf_counter()
-    keys, st, seq = dev.search(qarr, params.k, exact=exact, visited=visited, seq_cap=seq_cap,
-                               timing=stats is not None, kernel=kernel)
+    with dev.lock:
+        dev.ensure_tree(tree, plan if (plan is not None and plan.num_chunks > 1) else None)
+        t1 = time.perf_counter()
+        # the visit log holds one (query, visit, leaf) triple per visit that
+        # happens: start from 64 per query and, if the device counted more
+        # (it reports the total even when the log is full), repeat the
+        # deterministic search with the exact size
+        seq_cap = min(m * tree.n_leaves, 64 * m) if record else 0
+        keys, st, seq = dev.search(qarr, params.k, exact=exact, visited=visited, seq_cap=seq_cap,
+                                   timing=stats is not None, kernel=kernel, allow_seq_overflow=record)
+        if record and st.get("seq_needed", 0) > seq_cap:
+            keys, st, seq = dev.search(qarr, params.k, exact=exact, visited=visited,
+                                       seq_cap=int(st["seq_needed"]), timing=True, kernel=kernel)
     t2 = time.perf_counter()
     result = NeighborBatch.from_keys(keys, params.k)  # every row is full: counts built on first access
 

@@ -95,6 +95,9 @@ struct bkt_ctx {
   long long* tc_row_base = nullptr;
   float* tc_centroid = nullptr;
   float* tc_pnmax = nullptr;
+  int* tc_cbase = nullptr;     // nl + 1: first 128-row chunk of each leaf (TC layout)
+  float* tc_box = nullptr;     // per 128-row chunk: lo[d], hi[d] bounding box of its points
+  unsigned long long* tc_need = nullptr;  // BKT_TC_SKIPDIAG: per-tile mask of chunks some query needs
   unsigned long long* tc_ctr = nullptr;  // BKT_TC_COUNTERS diagnostics (8 counters)
   // leaf-internal blocks: each leaf of the tensor-core layout is ordered as
   // kBlockRows-point blocks along a small k-d split tree.  Queries are
@@ -234,7 +237,7 @@ int leafscan_grid(bkt_ctx* ctx, int D, int kb, bool fma, int* grid) {
 }
 
 void free_tree(bkt_ctx* c) {
-  dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid); dfree(c->tc_pnmax);
+  dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid); dfree(c->tc_pnmax); dfree(c->tc_cbase); dfree(c->tc_box);
   c->has_tc = false;
   dfree(c->blk_base); dfree(c->nodes);
   c->nkeys = 0;
@@ -758,9 +761,41 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       CU(cudaMemcpy(ctx->tc_rowsxyz, hrows.data(), sizeof(float) * R * d, cudaMemcpyHostToDevice));
       CU(cudaMemcpy(ctx->tc_row_base, rb.data(), sizeof(long long) * (nl + 1), cudaMemcpyHostToDevice));
       CU(cudaMemcpy(ctx->tc_centroid, hcen.data(), sizeof(float) * nl * KT, cudaMemcpyHostToDevice));
+      {
+        // bounding box of every 128-row chunk (the scan's chunk) of the TC layout
+        std::vector<int> cb(nl + 1, 0);
+        for (int l = 0; l < nl; ++l) cb[l + 1] = cb[l] + (int)((rb[l + 1] - rb[l] + 127) / 128);
+        std::vector<float> box((size_t)cb[nl] * 2 * d);
+        for (int l = 0; l < nl; ++l)
+          for (int c = 0; c < cb[l + 1] - cb[l]; ++c) {
+            float* bx = box.data() + (size_t)(cb[l] + c) * 2 * d;
+            for (int j = 0; j < d; ++j) { bx[j] = __builtin_inff(); bx[d + j] = -__builtin_inff(); }
+            const long long r0 = rb[l] + 128ll * c, r1 = std::min(rb[l + 1], r0 + 128);
+            for (long long r = r0; r < r1; ++r) {
+              if (hidx[r] == kIndexSentinel) continue;
+              for (int j = 0; j < d; ++j) {
+                bx[j] = std::min(bx[j], hrows[r * d + j]);
+                bx[d + j] = std::max(bx[d + j], hrows[r * d + j]);
+              }
+            }
+          }
+        CU(cudaMalloc(&ctx->tc_cbase, sizeof(int) * (nl + 1)));
+        CU(cudaMemcpy(ctx->tc_cbase, cb.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice));
+        CU(cudaMalloc(&ctx->tc_box, sizeof(float) * box.size()));
+        CU(cudaMemcpy(ctx->tc_box, box.data(), sizeof(float) * box.size(), cudaMemcpyHostToDevice));
+      }
       ctx->KT = KT;
       ctx->tc_rows = R;
-      ctx->has_tc = true;
+      // The filter's error bound is relative to |q'|^2 + |p'|^2 and assumes
+      // no overflow and no flushed products (leafscan_tc.cuh header): a leaf
+      // whose centred norms overflow or are tiny-but-nonzero keeps the tree
+      // on the CUDA-core scan (same results, no filter).
+      bool tc_safe = true;
+      for (int l = 0; l < nl; ++l) {
+        const float pm = hpn[l];
+        if (!(pm <= 1e30f) || (pm > 0.0f && pm < 1e-30f)) tc_safe = false;
+      }
+      ctx->has_tc = tc_safe;
     }
   } else {
     // chunk bounds: the reference row bounds (ChunkPlan.bounds) mapped to the
@@ -918,6 +953,8 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.row_base = ctx->tc_row_base;
     t.centroid = ctx->tc_centroid;
     t.pnmax = ctx->tc_pnmax;
+    t.cbase = ctx->tc_cbase;
+    t.box = ctx->tc_box;
     t.kth = ctx->kthv;
     t.d = ctx->d;
     t.qstride = ctx->D;
@@ -967,7 +1004,36 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
       R.leafscan_launches++;
       return BKT_OK;
     }
+    const bool skipdiag = R.counters && std::getenv("BKT_TC_SKIPDIAG");
+    if (skipdiag) {
+      // how many (tile, chunk) pairs some query of the tile needs (box lower
+      // bound <= its k-th distance at the tile start), per round
+      constexpr int kNeedCap = 1 << 21;
+      if (!ctx->tc_need) CU(cudaMalloc(&ctx->tc_need, sizeof(unsigned long long) * kNeedCap));
+      CU(cudaMemsetAsync(ctx->tc_need, 0, sizeof(unsigned long long) * kNeedCap, ctx->stream));
+      t.need_dbg = ctx->tc_need;
+    }
     CU(launch_leafscan_tc(ctx->KT, R.kb, R.fma, R.grid_scan, ctx->stream, t, nullptr, R.tc_rows, R.tc_cps));
+    if (skipdiag) {
+      int nt = 0;
+      CU(cudaMemcpyAsync(&nt, &ctx->ctl->num_tiles, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      nt = std::min(nt, 1 << 21);
+      std::vector<int4> tiles(nt);
+      std::vector<unsigned long long> need(nt);
+      std::vector<long long> rbh(ctx->nl + 1);
+      CU(cudaMemcpy(tiles.data(), ctx->tiles, sizeof(int4) * nt, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(need.data(), ctx->tc_need, sizeof(unsigned long long) * nt, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(rbh.data(), ctx->tc_row_base, sizeof(long long) * (ctx->nl + 1), cudaMemcpyDeviceToHost));
+      long long tot = 0, nd = 0;
+      for (int i = 0; i < nt; ++i) {
+        const long long nc = std::min(64ll, (rbh[tiles[i].x + 1] - rbh[tiles[i].x] + 127) / 128);
+        tot += nc;
+        nd += __builtin_popcountll(need[i]);
+      }
+      std::fprintf(stderr, "skipdiag launch %d tiles %d cta_chunks %lld cta_needed %lld (%.3f)\n", R.leafscan_launches, nt,
+                   tot, nd, tot ? (double)nd / tot : 0.0);
+    }
     if (R.ctr_rounds && R.leafscan_launches < R.ctr_rounds_cap)
       CU(cudaMemcpyAsync(R.ctr_rounds + 16 * R.leafscan_launches, ctx->tc_ctr, sizeof(unsigned long long) * 16,
                          cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1490,8 +1556,8 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     CU(cudaMemcpy(c, ctx->tc_ctr, sizeof(c), cudaMemcpyDeviceToHost));
     std::fprintf(stderr,
                  "tc counters: groups %llu any %llu survivors %llu loop_trips %llu merges %llu tiles %llu "
-                 "queries %llu first_visit_survivors %llu pairs %llu inserted %llu\n",
-                 c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], pairs, c[8]);
+                 "queries %llu first_visit_survivors %llu pairs %llu inserted %llu warp_chunks %llu warp_needed %llu\n",
+                 c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], pairs, c[8], c[9], c[10]);
   }
   if (std::getenv("BKT_TRACE_ROUNDS") && !per_launch.empty()) {
     // per-round diagnostics of the last batch: active queries and leafscan ms

@@ -89,6 +89,9 @@ struct TcArgs {
   const long long* row_base;   // nl + 1, first padded row of each leaf (multiples of 32)
   const float* centroid;       // nl x KT
   const float* pnmax;          // nl: max over the leaf of |p - c|^2 (upper-bound helper)
+  const int* cbase;            // nl + 1: first 128-row chunk of each leaf
+  const float* box;            // per 128-row chunk: lo[d], hi[d]
+  unsigned long long* need_dbg;  // diagnostics (BKT_TC_SKIPDIAG): per tile, chunks some query needs
   float* kth;                  // per query: current k-th distance (== key_dist(keys[k-1]))
   int d;                       // real dimensionality
   int qstride;                 // row stride of the query block (kernel D of the direct path)
@@ -648,7 +651,13 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         if (A.ctr) { c_tile += 1; c_q += valid ? 1 : 0; }
       }
       const float qnc = (1.0f - kTcMargin) * qn;
+      // The error bound needs |q'|^2 in [1e-30, 1e30] (no overflow, no flushed
+      // products; the load-time check covers the points).  Rows outside it
+      // pass every point to the exact re-evaluation (comparisons below are
+      // written !(v > thr) so that NaN from an overflowed dot product passes).
+      const bool force = valid && !(qn >= 1e-30f && qn <= 1e30f);
       auto threshold = [&](float kk) {
+        if (force) return __int_as_float(0x7f800000);
         // kth - (1 - C) qn, rounded up by a hair so the fp32 subtraction cannot cut a candidate
         float t0 = __fsub_ru(kk, qnc);
         return t0 + 1e-6f * (fabsf(kk) + qnc);
@@ -704,7 +713,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         if constexpr (kTcDiag) c_grp += 1;
         uint32_t mask = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) <= thr ? 1u : 0u) << j;
+        for (int j = 0; j < 32; ++j) mask |= (!(__uint_as_float(v[j]) > thr) ? 1u : 0u) << j;
         if constexpr (kTcDiag) {
           c_any += 1;
           c_surv += __popc(mask);
@@ -732,7 +741,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
                 else acc = __fadd_rn(acc, __fmul_rn(df, df));
               }
             }
-            if (acc <= kflt) {
+            if (acc <= kflt && ids[j] != kIndexSentinel) {  // padding rows pass only forced rows
               qslot[(cn++) * kNT] = pack_key(acc, ids[j]);
               if constexpr (kTcDiag) c_ins += 1;
             }
@@ -756,6 +765,28 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         const int s = g % kTcStages;
         const uint32_t b = g % kTcBufs;
         const long long te0 = kTcDiag ? clock64() : 0;
+        if constexpr (kTcDiag) {
+          if (A.need_dbg) {
+            // could this warp / this tile skip the chunk?  box lower bound vs
+            // the k-th distance at the tile start (later visits only)
+            const float* bx = A.box + (long long)(__ldg(A.cbase + cu.leaf) + c) * 2 * d;
+            float lb = 0.0f;
+            for (int j = 0; j < d; ++j) {
+              const float qj = sq[j * 128];
+              const float e = fmaxf(fmaxf(__ldg(bx + j) - qj, qj - __ldg(bx + d + j)), 0.0f);
+              lb = __fmaf_rn(e, e, lb);
+            }
+            const bool need = valid && !(lb * 0.99999f > kth_in);
+            const unsigned bal = __ballot_sync(0xffffffffu, need), anyv = __ballot_sync(0xffffffffu, valid);
+            if (lane == 0 && anyv && !first_visit) {
+              atomicAdd(A.ctr + 9, 1ull);
+              if (bal) {
+                atomicAdd(A.ctr + 10, 1ull);
+                if (c < 64) atomicOr(A.need_dbg + t, 1ull << c);
+              }
+            }
+          }
+        }
         // Only the accumulator is waited for here.  The stage's ids and
         // coordinates (TMA -> full[s]) are read by survivor re-evaluation
         // alone, which waits for full[s] itself; most chunks have none.
@@ -793,7 +824,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
 #pragma unroll
             for (int i = 0; i < KB; ++i) gmax = fmaxf(gmax, gm[i]);
             const float kub = __fadd_ru(__fadd_ru(gmax, qn), 2.0f * kTcMargin * (qn + cu.pnmax) * 1.0001f);
-            if (first_visit && kub < kflt) {
+            if (first_visit && !force && kub < kflt) {
               kflt = kub;
               thr = threshold(kflt);
             }
@@ -834,13 +865,13 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
 #pragma unroll
         for (int gi = 1; gi < kGrp; ++gi) mchunk = fminf(mchunk, gmn[gi]);
         if (dbg_on) A.dbg[16 * g + 8] = clock64();
-        if (__any_sync(0xffffffffu, mchunk <= thr)) {
+        if (__any_sync(0xffffffffu, !(mchunk > thr))) {
           mbar_wait(&full[s], (g / kTcStages) & 1u);
           load_qv();
           if (NR == 64) {
             // both groups are still in registers
-            if (__any_sync(0xffffffffu, gmn[0] <= thr)) process(va, 0, s);
-            if (__any_sync(0xffffffffu, gmn[1] <= thr)) process(vb, 32, s);
+            if (__any_sync(0xffffffffu, !(gmn[0] > thr))) process(va, 0, s);
+            if (__any_sync(0xffffffffu, !(gmn[1] > thr))) process(vb, 32, s);
           } else {
 #pragma unroll 1
             for (int gi = 0; gi < ngrp; ++gi) {
@@ -848,7 +879,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
               float gv = gmn[0];
 #pragma unroll
               for (int j = 1; j < kGrp; ++j) gv = gi == j ? gmn[j] : gv;
-              if (!__any_sync(0xffffffffu, gv <= thr)) continue;
+              if (!__any_sync(0xffffffffu, !(gv > thr))) continue;
               tmem_ld32_async(tbase + 32 * gi, va);
               tmem_wait(va);
               process(va, 32 * gi, s);

@@ -21,6 +21,7 @@ and real device buffers:
 from __future__ import annotations
 
 import ctypes
+import threading
 import time
 from dataclasses import dataclass
 
@@ -122,6 +123,9 @@ class GpuDevice:
         self._tree_key = None
         self._tree_ref = None
         self._closed = False
+        # One bkt context serves one call at a time (include/bkt.h): calls
+        # from several host threads on this device serialise here.
+        self.lock = threading.RLock()
         h = ctypes.c_void_p()
         _native.check(_native.lib().bkt_open(int(spec.cuda_device), ctypes.byref(h)))
         self._ctx = h
@@ -168,8 +172,12 @@ class GpuDevice:
         num = 1 if plan is None else plan.num_chunks
         bounds = None if plan is None else np.ascontiguousarray(plan.bounds, dtype=np.int64)
         key = (id(tree), num, None if bounds is None else bounds.tobytes())
-        if self._tree_key == key and self._tree_ref is tree:
-            return
+        with self.lock:
+            if self._tree_key == key and self._tree_ref is tree:
+                return
+            self._load_tree(tree, num, bounds, key)
+
+    def _load_tree(self, tree, num, bounds, key) -> None:
         top, leaves = tree.top, tree.leaves
         pts = np.ascontiguousarray(np.asarray(leaves.points), dtype=np.float32)
         orig = np.ascontiguousarray(leaves.original_index, dtype=np.int64)
@@ -184,8 +192,12 @@ class GpuDevice:
 
     def search(self, queries: np.ndarray, k: int, *, exact: bool = True, visited: np.ndarray | None = None,
                seq_cap: int = 0, timing: bool = False, batch_queries: int = 0,
-               out_keys: np.ndarray | None = None, kernel: str = "auto") -> tuple[np.ndarray, dict, np.ndarray | None]:
-        """bkt_search on host arrays; returns (keys, stats, seq triples)."""
+               out_keys: np.ndarray | None = None, kernel: str = "auto",
+               allow_seq_overflow: bool = False) -> tuple[np.ndarray, dict, np.ndarray | None]:
+        """bkt_search on host arrays; returns (keys, stats, seq triples).
+        stats["seq_needed"] is the number of visits the device counted; with
+        allow_seq_overflow a log smaller than that is returned truncated
+        (the caller repeats the search with the exact size)."""
         q = np.ascontiguousarray(queries, dtype=np.float32)
         m = q.shape[0]
         keys = out_keys if out_keys is not None else _native.host_empty((m, k), np.uint64)
@@ -204,13 +216,16 @@ class GpuDevice:
             opts.seq_cap = int(seq_cap)
             opts.seq_count_out = ctypes.addressof(seq_count)
         st = _native.Stats()
-        _native.check(_native.lib().bkt_search(self.ctx, _native.ptr(q), m, int(k), ctypes.byref(opts),
-                                               _native.ptr(keys), ctypes.byref(st)), self.ctx)
+        with self.lock:
+            _native.check(_native.lib().bkt_search(self.ctx, _native.ptr(q), m, int(k), ctypes.byref(opts),
+                                                   _native.ptr(keys), ctypes.byref(st)), self.ctx)
+        out = st.as_dict()
         if seq is not None:
-            if seq_count.value > seq_cap:
+            out["seq_needed"] = int(seq_count.value)
+            if seq_count.value > seq_cap and not allow_seq_overflow:
                 raise RuntimeError("leaf sequence log overflowed")
-            seq = seq[: seq_count.value]
-        return keys, st.as_dict(), seq
+            seq = seq[: min(seq_count.value, seq_cap)]
+        return keys, out, seq
 
     def search_device(self, q_dev_ptr: int, m: int, k: int, keys_dev_ptr: int, *, exact: bool = True,
                       timing: bool = False, kernel: str = "auto") -> dict:
@@ -223,9 +238,10 @@ class GpuDevice:
         opts.record_timing = 1 if timing else 0
         opts.kernel = _KERNELS[kernel]
         st = _native.Stats()
-        _native.check(_native.lib().bkt_search(self.ctx, ctypes.c_void_p(q_dev_ptr), int(m), int(k),
-                                               ctypes.byref(opts), ctypes.c_void_p(keys_dev_ptr),
-                                               ctypes.byref(st)), self.ctx)
+        with self.lock:
+            _native.check(_native.lib().bkt_search(self.ctx, ctypes.c_void_p(q_dev_ptr), int(m), int(k),
+                                                   ctypes.byref(opts), ctypes.c_void_p(keys_dev_ptr),
+                                                   ctypes.byref(st)), self.ctx)
         return st.as_dict()
 
     # --------------------------------------------------------- fine seam
@@ -320,15 +336,19 @@ def device_init(spec: DeviceSpec, chunk_bytes: int | None = None, query_block_by
 
 
 _DEFAULT: dict[int, GpuDevice] = {}
+_DEFAULT_LOCK = threading.Lock()
 
 
 def default_device(cuda_device: int = 0) -> GpuDevice:
-    """Process-wide device used when lazy_search gets device=None."""
-    dev = _DEFAULT.get(cuda_device)
-    if dev is None or dev._closed:
-        dev = GpuDevice(DeviceSpec(cuda_device=cuda_device))
-        _DEFAULT[cuda_device] = dev
-    return dev
+    """Process-wide device used when lazy_search gets device=None (its
+    ``lock`` serialises concurrent callers; the reference instead builds a
+    private simulated device per call, buffer_tree.py:553-561)."""
+    with _DEFAULT_LOCK:
+        dev = _DEFAULT.get(cuda_device)
+        if dev is None or dev._closed:
+            dev = GpuDevice(DeviceSpec(cuda_device=cuda_device))
+            _DEFAULT[cuda_device] = dev
+        return dev
 
 
 class ChunkPipeline:

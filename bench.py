@@ -136,6 +136,19 @@ def job_value(total_queries: int, steps: int, rank_seconds: list[float]) -> floa
     return steps * total_queries / max(rank_seconds)
 
 
+def reduce_ranks(dev_ms: float, e2e_s: float | None, parity_ok: bool | None, device=None) -> dict:
+    """The only cross-rank traffic of a bench run: the slowest rank's device
+    and end-to-end times (max over ranks) and the AND of the per-rank parity
+    checks.  Every rank calls it in the same order (collectives)."""
+    from paper_1512_02831_b200.dist import max_over_ranks
+    out = {"dev_ms_max": max_over_ranks(dev_ms, device=device)}
+    if e2e_s is not None:
+        out["e2e_s_max"] = max_over_ranks(e2e_s, device=device)
+    if parity_ok is not None:
+        out["parity_all"] = -max_over_ranks(-float(parity_ok), device=device) >= 1.0
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -298,7 +311,6 @@ def main() -> None:
     red_t = torch.device("cpu") if shared else dev_t
 
     import paper_1512_02831_b200 as bkt
-    from paper_1512_02831_b200.dist import max_over_ranks
     w = rank_work(a.scaling, rank, world, a.n, a.m)
     refs, queries = workload(w, a.n, a.m)
     m = queries.shape[0]
@@ -376,24 +388,27 @@ def main() -> None:
         # device and host paths must agree
         if not np.array_equal(res.keys, keys_dev[:m].cpu().numpy().view(np.uint64)):
             raise RuntimeError("device-resident and host API results differ")
-        e2e_time_max = max_over_ranks(tot, device=red_t)
-        e2e = {"value": job_value(w["total"], e2e_steps, [e2e_time_max]), "unit": UNIT,
-               "h2d_bytes_per_step": int(m * DIM * 4), "d2h_bytes_per_step": int(m * K * 8)}
-
-    # reductions across ranks: the slowest rank's device time
-    dev_ms_max = max_over_ranks(dev_ms, device=red_t)
-    value = job_value(w["total"], a.steps, [dev_ms_max / 1e3])
+        e2e = {"steps": e2e_steps, "seconds": tot}
 
     # every rank checks a sample of its own rows against the CPU oracle
     threads = os.cpu_count() or 1
     otree = None
-    parity = None
+    ok = None
     if a.check_rows > 0:
         otree = oracle_tree_of(tree)
         ok = check_rows(otree, queries, keys_dev[:m].cpu().numpy(), a.check_rows,
                         max(1, threads // max(1, world)), exact)
-        ok_all = -max_over_ranks(-float(ok), device=red_t)  # min over ranks
-        parity = {"rows_per_rank": min(a.check_rows, m), "ranks": world, "all_match": bool(ok_all >= 1.0),
+
+    # reductions across ranks: the slowest rank's device / e2e time, parity AND
+    red = reduce_ranks(dev_ms, e2e["seconds"] if e2e else None, ok, device=red_t)
+    dev_ms_max = red["dev_ms_max"]
+    value = job_value(w["total"], a.steps, [dev_ms_max / 1e3])
+    if e2e is not None:
+        e2e = {"value": job_value(w["total"], e2e["steps"], [red["e2e_s_max"]]), "unit": UNIT,
+               "h2d_bytes_per_step": int(m * DIM * 4), "d2h_bytes_per_step": int(m * K * 8)}
+    parity = None
+    if ok is not None:
+        parity = {"rows_per_rank": min(a.check_rows, m), "ranks": world, "all_match": bool(red["parity_all"]),
                   "rule": "exact: bit-identical keys" if exact else "fma: distances within 1e-5 relative"}
 
     # Roofline of the dominant kernel (the leaf scan).  It runs on the tensor

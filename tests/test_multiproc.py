@@ -1,4 +1,4 @@
-"""World-size-2 CPU coverage of the N>1 path (gloo): query shards per rank,
+"""World-size-2 CPU coverage of the N>1 path (gloo): bench.py's query shards per rank,
 no data-path collective, results gathered only for checking, timing reduced
 as the max over ranks -- the same host logic bench.py runs under torchrun
 with NCCL on B200s.  The per-rank search here is the CPU oracle (no GPU in
@@ -24,27 +24,31 @@ def _free_port() -> int:
 
 
 def _worker(rank, world, port, out):
+    """One rank of bench.py's multi-rank flow at a small size: the rank's
+    workload (bench.rank_work / bench.workload), a per-rank search (the CPU
+    oracle stands in for the B200 engine here), the per-rank parity check
+    (bench.check_rows) and the only cross-rank traffic (bench.reduce_ranks,
+    bench.job_value)."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import torch
+    import bench
     from oracle import oracle as O
-    rng = np.random.default_rng(5)
-    refs = rng.random((3000, 6), dtype=np.float32)
-    queries = rng.random((1001, 6), dtype=np.float32)
-    tree = O.build_tree(refs, 5)
-    lo, hi = shard_range(queries.shape[0], rank, world)
-    keys = O.knn_tree(tree, queries[lo:hi], 7)["keys"]
-    t = max_over_ranks(float(rank + 1))
-    # gather shards (checking only; the search itself exchanged nothing)
-    sizes = [None] * world
-    dist.all_gather_object(sizes, (lo, hi, keys.view(np.int64).tolist()))
+    n, m = 4000, 1001
+    res = {}
+    for scaling in ("strong", "weak"):
+        w = bench.rank_work(scaling, rank, world, n, m)
+        refs, queries = bench.workload(w, n, m)
+        otree = O.build_tree(refs, 5)
+        keys = O.knn_tree(otree, queries, bench.K)["keys"]
+        ok = bench.check_rows(otree, queries, keys.view(np.int64), 50, 1, True)
+        red = bench.reduce_ranks(float(rank + 1), 0.5 * (rank + 1), ok)
+        value = bench.job_value(w["total"], 3, [red["dev_ms_max"] / 1e3])
+        parts = [None] * world
+        dist.all_gather_object(parts, (w, queries.tolist(), keys.view(np.int64).tolist()))
+        res[scaling] = (red, value, parts, refs)
     if rank == 0:
-        full = np.zeros((queries.shape[0], 7), np.uint64)
-        for lo_, hi_, k_ in sizes:
-            full[lo_:hi_] = np.asarray(k_, np.int64).view(np.uint64).reshape(hi_ - lo_, 7)
-        want = O.brute_keys(refs, queries, 7)
-        out.put((bool(np.array_equal(full, want)), t))
+        out.put(res)
     dist.destroy_process_group()
 
 
@@ -60,16 +64,39 @@ def test_shard_range_partitions():
         shard_range(5, 2, 2)
 
 
-def test_two_rank_gloo_sharded_search():
+def test_two_rank_gloo_bench_flow():
+    """bench.py's rank logic on two gloo ranks: strong scaling shards the
+    config-2 queries exactly (the shards concatenate to the single-rank
+    queries and their results to the single-rank results), weak scaling gives
+    rank 1 config 3's chunk 1, timings reduce to the slowest rank and parity
+    to the AND over ranks."""
+    import bench
+    from oracle import oracle as O
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
+    res = q.get(timeout=180)
     for p in procs:
-        p.join(timeout=120)
+        p.join(timeout=60)
     assert all(p.exitcode == 0 for p in procs)
-    ok, tmax = q.get(timeout=5)
-    assert ok
-    assert tmax == 2.0
+    n, m = 4000, 1001
+    refs_all, q_all = bench.mixture_rows(n, m, 0, m)
+    want = O.knn_tree(O.build_tree(refs_all, 5), q_all, bench.K)["keys"]
+    # strong: shards partition the queries; whole job = m queries per step
+    red, value, parts, refs = res["strong"]
+    assert np.array_equal(refs, refs_all)
+    assert [p_[0]["lo"] for p_ in parts] == [0, 501] and parts[-1][0]["hi"] == m
+    assert np.array_equal(np.concatenate([np.asarray(p_[1], np.float32) for p_ in parts]), q_all)
+    got = np.concatenate([np.asarray(p_[2], np.int64).view(np.uint64) for p_ in parts])
+    assert np.array_equal(got, want)
+    assert red == {"dev_ms_max": 2.0, "e2e_s_max": 1.0, "parity_all": True}
+    assert value == 3 * m / 2e-3
+    # weak: rank 0 the config-2 queries, rank 1 config 3's chunk 1; total = 2m per step
+    red, value, parts, _ = res["weak"]
+    assert parts[0][0]["kind"] == "cfg2" and parts[1][0] == {"kind": "chunk", "chunk": 1, "size": m, "total": 2 * m}
+    assert np.array_equal(np.asarray(parts[0][1], np.float32), q_all)
+    assert np.array_equal(np.asarray(parts[1][1], np.float32), bench.query_chunk(1, m))
+    assert value == 3 * 2 * m / 2e-3

@@ -196,7 +196,7 @@ int main(int argc, char **argv) {
     tot[hm] += nc; needc[hm] += __builtin_popcountll(recs[i].need);
   }
   printf("per-query needed chunk fraction: later visits %.4f, home visits %.4f\n", needc[0] / tot[0], needc[1] / tot[1]);
-  int tiles[] = {1, 2, 3, 4, 8, 13};
+  int tiles[] = {1, 13, 26, 52, 128, 256};
   for (order_mode = 0; order_mode < 2; ++order_mode) {
     qsort(recs, nr, sizeof(rec_t), cmprec);
     for (int ti = 0; ti < 6; ++ti) {

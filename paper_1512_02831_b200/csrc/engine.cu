@@ -32,6 +32,7 @@
 #include "dims.h"
 #include "leafscan_tc.cuh"
 #include "round_kernels.cuh"
+#include "split_launch.cuh"
 
 using namespace bkt;
 
@@ -109,6 +110,12 @@ struct bkt_ctx {
   int nbuckets = 0;           // nl * sub_w
   int* blk_base = nullptr;    // nl + 1: first block of each leaf
   int4* nodes = nullptr;      // {split value bits, dim, left, right}; child < 0: ~local block
+  // split rounds (split_scan.cuh): each leaf's chunks grouped into windows
+  // of split_W consecutive 128-row chunks; key = leaf * split_NW + window
+  int split_W = 0, split_NW = 0;  // split_NW == 0: split rounds unavailable
+  int min_leaf = 0;                // smallest leaf (split rounds need kth finite after the home visit)
+  int* win_base = nullptr;         // nl + 1
+  float* win_box = nullptr;        // per window: lo[d], hi[d]
 
   // ---- per-batch work buffers
   long long cap_m = 0;
@@ -157,6 +164,25 @@ struct bkt_ctx {
   uint64_t* keys_alt = nullptr;
   long long cap_alt = 0;
   int cap_alt_k = 0;
+  // query renumbering (capacity perm_cap queries)
+  long long perm_cap = 0;
+  int perm_k = 0;
+  int* perm = nullptr;          // search id -> caller's id
+  float* q_perm = nullptr;      // m x D rows in search order
+  uint64_t* keys_tmp = nullptr; // m x k
+  uint32_t* visits_tmp = nullptr;
+  // split-round per-query buffers (capacity split_cap queries)
+  long long split_cap = 0;
+  float* arow = nullptr;                 // m x kSplitKT
+  int* ccnt = nullptr;                   // m
+  uint64_t* cand = nullptr;              // m x kSplitCap
+  int* ovf = nullptr;                    // m
+  unsigned long long* qmask = nullptr;   // m
+  int* cbase = nullptr;                  // route tiles x split_NW
+  int* items = nullptr;                  // m x split_NW
+  int* stoff = nullptr;                  // nl * split_NW + 1
+  int4* stiles = nullptr;
+  long long stiles_cap = 0;
 
   std::vector<cudaEvent_t> ev_pool;   // leafscan timing events
   cudaEvent_t ring_ev[4] = {};        // round-check ring (kRing)
@@ -240,6 +266,8 @@ void free_tree(bkt_ctx* c) {
   dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid); dfree(c->tc_pnmax); dfree(c->tc_cbase); dfree(c->tc_box);
   c->has_tc = false;
   dfree(c->blk_base); dfree(c->nodes);
+  dfree(c->win_base); dfree(c->win_box);
+  c->split_W = 0; c->split_NW = 0;
   c->nkeys = 0;
   dfree(c->split); dfree(c->quad_base); dfree(c->leaf_size); dfree(c->pts); dfree(c->pidx);
   hfree(c->h_pts); hfree(c->h_pidx);
@@ -261,6 +289,50 @@ void free_work(bkt_ctx* c) {
   c->cap_m = 0; c->cap_k = 0;
   dfree(c->q_alt); dfree(c->q_raw_alt); dfree(c->keys_alt);
   c->cap_alt = 0; c->cap_alt_k = 0;
+  dfree(c->arow); dfree(c->ccnt); dfree(c->cand); dfree(c->ovf); dfree(c->qmask); dfree(c->cbase);
+  dfree(c->items); dfree(c->stoff); dfree(c->stiles);
+  c->split_cap = 0; c->stiles_cap = 0;
+  dfree(c->perm); dfree(c->q_perm); dfree(c->keys_tmp); dfree(c->visits_tmp);
+  c->perm_cap = 0; c->perm_k = 0;
+}
+
+int ensure_perm(bkt_ctx* ctx, long long m, int k) {
+  if (ctx->perm_cap >= m && ctx->perm_k >= k) return BKT_OK;
+  dfree(ctx->perm); dfree(ctx->q_perm); dfree(ctx->keys_tmp); dfree(ctx->visits_tmp);
+  const long long M = std::max<long long>(m, 1);
+  CU(cudaMalloc(&ctx->perm, sizeof(int) * M));
+  CU(cudaMalloc(&ctx->q_perm, sizeof(float) * M * ctx->D));
+  CU(cudaMalloc(&ctx->keys_tmp, sizeof(uint64_t) * M * k));
+  CU(cudaMalloc(&ctx->visits_tmp, sizeof(uint32_t) * M));
+  ctx->perm_cap = M;
+  ctx->perm_k = k;
+  return BKT_OK;
+}
+
+// per-query bytes of the split-round buffers
+long long split_bytes_per_query(const bkt_ctx* c) {
+  return 4ll * kSplitKT + 4 + 8ll * kSplitCap + 4 + 8 + 4ll * c->split_NW + 16ll * c->split_NW / kNT + 16;
+}
+
+int ensure_split(bkt_ctx* ctx, long long m) {
+  if (ctx->split_cap >= m) return BKT_OK;
+  dfree(ctx->arow); dfree(ctx->ccnt); dfree(ctx->cand); dfree(ctx->ovf); dfree(ctx->qmask); dfree(ctx->cbase);
+  dfree(ctx->items); dfree(ctx->stoff); dfree(ctx->stiles);
+  const long long M = std::max<long long>(m, 1);
+  const long long NW = ctx->split_NW;
+  CU(cudaMalloc(&ctx->arow, sizeof(float) * M * kSplitKT));
+  CU(cudaMalloc(&ctx->ccnt, sizeof(int) * M));
+  CU(cudaMemset(ctx->ccnt, 0, sizeof(int) * M));
+  CU(cudaMalloc(&ctx->cand, sizeof(uint64_t) * M * kSplitCap));
+  CU(cudaMalloc(&ctx->ovf, sizeof(int) * M));
+  CU(cudaMalloc(&ctx->qmask, sizeof(unsigned long long) * M));
+  CU(cudaMalloc(&ctx->cbase, sizeof(int) * (M / kRouteQ + ctx->nl + 1) * NW));
+  CU(cudaMalloc(&ctx->items, sizeof(int) * M * NW));
+  CU(cudaMalloc(&ctx->stoff, sizeof(int) * ((long long)ctx->nl * NW + 1)));
+  ctx->stiles_cap = M * NW / kNT + (long long)ctx->nl * NW + 1;
+  CU(cudaMalloc(&ctx->stiles, sizeof(int4) * ctx->stiles_cap));
+  ctx->split_cap = M;
+  return BKT_OK;
 }
 
 int ensure_alt(bkt_ctx* ctx, long long m, int k) {
@@ -783,6 +855,39 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
         CU(cudaMemcpy(ctx->tc_cbase, cb.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice));
         CU(cudaMalloc(&ctx->tc_box, sizeof(float) * box.size()));
         CU(cudaMemcpy(ctx->tc_box, box.data(), sizeof(float) * box.size(), cudaMemcpyHostToDevice));
+        if (KT == kSplitKT && d <= kSplitKT - 3) {
+          // split rounds: windows of W consecutive chunks (<= 64 per leaf), box = union of its chunks
+          int W = 2;
+          if (const char* e = std::getenv("BKT_SPLIT_W")) W = std::max(1, std::atoi(e));
+          int maxch = 1;
+          for (int l = 0; l < nl; ++l) maxch = std::max(maxch, cb[l + 1] - cb[l]);
+          while ((maxch + W - 1) / W > 64) W *= 2;
+          std::vector<int> wb(nl + 1, 0);
+          for (int l = 0; l < nl; ++l) wb[l + 1] = wb[l] + (cb[l + 1] - cb[l] + W - 1) / W;
+          std::vector<float> wbox((size_t)wb[nl] * 2 * d);
+          int NW = 1;
+          for (int l = 0; l < nl; ++l) {
+            const int nch = cb[l + 1] - cb[l];
+            NW = std::max(NW, wb[l + 1] - wb[l]);
+            for (int w = 0; w < wb[l + 1] - wb[l]; ++w) {
+              float* bx = wbox.data() + (size_t)(wb[l] + w) * 2 * d;
+              for (int j = 0; j < d; ++j) { bx[j] = __builtin_inff(); bx[d + j] = -__builtin_inff(); }
+              for (int c = w * W; c < std::min(nch, (w + 1) * W); ++c) {
+                const float* cx = box.data() + (size_t)(cb[l] + c) * 2 * d;
+                for (int j = 0; j < d; ++j) {
+                  bx[j] = std::min(bx[j], cx[j]);
+                  bx[d + j] = std::max(bx[d + j], cx[d + j]);
+                }
+              }
+            }
+          }
+          CU(cudaMalloc(&ctx->win_base, sizeof(int) * (nl + 1)));
+          CU(cudaMemcpy(ctx->win_base, wb.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice));
+          CU(cudaMalloc(&ctx->win_box, sizeof(float) * wbox.size()));
+          CU(cudaMemcpy(ctx->win_box, wbox.data(), sizeof(float) * wbox.size(), cudaMemcpyHostToDevice));
+          ctx->split_W = W;
+          ctx->split_NW = NW;
+        }
       }
       ctx->KT = KT;
       ctx->tc_rows = R;
@@ -852,7 +957,8 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
     int w = std::atoi(e);
     if (w >= 1 && (w & (w - 1)) == 0) ctx->sub_w = w;
   }
-  ctx->nbuckets = nl * ctx->sub_w;
+  ctx->nbuckets = nl * std::max(ctx->sub_w, ctx->split_NW);
+  ctx->min_leaf = *std::min_element(ctx->h_leaf_size.begin(), ctx->h_leaf_size.end());
   if (ensure_leafbufs(ctx, nl, ctx->nbuckets) != BKT_OK) return BKT_ECUDA;
   ctx->has_tree = true;
   return BKT_OK;
@@ -895,6 +1001,9 @@ struct SearchRun {
   long long drain_at = -1;
   long long finish_at = -1;  // tail finisher: one launch once at most this many queries remain (-1: off)
   bool finish_cta = false;   // finisher with one CTA per query (else one warp per query)
+  bool split = false;        // later rounds as (leaf, window) items (split_scan.cuh)
+  bool renumber = false;     // search in home-bucket order (gather_rows_kernel)
+  int split_from = 1;        // first split round (earlier rounds: leaf-level tiles)
   bool drain_fired = false;
   std::function<void()> drain_start;
 };
@@ -1117,13 +1226,219 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
 }
 
 // One batch: queries already in ctx->q (m x D).  Runs rounds until no query is active.
+// one launch of the tail finisher over `list` (ctl->active entries)
+int launch_finisher(bkt_ctx* ctx, SearchRun& R, const int* list) {
+  const int blocks = (int)std::max<long long>(1, (R.finish_at + kFinishWarps - 1) / kFinishWarps);
+  const TopTreeView top{ctx->split, ctx->h, ctx->d};
+  int* seq = R.seq ? ctx->seq_dev : nullptr;
+  const int cta_blocks = (int)std::max<long long>(1, std::min<long long>(R.finish_at, ctx->sm_count * 8ll));
+  if (R.finish_cta && R.fma)
+    finish_cta_kernel<true><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
+        list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+  else if (R.finish_cta)
+    finish_cta_kernel<false><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
+        list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+  else if (R.fma)
+    finish_kernel<true><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
+        list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+  else
+    finish_kernel<false><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
+        list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
+        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+  CU(cudaGetLastError());
+  R.launches++;
+  return BKT_OK;
+}
+
+// advance over `list` (ctl->active entries): merge, FindLeaf, next-leaf bucket slot, A row
+int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
+  AdvanceArgs a{};
+  a.list = list;
+  a.ctl = ctx->ctl;
+  a.pos = ctx->pos;
+  a.counts = ctx->counts;
+  a.q = ctx->q;
+  a.D = ctx->D;
+  a.k = R.k;
+  a.top = TopTreeView{ctx->split, ctx->h, ctx->d};
+  a.keys = ctx->keys;
+  a.kthv = ctx->kthv;
+  a.state = ctx->state;
+  a.next = ctx->next;
+  a.visits = ctx->visits;
+  a.ccnt = ctx->ccnt;
+  a.cand = ctx->cand;
+  a.centroid = ctx->tc_centroid;
+  a.arow = ctx->arow;
+  a.seq_log = R.seq ? ctx->seq_dev : nullptr;
+  a.seq_pos = ctx->seq_pos;
+  a.seq_cap = R.seq_cap;
+  CU(launch_advance(R.kb, R.grid_small, ctx->stream, a));
+  R.launches++;
+  return BKT_OK;
+}
+
+// rounds >= 1 as (leaf, window) items until no query is active.  On entry
+// work[cur ^ 1] holds the queries just advanced (pos = their next leaf and
+// bucket slot, counts per leaf).
+int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
+  cudaEvent_t* ring = ctx->ring_ev;
+  const int nkeys = ctx->nl * ctx->split_NW;
+  for (;;) {
+    // the round's queries bucketed by leaf, in route tiles of kRouteQ
+    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, 1, ctx->nl, ctx->leaf_off,
+                                                     ctx->tile_off, ctx->ctl, ctx->nl, kRouteQ, ctx->hist, kHistCap,
+                                                     ctx->d_ctl_mirror + round % kRing);
+    CU(cudaGetLastError());
+    R.launches++;
+    CU(cudaEventRecord(ring[round % kRing], ctx->stream));
+    scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], 0, ctx->pos, ctx->qkey, ctx->key_off,
+                                                           ctx->work[cur], ctx->ctl, ctx->leaf_off, ctx->tile_off,
+                                                           ctx->nl, 1, kRouteQ, ctx->tiles,
+                                                           (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
+    CU(cudaGetLastError());
+    R.launches++;
+    RouteArgs ra{};
+    ra.work = ctx->work[cur];
+    ra.rtiles = ctx->tiles;
+    ra.ctl = ctx->ctl;
+    ra.kthv = ctx->kthv;
+    ra.q = ctx->q;
+    ra.D = ctx->D;
+    ra.d = ctx->d;
+    ra.NW = ctx->split_NW;
+    ra.win_base = ctx->win_base;
+    ra.win_box = ctx->win_box;
+    ra.leaf_size = ctx->leaf_size;
+    ra.qmask = ctx->qmask;
+    ra.counts = ctx->counts;
+    ra.cbase = ctx->cbase;
+    ra.key_off = ctx->key_off;
+    ra.stoff = ctx->stoff;
+    ra.nkeys = nkeys;
+    ra.items = ctx->items;
+    ra.stiles = ctx->stiles;
+    ra.stiles_cap = (int)std::min<long long>(ctx->stiles_cap, INT32_MAX);
+    ra.pairs = ctx->pairs;
+    CU(launch_route(R.grid_small, ctx->stream, ra));
+    R.launches++;
+    CU(launch_plan_split(ctx->stream, ctx->counts, ctx->key_off, nkeys, ctx->stoff, ctx->ctl));
+    R.launches++;
+    CU(launch_place(R.grid_small, ctx->stream, ra));
+    R.launches++;
+    SplitScanArgs sa{};
+    sa.q = ctx->q;
+    sa.qstride = ctx->D;
+    sa.arow = ctx->arow;
+    sa.ccnt = ctx->ccnt;
+    sa.cand = ctx->cand;
+    sa.ovf = ctx->ovf;
+    sa.novf = &ctx->ctl->novf;
+    sa.items = ctx->items;
+    sa.tiles = ctx->stiles;
+    sa.num_tiles = &ctx->ctl->stiles;
+    sa.tile_next = &ctx->ctl->tile_next;
+    sa.B = ctx->tc_B;
+    sa.ridx = ctx->tc_idx;
+    sa.rows = ctx->tc_rowsxyz;
+    sa.row_base = ctx->tc_row_base;
+    sa.d = ctx->d;
+    sa.W = ctx->split_W;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (R.timing) {
+      e0 = get_event(ctx, R.ev_next++);
+      e1 = get_event(ctx, R.ev_next++);
+      CU(cudaEventRecord(e0, ctx->stream));
+    }
+    CU(launch_splitscan(R.fma, R.grid_scan, ctx->stream, sa));
+    if (R.timing) {
+      CU(cudaEventRecord(e1, ctx->stream));
+      R.scan_events.emplace_back(e0, e1);
+    }
+    R.launches++;
+    R.leafscan_launches++;
+    CU(launch_rescan(R.fma, ctx->sm_count * 4, ctx->stream, ctx->ovf, ctx->ctl, ctx->q, ctx->D, R.k, ctx->d,
+                     ctx->keys, ctx->kthv, ctx->next, ctx->pts, ctx->pidx, ctx->quad_base));
+    R.launches++;
+    int rc = launch_advance_round(ctx, R, ctx->work[cur]);
+    if (rc != BKT_OK) return rc;
+    cur ^= 1;
+    ++round;
+    if (round >= kRing - 1) {
+      const int chk = (int)((round - (kRing - 1)) % kRing);
+      CU(cudaEventSynchronize(ring[chk]));
+      if (ctx->h_ctl[chk].active == 0) break;
+      if (R.finish_at >= 0 && ctx->h_ctl[chk].active <= R.finish_at) {
+        // the list just advanced (work[cur ^ 1], ctl->active entries) holds every
+        // query still active, each with its next leaf set: finish in one launch
+        rc = launch_finisher(ctx, R, ctx->work[cur ^ 1]);
+        if (rc != BKT_OK) return rc;
+        break;
+      }
+    }
+  }
+  return BKT_OK;
+}
+
+int search_batch_impl(bkt_ctx* ctx, SearchRun& R);
+
+// The batch in home-bucket order: a first start/plan/scatter pass orders the
+// queries by (home leaf, home block); the search runs on the reordered rows
+// and its per-query outputs (keys, visit counts, visit log) are mapped back.
 int search_batch(bkt_ctx* ctx, SearchRun& R) {
+  if (!R.renumber || R.m < (1 << 16)) return search_batch_impl(ctx, R);
   const long long m = R.m;
   TopTreeView top{ctx->split, ctx->h, ctx->d};
   RoundCtl init{};
   init.active = (int)m;
   CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
+  start_kernel<<<R.grid_small, kStartQ, start_smem_bytes(ctx->h, ctx->D), ctx->stream>>>(
+      ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits, nullptr, ctx->seq_pos, 0,
+      ctx->kthv, ctx->blk_base, ctx->nodes, ctx->sub_w, ctx->qkey, ctx->counts, ctx->pos);
+  CU(cudaGetLastError());
+  plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, ctx->sub_w, ctx->nl * ctx->sub_w,
+                                                   ctx->leaf_off, ctx->tile_off, ctx->ctl, ctx->nl, kNT, nullptr, 0,
+                                                   nullptr);
+  CU(cudaGetLastError());
+  scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(nullptr, 1, ctx->pos, ctx->qkey, ctx->key_off, ctx->perm,
+                                                         ctx->ctl, ctx->leaf_off, ctx->tile_off, ctx->nl, ctx->sub_w,
+                                                         kNT, ctx->tiles, 0);
+  CU(cudaGetLastError());
+  gather_rows_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->q, ctx->perm, ctx->D, m, ctx->q_perm);
+  CU(cudaGetLastError());
+  R.launches += 4;
+  float* q_caller = ctx->q;
+  ctx->q = ctx->q_perm;
+  int rc = search_batch_impl(ctx, R);
+  ctx->q = q_caller;
+  if (rc != BKT_OK) return rc;
+  unpermute_keys_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->keys, ctx->perm, R.k, m, ctx->keys_tmp);
+  unpermute_u32_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->visits, ctx->perm, m, ctx->visits_tmp);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(ctx->keys, ctx->keys_tmp, sizeof(uint64_t) * m * R.k, cudaMemcpyDeviceToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->visits, ctx->visits_tmp, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+  R.launches += 2;
+  if (R.seq) {
+    remap_seq_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->seq_dev, ctx->seq_pos, R.seq_cap, ctx->perm);
+    CU(cudaGetLastError());
+    R.launches++;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));  // callers read the results from other streams
+  return BKT_OK;
+}
+
+int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
+  const long long m = R.m;
+  TopTreeView top{ctx->split, ctx->h, ctx->d};
+  RoundCtl init{};
+  init.active = (int)m;
+  CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
+  if (R.split) CU(cudaMemsetAsync(ctx->ccnt, 0, sizeof(int) * m, ctx->stream));
   start_kernel<<<R.grid_small, kStartQ, start_smem_bytes(ctx->h, ctx->D), ctx->stream>>>(
       ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
                                                        ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
@@ -1167,9 +1482,19 @@ int search_batch(bkt_ctx* ctx, SearchRun& R) {
     } else {
       ScanArgs a = make_scan_args(ctx, R, cur);
       const bool unfused = R.tc && R.unfused;
-      if (unfused) a.fused = 0;
+      const bool to_split = R.split && round == R.split_from - 1;
+      if (unfused || to_split) a.fused = 0;
       int rc = launch_scan(ctx, R, a);
       if (rc != BKT_OK) return rc;
+      if (to_split) {
+        // this round's rows and kth are final: FindLeaf, next-leaf buckets and
+        // A rows (advance), then the split rounds
+        rc = launch_advance_round(ctx, R, ctx->work[cur]);
+        if (rc != BKT_OK) return rc;
+        rc = split_rounds(ctx, R, cur ^ 1, round + 1);
+        if (rc != BKT_OK) return rc;
+        break;
+      }
       if (unfused) {
         // FindLeaf as its own high-occupancy pass: its dependent top-tree loads
         // then overlap across many warps instead of stalling the scan's epilogue
@@ -1270,6 +1595,15 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   if (R.tc_cps == 3 && !std::getenv("BKT_TC_N")) R.tc_rows = 64;
   if (const char* e = std::getenv("BKT_TC_UNFUSED")) R.unfused = std::atoi(e) != 0;
   if (o.kernel == 2 && !R.tc) return set_err(ctx, BKT_EINVAL, "tensor-core kernel requested but unavailable (needs a resident tree and d <= 31)");
+  // split rounds (split_scan.cuh): tensor-core path with the 16-column layout
+  // (d <= 13), k <= 64 (the rescan's row) and leaves of >= k points (a finite
+  // k-th distance after the home visit); BKT_SPLIT=0 keeps the leaf-level rounds
+  R.split = R.tc && !R.unfused && ctx->split_NW > 0 && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 &&
+            R.tc_cps == 2;
+  if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
+  if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
+  R.renumber = ctx->residency == 0 && !std::getenv("BKT_EARLY_DRAIN");
+  if (const char* e = std::getenv("BKT_RENUMBER")) R.renumber = R.renumber && std::atoi(e) != 0;
   int rc = BKT_OK;
   if (R.tc) {
     // two CTAs per SM (2 x 256 TMEM columns); the attributes are set by the query
@@ -1308,7 +1642,8 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   if (const char* e = std::getenv("BKT_FINISH_CTA")) R.finish_cta = std::atoi(e) != 0;
 
   // batch size: whatever fits comfortably in free memory (or the caller's choice)
-  const long long per_query = 4ll * ctx->D + 4ll * ctx->d + 8ll * k + 4 * 5;
+  const long long per_query = 4ll * ctx->D + 4ll * ctx->d + 8ll * k + 4 * 5 + (R.split ? split_bytes_per_query(ctx) : 0) +
+                              (R.renumber ? 4ll * ctx->D + 8ll * k + 8 : 0);
   long long batch = o.batch_queries;
   if (batch <= 0) {
     size_t fr = 0, to = 0;
@@ -1329,6 +1664,14 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   batch = std::min<long long>(batch, (long long)INT32_MAX / 2);
   rc = ensure_work(ctx, batch, k);
   if (rc != BKT_OK) return rc;
+  if (R.split) {
+    rc = ensure_split(ctx, batch);
+    if (rc != BKT_OK) return rc;
+  }
+  if (R.renumber) {
+    rc = ensure_perm(ctx, batch, k);
+    if (rc != BKT_OK) return rc;
+  }
   if (R.seq) {
     if (ctx->seq_dev_cap < R.seq_cap) {
       dfree(ctx->seq_dev);

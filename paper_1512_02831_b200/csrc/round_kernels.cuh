@@ -32,6 +32,10 @@ struct RoundCtl {
   long long scans;  // (query, leaf) scans so far (SearchStats.leaf_scan_events)
   int late_n;       // early result drain: queries still active when it started
   int tile_next;    // dynamic tile counter of the round's leaf scan (reset by plan_kernel)
+  // split rounds (split_scan.cuh)
+  int stiles;       // (leaf, window) tiles this round
+  int novf;         // queries whose candidate list overflowed this round
+  int items;        // (query, window) work items this round
 };
 
 // Early result drain: remember the queries of the round just scanned (every
@@ -322,6 +326,38 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
     }
     pos[i] = make_int2(nxt, rk);
   }
+}
+
+// Query renumbering (engine.cu search_batch): the batch is searched in home-
+// bucket order -- query j of the search is query perm[j] of the caller -- so
+// that queries with neighbouring ids are spatial neighbours and the per-query
+// arrays of every round are read in runs instead of scattered sectors.
+__global__ void gather_rows_kernel(const float* __restrict__ src, const int* __restrict__ perm, int D, long long m,
+                                   float* __restrict__ dst) {
+  const long long total = m * D;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long j = t / D;
+    dst[t] = __ldg(src + (long long)__ldg(perm + j) * D + (t - j * D));
+  }
+}
+__global__ void unpermute_keys_kernel(const uint64_t* __restrict__ src, const int* __restrict__ perm, int k, long long m,
+                                      uint64_t* __restrict__ dst) {
+  const long long total = m * k;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long j = t / k;
+    dst[(long long)__ldg(perm + j) * k + (t - j * k)] = src[t];
+  }
+}
+__global__ void unpermute_u32_kernel(const uint32_t* __restrict__ src, const int* __restrict__ perm, long long m,
+                                     uint32_t* __restrict__ dst) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x)
+    dst[__ldg(perm + j)] = src[j];
+}
+__global__ void remap_seq_kernel(int* seq_log, const unsigned long long* seq_pos, long long seq_cap,
+                                 const int* __restrict__ perm) {
+  const long long n = min((long long)*seq_pos, seq_cap);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    seq_log[3 * p] = __ldg(perm + seq_log[3 * p]);
 }
 
 // m x d host layout -> m x D kernel layout (zero padded; exact: +0 dims add 0).

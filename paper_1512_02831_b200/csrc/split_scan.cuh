@@ -1,0 +1,768 @@
+// split_scan.cuh -- ProcessAllBuffers' leaf stage for rounds >= 1, split into
+// (leaf, window) work items.
+//
+// Why.  A query that visits a leaf a second time or later (every round after
+// the home round) carries a finite k-th distance kth, and only the part of the
+// leaf inside its kth-ball can change its top-k.  A leaf of the tensor-core
+// layout is ordered as 64-point blocks along a small k-d split tree
+// (engine.cu build_leaf_blocks), so consecutive 128-row chunks are compact
+// boxes; on config 2 a later visit needs only 26% of a leaf's chunks (box
+// lower bound <= kth, tools/skip_sim.c).  A 128-query tile of the leaf-level
+// scan needs the union over its queries -- 94-98% of the chunks, measured on
+// the B200 (BKT_TC_SKIPDIAG) -- so the skip has to happen per query: every
+// query is routed to the windows (W consecutive chunks) it needs, and a tile
+// is (leaf, window, <= 128 queries).
+//
+// Per round (engine.cu split_rounds):
+//   plan, scatter : the queries of the round bucketed by leaf (plan_kernel and
+//              scatter_kernel of round_kernels.cuh, 1024-query route tiles).
+//   route    : per route tile, the leaf's window boxes in shared memory; each
+//              query's needed windows (box lower bound <= kth) -> mask, per
+//              window counts (shared, then one global atomic per tile and
+//              window: the tile's base slot in that key).
+//   plan_split : key offsets and 128-item tiles per key (key = leaf * NW + window).
+//   place    : items into their key's slice (route tile base + shared rank),
+//              and the (leaf, window) tile records.
+//   scan     : splitscan_tc_kernel -- the tensor-core filter of leafscan_tc.cuh
+//              on each tile's window against each query's kth; survivors
+//              re-evaluated in the reference arithmetic; points with
+//              D_ref <= kth are flushed to the query's candidate list.
+//   rescan   : a query whose candidates exceed kSplitCap in one round gets its
+//              whole leaf rescanned by one warp (exact), instead of merging.
+//   advance  : per query -- merge its candidates into the top-k row (the
+//              reference's update_rows, core.py:251-262; any order: the result
+//              is the best k of the row and the leaf), FindLeaf
+//              (buffer_tree.py:330-349) with the new kth, count the next leaf
+//              (bucket slot), write the A row of the next visit
+//              (tf32(q - c_leaf), 1, .., kth, |q - c|^2).
+// A visit none of whose windows can hold a point within kth is a visit with
+// no items: the query still goes through advance the next round.
+//
+// Exactness.  A point can enter the top-k during a visit only if its key is
+// below the k-th key at the visit's start, so its reference distance is
+// <= kth; such a point lies in a window whose box lower bound (computed in
+// f32, relaxed by 1e-5) is <= kth, survives the filter (leafscan_tc.cuh
+// header) and is a candidate.  The top-k after the visit = best k of (row,
+// candidates) = best k of (row, leaf): identical to the reference.
+#pragma once
+#include "leafscan_tc.cuh"
+#include "round_kernels.cuh"
+
+namespace bkt {
+
+constexpr int kSplitKT = 16;     // A row: d coordinates, 1.0 at column d, zeros, kth at KT-2, |q'|^2 at KT-1 (d <= 13)
+constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers up to 3 tiles ahead
+constexpr int kSplitStages = 4;  // TMA ring stages (128-row chunks)
+constexpr int kSplitCap = 32;    // candidates per query and round; beyond it the leaf is rescanned
+constexpr int kSplitThreads = 192;
+
+struct SplitScanArgs {
+  const float* q;            // m x qstride original coordinates (survivor re-evaluation)
+  int qstride;
+  const float* arow;         // m x kSplitKT A rows (advance_kernel)
+  int* ccnt;                 // m: candidates flushed this round
+  uint64_t* cand;            // m x kSplitCap
+  int* ovf;                  // queries whose candidates overflowed (rescan list)
+  int* novf;
+  const int* items;          // this round's items (query ids), grouped by key
+  const int4* tiles;         // {leaf, first item, item count, window}
+  const int* num_tiles;
+  int* tile_next;            // dynamic tile counter (zeroed by plan_split_kernel)
+  const float* B;            // tensor-core layout (engine.cu build_tc_layout)
+  const uint32_t* ridx;
+  const float* rows;
+  const long long* row_base;
+  int d;
+  int W;                     // chunks per window
+};
+
+struct SplitSmem {
+  static constexpr int KT = kSplitKT;
+  static constexpr int kStageB = 128 * KT * 4;
+  static constexpr int kStageIdx = 128 * 4;
+  static constexpr int kStageRows = 128 * (KT - 1) * 4;
+  static constexpr int kA = 128 * KT * 4;
+  static constexpr int kOffIdx = kSplitStages * kStageB;
+  static constexpr int kOffRows = kOffIdx + kSplitStages * kStageIdx;
+  static constexpr int kOffA = kOffRows + kSplitStages * kStageRows;
+  static constexpr int kOffQi = kOffA + kSplitNA * kA;
+  static constexpr int kOffQ = kOffQi + kSplitNA * 128 * 4;
+  static constexpr int kOffRec = kOffQ + kQueue * 128 * 8;
+  static constexpr int kOffBar = kOffRec + kSplitNA * 16;
+  static constexpr int kNumBars = 2 * kSplitStages + 4 + 2 * kSplitNA;
+  static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
+  static_assert(kBytes <= tc_smem_per_cta(2), "split scan shared memory exceeds half an SM");
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+// element (r, k) of a 128 x KT K-major canonical (SWIZZLE_NONE) operand, in floats
+__host__ __device__ __forceinline__ int canon_off(int r, int k, int KT) {
+  return (r >> 3) * (KT * 8) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
+
+template <bool FMA>
+__global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const SplitScanArgs A) {
+  using S = SplitSmem;
+  constexpr int KT = kSplitKT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  float* sB = reinterpret_cast<float*>(smem);
+  uint32_t* sIdx = reinterpret_cast<uint32_t*>(smem + S::kOffIdx);
+  float* sRows = reinterpret_cast<float*>(smem + S::kOffRows);
+  float* sA = reinterpret_cast<float*>(smem + S::kOffA);
+  int* sQi = reinterpret_cast<int*>(smem + S::kOffQi);
+  uint64_t* s_queue = reinterpret_cast<uint64_t*>(smem + S::kOffQ);
+  int4* s_rec = reinterpret_cast<int4*>(smem + S::kOffRec);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* full = bars;                       // [stages] TMA -> MMA / survivors
+  uint64_t* empty = bars + kSplitStages;       // [stages] epilogue -> TMA
+  uint64_t* tfull = bars + 2 * kSplitStages;   // [2] MMA -> epilogue
+  uint64_t* tempty = tfull + 2;                // [2] epilogue -> MMA
+  uint64_t* afull = tempty + 2;                // [NA] producer (A rows, ids, tile record) -> MMA, epilogue
+  uint64_t* aempty = afull + kSplitNA;         // [NA] MMA (tile issued) + 4 epilogue warps -> producer
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + S::kNumBars);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kSplitStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTcEpiWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kTcEpiWarps);
+    }
+    for (int b = 0; b < kSplitNA; ++b) {
+      mbar_init(&afull[b], 32);
+      mbar_init(&aempty[b], 1 + kTcEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(s_tmem)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  const int tiles_end = *A.num_tiles;
+  const int d = A.d;
+
+  // chunk range of a tile's window
+  auto window = [&](const int4& rec, long long& r0, long long& r1, int& cb, int& ce) {
+    r0 = __ldg(A.row_base + rec.x);
+    r1 = __ldg(A.row_base + rec.x + 1);
+    const int nch = (int)((r1 - r0 + 127) / 128);
+    cb = rec.w * A.W;
+    ce = min(nch, cb + A.W);
+  };
+
+  if (warp == 4) {
+    // ===== producer: tile records, A-row gather (all lanes, cp.async, kAhead
+    // tiles in flight), TMA of the window's chunks (lane 0) =====
+    constexpr int kAhead = 2;
+    uint32_t g = 0;
+    // the next tile to issue: record and query ids, loaded one issue ahead
+    int4 rec_i;
+    int qi_i[4];
+    auto grab = [&]() {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(A.tile_next, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      rec_i = t < tiles_end ? __ldg(A.tiles + t) : make_int4(0, 0, -1, 0);
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int r = lane + 32 * rr;
+        qi_i[rr] = r < rec_i.z ? __ldg(A.items + rec_i.y + r) : -1;
+      }
+    };
+    bool done_issue = false;
+    uint32_t issued = 0;
+    auto issue = [&]() {
+      if (!done_issue) {
+        const uint32_t ab = issued % kSplitNA;
+        if (issued >= kSplitNA) mbar_wait(&aempty[ab], ((issued / kSplitNA) - 1) & 1u);
+        if (lane == 0) s_rec[ab] = rec_i;
+        float* abuf = sA + ab * (S::kA / 4);
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const int r = lane + 32 * rr;
+          const int qi = qi_i[rr];
+          sQi[ab * 128 + r] = qi;
+          if (qi >= 0) {
+            const float* src = A.arow + (long long)qi * KT;
+            float* dst = abuf + canon_off(r, 0, KT);
+#pragma unroll
+            for (int kc = 0; kc < KT / 4; ++kc) cp_async16(dst + kc * 32, src + 4 * kc);
+          }
+        }
+        ++issued;
+        if (rec_i.z < 0) done_issue = true;
+        else grab();
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");  // (empty once every tile is issued)
+    };
+    grab();
+    for (int a0 = 0; a0 < kAhead; ++a0) issue();
+    for (uint32_t j = 0;; ++j) {
+      issue();  // tile j + kAhead
+      asm volatile("cp.async.wait_group %0;" ::"n"(kAhead) : "memory");  // tile j's rows landed
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      const uint32_t ab = j % kSplitNA;
+      const int4 rec = s_rec[ab];
+      mbar_arrive(&afull[ab]);
+      if (rec.z < 0) break;
+      if (lane == 0) {
+        long long r0, r1;
+        int cb, ce;
+        window(rec, r0, r1, cb, ce);
+        for (int c = cb; c < ce; ++c, ++g) {
+          const int s = g % kSplitStages;
+          const uint32_t use = g / kSplitStages;
+          if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
+          const long long row = r0 + (long long)c * 128;
+          const int nr = (int)dmin_ll(128, r1 - row);
+          mbar_arrive_expect_tx(&full[s], nr * (KT * 4 + 4 + d * 4));
+          bulk_g2s(sB + s * (S::kStageB / 4), A.B + row * KT, nr * KT * 4, &full[s]);
+          bulk_g2s(sIdx + s * 128, A.ridx + row, nr * 4, &full[s]);
+          bulk_g2s(sRows + s * (S::kStageRows / 4), A.rows + row * d, nr * d * 4, &full[s]);
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 5) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      uint32_t g = 0;
+      const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
+      for (uint32_t j = 0;; ++j) {
+        const uint32_t ab = j % kSplitNA;
+        mbar_wait(&afull[ab], (j / kSplitNA) & 1u);
+        const int4 rec = s_rec[ab];
+        if (rec.z < 0) break;
+        tc_fence_after();
+        long long r0, r1;
+        int cb, ce;
+        window(rec, r0, r1, cb, ce);
+        for (int c = cb; c < ce; ++c, ++g) {
+          const int s = g % kSplitStages;
+          const uint32_t b = g & 1u, use = g >> 1;
+          mbar_wait(&full[s], (g / kSplitStages) & 1u);
+          if (use > 0) mbar_wait(&tempty[b], (use - 1) & 1u);
+          tc_fence_after();
+          const int nr = (int)dmin_ll(128, r1 - (r0 + (long long)c * 128));
+          const uint32_t idesc = idesc_tf32(nr);
+#pragma unroll
+          for (int h = 0; h < KT / 8; ++h) {
+            const uint64_t da = umma_desc(a_base + ab * S::kA + h * 256, 128, KT * 32);
+            const uint64_t db = umma_desc(b_base + s * S::kStageB + h * 256, 128, KT * 32);
+            const uint32_t acc = h > 0 ? 1u : 0u;
+            asm volatile(
+                "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(
+                    tmem + b * 128),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_addr(&tfull[b]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_addr(&aempty[ab]))
+                     : "memory");
+      }
+    }
+  } else {
+    // ===== epilogue: one thread per item (query) of the tile =====
+    uint64_t* qslot = s_queue + tid;
+    const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
+    uint32_t g = 0;
+    for (uint32_t j = 0;; ++j) {
+      const uint32_t ab = j % kSplitNA;
+      mbar_wait(&afull[ab], (j / kSplitNA) & 1u);
+      const int4 rec = s_rec[ab];
+      if (rec.z < 0) break;
+      const bool valid = tid < rec.z;
+      const int qi = valid ? sQi[ab * 128 + tid] : 0;
+      const float* arow_s = sA + ab * (S::kA / 4);
+      const float kth = valid ? arow_s[canon_off(tid, KT - 2, KT)] : -__int_as_float(0x7f800000);
+      const float qn = valid ? arow_s[canon_off(tid, KT - 1, KT)] : 0.0f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aempty[ab]);
+      long long r0, r1;
+      int cb, ce;
+      window(rec, r0, r1, cb, ce);
+
+      const float qnc = (1.0f - kTcMargin) * qn;
+      const bool force = valid && !(qn >= 1e-30f && qn <= 1e30f);
+      // kth - (1 - C) qn, rounded up by a hair (leafscan_tc.cuh); forced rows pass everything
+      float thr = -__int_as_float(0x7f800000);
+      if (valid) thr = force ? __int_as_float(0x7f800000) : __fsub_ru(kth, qnc) + 1e-6f * (fabsf(kth) + qnc);
+      int cn = 0;
+      bool have_q = false;
+      float qv[KT - 1];
+#pragma unroll
+      for (int jj = 0; jj < KT - 1; ++jj) qv[jj] = 0.0f;
+
+      // the query's candidates (reference distance <= kth) to its list
+      auto flush = [&]() {
+        if (cn > 0) {
+          const int base = atomicAdd(A.ccnt + qi, cn);
+          uint64_t* dst = A.cand + (long long)qi * kSplitCap;
+          for (int e = 0; e < cn; ++e)
+            if (base + e < kSplitCap) dst[base + e] = qslot[e * kNT];
+          if (base <= kSplitCap && base + cn > kSplitCap) A.ovf[atomicAdd(A.novf, 1)] = qi;
+          cn = 0;
+        }
+      };
+      auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
+        uint32_t mask = 0;
+        if (valid) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) mask |= (!(__uint_as_float(v[jj]) > thr) ? 1u : 0u) << jj;
+        }
+        if (mask && !have_q) {
+          const float* qp = A.q + (long long)qi * A.qstride;
+#pragma unroll
+          for (int jj = 0; jj < KT - 1; ++jj) qv[jj] = jj < d ? __ldg(qp + jj) : 0.0f;
+          have_q = true;
+        }
+        const uint32_t* ids = sIdx + s * 128 + gcol;
+        const float* prow = sRows + s * (S::kStageRows / 4) + gcol * d;
+        while (__any_sync(0xffffffffu, mask != 0)) {
+          if (mask) {
+            const int jj0 = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float* pp = prow + jj0 * d;
+            float pv[KT - 1];
+#pragma unroll
+            for (int jj = 0; jj < KT - 1; ++jj) pv[jj] = jj < d ? pp[jj] : 0.0f;
+            float acc = 0.0f;
+#pragma unroll
+            for (int jj = 0; jj < KT - 1; ++jj) {
+              if (jj < d) {
+                const float df = __fsub_rn(qv[jj], pv[jj]);
+                if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
+                else acc = __fadd_rn(acc, __fmul_rn(df, df));
+              }
+            }
+            if (acc <= kth && ids[jj0] != kIndexSentinel) qslot[(cn++) * kNT] = pack_key(acc, ids[jj0]);
+          }
+          if (__any_sync(0xffffffffu, cn == kQueue)) flush();
+        }
+      };
+
+      for (int c = cb; c < ce; ++c, ++g) {
+        const int s = g % kSplitStages;
+        const uint32_t b = g & 1u;
+        mbar_wait(&tfull[b], (g >> 1) & 1u);
+        tc_fence_after();
+        const long long row0 = r0 + (long long)c * 128;
+        const int ngrp = (int)dmin_ll(128, r1 - row0) / 32;
+        const uint32_t tbase = tmem + lane_base + b * 128;
+        uint32_t va[32], vb[32];
+        float gmn[4];
+        const float kInf = __int_as_float(0x7f800000);
+        tmem_ld32_async(tbase, va);
+        if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
+        tmem_wait(va);
+        tmem_touch(vb);
+        gmn[0] = min32(va);
+        gmn[1] = ngrp > 1 ? min32(vb) : kInf;
+        if (ngrp > 2) {
+          tmem_ld32_async(tbase + 64, va);
+          if (ngrp > 3) tmem_ld32_async(tbase + 96, vb);
+          tmem_wait(va);
+          tmem_touch(vb);
+          gmn[2] = min32(va);
+          gmn[3] = ngrp > 3 ? min32(vb) : kInf;
+        } else {
+          gmn[2] = kInf;
+          gmn[3] = kInf;
+        }
+        const float mchunk = fminf(fminf(gmn[0], gmn[1]), fminf(gmn[2], gmn[3]));
+        if (__any_sync(0xffffffffu, valid && !(mchunk > thr))) {
+          mbar_wait(&full[s], (g / kSplitStages) & 1u);
+#pragma unroll 1
+          for (int gi = 0; gi < ngrp; ++gi) {
+            float gv = gmn[0];
+#pragma unroll
+            for (int jj = 1; jj < 4; ++jj) gv = gi == jj ? gmn[jj] : gv;
+            if (!__any_sync(0xffffffffu, valid && !(gv > thr))) continue;
+            tmem_ld32_async(tbase + 32 * gi, va);
+            tmem_wait(va);
+            process(va, 32 * gi, s);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&tempty[b]);
+          mbar_arrive(&empty[s]);
+        }
+      }
+      if (__any_sync(0xffffffffu, cn > 0)) flush();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// advance: merge -> FindLeaf -> route (one thread per query of the list)
+// ---------------------------------------------------------------------------
+struct AdvanceArgs {
+  const int* list;           // queries of the round just scanned (length ctl->active)
+  RoundCtl* ctl;
+  int2* pos;                 // per list position: {next leaf or -1, slot in that leaf's bucket}
+  int* counts;               // per leaf: next round's bucket sizes
+  const float* q;
+  int D;
+  int k;
+  TopTreeView top;
+  uint64_t* keys;
+  float* kthv;
+  uint32_t* state;
+  int* next;
+  uint32_t* visits;
+  int* ccnt;                 // candidates of the round (all zero after the home round)
+  const uint64_t* cand;
+  const float* centroid;     // nl x kSplitKT
+  float* arow;               // m x kSplitKT
+  int* seq_log;
+  unsigned long long* seq_pos;
+  long long seq_cap;
+};
+
+constexpr int kAdvThreads = 256;
+__host__ __device__ inline int advance_smem_bytes(int h, int d) { return (start_tree_smem(h) + d * kAdvThreads) * 4; }
+
+template <int KB>
+__global__ void __launch_bounds__(kAdvThreads) advance_kernel(const AdvanceArgs a) {
+  extern __shared__ float s_adv[];
+  const int ntree = start_tree_smem(a.top.h);
+  float* s_split = s_adv;
+  float* myq = s_adv + ntree + threadIdx.x;  // [j][thread]: the thread's query coordinates
+  for (int i = threadIdx.x; i < ntree; i += blockDim.x) s_split[i] = __ldg(a.top.split + i);
+  __syncthreads();
+  const int n = a.ctl->active;
+  const int d = a.top.d;
+  const int k = a.k;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int qi = __ldg(a.list + i);
+    // 1. merge this visit's candidates into the top-k row
+    const int nc = a.ccnt[qi];
+    float kth;
+    if (nc > 0) a.ccnt[qi] = 0;
+    if (nc > 0 && nc <= kSplitCap) {
+      // register top-k (descending, sentinel-padded: leafscan.cuh merge_queue)
+      uint64_t* row = a.keys + (long long)qi * k;
+      const uint64_t* cp = a.cand + (long long)qi * kSplitCap;
+      uint64_t arr[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) arr[j] = j < k ? row[k - 1 - j] : 0ull;
+      for (int e = 0; e < nc; ++e) {
+        const uint64_t c = cp[e];
+        if (c < arr[0]) topk_insert<KB>(arr, c);
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < k) row[k - 1 - j] = arr[j];
+      kth = key_dist(arr[0]);
+      a.kthv[qi] = kth;
+    } else {
+      kth = a.kthv[qi];  // unchanged, or rescanned (nc > cap)
+    }
+    // 2. FindLeaf with the new k-th distance
+    float qv[32];
+    const float* qp = a.q + (long long)qi * a.D;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      qv[j] = j < d ? __ldg(qp + j) : 0.0f;
+      if (j < d) myq[j * kAdvThreads] = qv[j];
+    }
+    auto qget = [myq](int j) { return myq[j * kAdvThreads]; };
+    const uint32_t st = a.state[qi];
+    uint32_t lf = st & 0xFFFFu, pend = st >> 16;
+    int nxt;
+    if (ntree)
+      nxt = find_next_leaf_with(a.top.h, d, [s_split](uint32_t node) { return s_split[node]; }, qget, kth, lf, pend);
+    else
+      nxt = find_next_leaf(a.top, qget, kth, lf, pend);
+    a.state[qi] = (pend << 16) | lf;
+    a.next[qi] = nxt;
+    int rk = 0;
+    if (nxt >= 0) {
+      const uint32_t vis = a.visits[qi] + 1;
+      a.visits[qi] = vis;
+      if (a.seq_log) {
+        const unsigned long long p = atomicAdd(a.seq_pos, 1ull);
+        if ((long long)p < a.seq_cap) {
+          a.seq_log[3 * p] = qi; a.seq_log[3 * p + 1] = (int)vis; a.seq_log[3 * p + 2] = nxt;
+        }
+      }
+      rk = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
+      // A row of the next visit: tf32(q - c) | 1 | 0.. | kth | |q - c|^2
+      const float* cen = a.centroid + (long long)nxt * kSplitKT;
+      float r[kSplitKT];
+      float qn = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kSplitKT; ++j) {
+        float v = 0.0f;
+        if (j < d) {
+          const float qc = __fsub_rn(qv[j], __ldg(cen + j));
+          qn = __fmaf_rn(qc, qc, qn);
+          v = __uint_as_float(tf32_rna(qc));
+        } else if (j == d) {
+          v = 1.0f;
+        }
+        r[j] = v;
+      }
+      r[kSplitKT - 2] = kth;
+      r[kSplitKT - 1] = qn;
+      float4* dst = reinterpret_cast<float4*>(a.arow + (long long)qi * kSplitKT);
+#pragma unroll
+      for (int j = 0; j < kSplitKT / 4; ++j) dst[j] = make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+    }
+    a.pos[i] = make_int2(nxt, rk);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// route: windows per query, one route tile = (leaf, <= kRouteQ queries of its bucket)
+// ---------------------------------------------------------------------------
+constexpr int kRouteQ = 1024;
+constexpr int kRouteThreads = 256;
+constexpr int kMaxWin = 64;
+
+struct RouteArgs {
+  const int* work;           // this round's queries, bucketed by leaf
+  const int4* rtiles;        // route tiles {leaf, first, count, -}
+  const RoundCtl* ctl;       // num_tiles = route tiles
+  const float* kthv;
+  const float* q;
+  int D;
+  int d;
+  int NW;
+  const int* win_base;
+  const float* win_box;
+  const int* leaf_size;
+  unsigned long long* qmask; // per work-list position
+  int* counts;               // per key
+  int* cbase;                // per route tile x NW: the tile's first slot in each key
+  const int* key_off;        // (place) per key
+  const int* stoff;          // (place) split tiles per key
+  int nkeys;
+  int* items;
+  int4* stiles;
+  int stiles_cap;
+  unsigned long long* pairs;
+};
+
+// pass 1: masks, per-key counts, each route tile's base slot per window; pairs
+__global__ void __launch_bounds__(kRouteThreads) route_kernel(const RouteArgs a) {
+  __shared__ float s_box[kMaxWin * 2 * 32];
+  __shared__ int s_cnt[kMaxWin];
+  const int nt = a.ctl->num_tiles;
+  const int d = a.d;
+  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+    const int4 rt = __ldg(a.rtiles + t);
+    const int leaf = rt.x;
+    const int w0 = __ldg(a.win_base + leaf), nw = __ldg(a.win_base + leaf + 1) - w0;
+    __syncthreads();  // previous tile's shared state consumed
+    for (int e = threadIdx.x; e < nw * 2 * d; e += blockDim.x) s_box[e] = __ldg(a.win_box + (long long)w0 * 2 * d + e);
+    for (int e = threadIdx.x; e < kMaxWin; e += blockDim.x) s_cnt[e] = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < rt.z; r += blockDim.x) {
+      const int p = rt.y + r;
+      const int qi = __ldg(a.work + p);
+      const float kth = __ldg(a.kthv + qi);
+      float qv[32];
+      const float* qp = a.q + (long long)qi * a.D;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) qv[j] = j < d ? __ldg(qp + j) : 0.0f;
+      unsigned long long mask = 0;
+      for (int w = 0; w < nw; ++w) {
+        // box lower bound in f32, relaxed by 1e-5: never above the reference distance
+        const float* bx = s_box + w * 2 * d;
+        float lb = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < d) {
+            const float e = fmaxf(fmaxf(bx[j] - qv[j], qv[j] - bx[d + j]), 0.0f);
+            lb = __fmaf_rn(e, e, lb);
+          }
+        }
+        if (!(lb * 0.99999f > kth)) mask |= 1ull << w;
+      }
+      a.qmask[p] = mask;
+      // per-window counts: one shared atomic per warp and window
+      const unsigned act = __activemask();
+      const int leader = __ffs(act) - 1;
+      for (int w = 0; w < nw; ++w) {
+        const unsigned b = __ballot_sync(act, (mask >> w) & 1ull);
+        if ((int)(threadIdx.x & 31) == leader && b) atomicAdd(&s_cnt[w], __popc(b));
+      }
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) {
+      const int c = s_cnt[w];
+      a.cbase[(long long)t * a.NW + w] = c ? atomicAdd(a.counts + leaf * a.NW + w, c) : 0;
+    }
+    if (threadIdx.x == 0 && a.pairs) atomicAdd(a.pairs, (unsigned long long)__ldg(a.leaf_size + leaf) * rt.z);
+  }
+}
+
+// pass 2 (after plan_split): items into their key's slice; split tile records
+__global__ void __launch_bounds__(kRouteThreads) place_kernel(const RouteArgs a) {
+  __shared__ int s_cnt[kMaxWin];
+  __shared__ int s_base[kMaxWin];
+  const int nt = a.ctl->num_tiles;
+  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+    const int4 rt = __ldg(a.rtiles + t);
+    const int leaf = rt.x;
+    const int nw = __ldg(a.win_base + leaf + 1) - __ldg(a.win_base + leaf);
+    __syncthreads();
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) {
+      s_cnt[w] = 0;
+      s_base[w] = __ldg(a.key_off + leaf * a.NW + w) + __ldg(a.cbase + (long long)t * a.NW + w);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < rt.z; r += blockDim.x) {
+      const int p = rt.y + r;
+      const int qi = __ldg(a.work + p);
+      unsigned long long m = __ldg(a.qmask + p);
+      while (m) {
+        const int w = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        a.items[s_base[w] + atomicAdd(&s_cnt[w], 1)] = qi;
+      }
+    }
+  }
+  // (leaf, window) tile records {leaf, first item, count, window}
+  const int ns = min(a.ctl->stiles, a.stiles_cap);
+  const int stride = gridDim.x * blockDim.x;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ns; t += stride) {
+    int lo = 0, hi = a.nkeys;  // last key with stoff[key] <= t (the key holding tile t)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(a.stoff + mid) <= t) lo = mid; else hi = mid;
+    }
+    const int p = __ldg(a.key_off + lo) + (t - __ldg(a.stoff + lo)) * kNT;
+    a.stiles[t] = make_int4(lo / a.NW, p, min(kNT, __ldg(a.key_off + lo + 1) - p), lo % a.NW);
+  }
+}
+
+// counts -> key offsets and 128-item tiles per key (one CTA)
+__global__ void __launch_bounds__(kPlanThreads) plan_split_kernel(int* __restrict__ counts, int* __restrict__ key_off,
+                                                                  int nkeys, int* __restrict__ toff, RoundCtl* ctl,
+                                                                  int tile_q) {
+  const int per = (nkeys + kPlanThreads - 1) / kPlanThreads;
+  const int lo = min(nkeys, (int)threadIdx.x * per), hi = min(nkeys, lo + per);
+  long long sc = 0, st = 0;
+  for (int e = lo; e < hi; ++e) {
+    const int c = counts[e];
+    sc += c;
+    st += (c + tile_q - 1) / tile_q;
+  }
+  long long ec = sc, et = st, tot_c, tot_t;
+  block_scan2(ec, et, tot_c, tot_t);
+  for (int e = lo; e < hi; ++e) {
+    const int c = counts[e];
+    key_off[e] = (int)ec;
+    toff[e] = (int)et;
+    ec += c;
+    et += (c + tile_q - 1) / tile_q;
+    counts[e] = 0;
+  }
+  if (threadIdx.x == 0) {
+    key_off[nkeys] = (int)tot_c;
+    toff[nkeys] = (int)tot_t;
+    ctl->novf = 0;
+    ctl->stiles = (int)tot_t;
+    ctl->tile_next = 0;
+    ctl->items = (int)tot_c;
+  }
+}
+
+// A query whose candidates overflowed its list: one warp rescans the whole
+// leaf of this round's visit (reference arithmetic over the quad layout, as
+// finish_kernel) and merges every point below the k-th key.
+template <bool FMA>
+__global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
+    const int* __restrict__ ovf, const RoundCtl* ctl, const float* __restrict__ q, int D, int k, int d,
+    uint64_t* __restrict__ keys, float* __restrict__ kthv, const int* __restrict__ next,
+    const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base) {
+  __shared__ uint64_t s_row[kFinishWarps][64];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  uint64_t* row = s_row[wl];
+  const int n = ctl->novf;
+  for (int i = blockIdx.x * kFinishWarps + wl; i < n; i += gridDim.x * kFinishWarps) {
+    const int qi = __ldg(ovf + i);
+    const int leaf = next[qi];
+    uint64_t* kp = keys + (long long)qi * k;
+    for (int j = lane; j < k; j += 32) row[j] = kp[j];
+    __syncwarp();
+    float qv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) qv[j] = j < d ? __ldg(q + (long long)qi * D + j) : 0.0f;
+    const long long g0 = __ldg(quad_base + leaf), g1 = __ldg(quad_base + leaf + 1);
+    uint64_t kkey = row[k - 1];
+    for (long long gb = g0; gb < g1; gb += 32) {
+      const long long g = gb + lane;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      const bool has = g < g1;
+      if (has) {
+        const float4* pq = reinterpret_cast<const float4*>(pts + g * 4 * D);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < d) {
+            const float4 p = __ldg(pq + j);
+            const float e[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float df = __fsub_rn(qv[j], e[t]);
+              if constexpr (FMA) acc[t] = __fmaf_rn(df, df, acc[t]);
+              else acc[t] = __fadd_rn(acc[t], __fmul_rn(df, df));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint64_t key = has ? pack_key(acc[t], __ldg(pidx + g * 4 + t)) : ~0ull;
+        unsigned bal = __ballot_sync(0xffffffffu, key < kkey);
+        while (bal) {
+          const int src = __ffs(bal) - 1;
+          bal &= bal - 1;
+          const uint64_t c = __shfl_sync(0xffffffffu, key, src);
+          if (lane == 0 && c < row[k - 1]) {
+            int j = k - 1;
+            while (j > 0 && row[j - 1] > c) {
+              row[j] = row[j - 1];
+              --j;
+            }
+            row[j] = c;
+          }
+          __syncwarp();
+          kkey = row[k - 1];
+        }
+      }
+    }
+    for (int j = lane; j < k; j += 32) kp[j] = row[j];
+    if (lane == 0) kthv[qi] = key_dist(row[k - 1]);
+    __syncwarp();
+  }
+}
+
+}  // namespace bkt

@@ -1,0 +1,12 @@
+#!/bin/bash
+# split-round variants: W (window chunks) x split_from
+out=gpurun_out/${1:-r2g}; mkdir -p $out
+python -m paper_1512_02831_b200.build > /dev/null 2>&1
+timeout 600 python -m pytest tests/test_gpu_scale_parity.py -m gpu -x -q -k "cfg2 or cfg5_shape_deep_trees and hbm" > $out/pytest.txt 2>&1; echo "rc=$?" >> $out/pytest.txt
+for v in "BKT_SPLIT=0" "BKT_SPLIT_W=2" "BKT_SPLIT_W=1" "BKT_SPLIT_W=4" "BKT_SPLIT_W=2 BKT_SPLIT_FROM=2" "BKT_SPLIT_W=2 BKT_SPLIT_FROM=3" "BKT_SPLIT_W=2 BKT_SPLIT_FROM=5" "BKT_SPLIT_W=1 BKT_SPLIT_FROM=3"; do
+  tag=$(echo $v | tr ' =' '_-')
+  bash tools/quickbench.sh $tag $v >> $out/ab.txt
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --check-rows 0 > $out/b.log 2>&1
+python tools/launch_summary.py $out/launches.csv > $out/launches_summary.txt
+echo done

@@ -174,8 +174,9 @@ struct bkt_ctx {
   // split-round per-query buffers (capacity split_cap queries)
   long long split_cap = 0;
   float* arow = nullptr;                 // m x kSplitKT
-  int* ccnt = nullptr;                   // m
-  uint64_t* cand = nullptr;              // m x kSplitCap
+  uint8_t* ccnt = nullptr;               // m x split_NW
+  uint64_t* cand = nullptr;              // m x split_NW x capw
+  int* ovflag = nullptr;                 // m
   int* ovf = nullptr;                    // m
   unsigned long long* qmask = nullptr;   // m
   int* cbase = nullptr;                  // route tiles x split_NW
@@ -289,7 +290,7 @@ void free_work(bkt_ctx* c) {
   c->cap_m = 0; c->cap_k = 0;
   dfree(c->q_alt); dfree(c->q_raw_alt); dfree(c->keys_alt);
   c->cap_alt = 0; c->cap_alt_k = 0;
-  dfree(c->arow); dfree(c->ccnt); dfree(c->cand); dfree(c->ovf); dfree(c->qmask); dfree(c->cbase);
+  dfree(c->arow); dfree(c->ccnt); dfree(c->cand); dfree(c->ovflag); dfree(c->ovf); dfree(c->qmask); dfree(c->cbase);
   dfree(c->items); dfree(c->stoff); dfree(c->stiles);
   c->split_cap = 0; c->stiles_cap = 0;
   dfree(c->perm); dfree(c->q_perm); dfree(c->keys_tmp); dfree(c->visits_tmp);
@@ -311,19 +312,22 @@ int ensure_perm(bkt_ctx* ctx, long long m, int k) {
 
 // per-query bytes of the split-round buffers
 long long split_bytes_per_query(const bkt_ctx* c) {
-  return 4ll * kSplitKT + 4 + 8ll * kSplitCap + 4 + 8 + 4ll * c->split_NW + 16ll * c->split_NW / kNT + 16;
+  return 4ll * kSplitKT + (1ll + 8ll * split_capw(c->split_NW)) * c->split_NW + 4 + 4 + 8 + 4ll * c->split_NW +
+         16ll * c->split_NW / kNT + 16;
 }
 
 int ensure_split(bkt_ctx* ctx, long long m) {
   if (ctx->split_cap >= m) return BKT_OK;
-  dfree(ctx->arow); dfree(ctx->ccnt); dfree(ctx->cand); dfree(ctx->ovf); dfree(ctx->qmask); dfree(ctx->cbase);
+  dfree(ctx->arow); dfree(ctx->ccnt); dfree(ctx->cand); dfree(ctx->ovflag); dfree(ctx->ovf); dfree(ctx->qmask); dfree(ctx->cbase);
   dfree(ctx->items); dfree(ctx->stoff); dfree(ctx->stiles);
   const long long M = std::max<long long>(m, 1);
   const long long NW = ctx->split_NW;
   CU(cudaMalloc(&ctx->arow, sizeof(float) * M * kSplitKT));
-  CU(cudaMalloc(&ctx->ccnt, sizeof(int) * M));
-  CU(cudaMemset(ctx->ccnt, 0, sizeof(int) * M));
-  CU(cudaMalloc(&ctx->cand, sizeof(uint64_t) * M * kSplitCap));
+  CU(cudaMalloc(&ctx->ccnt, M * NW));
+  CU(cudaMemset(ctx->ccnt, 0, M * NW));
+  CU(cudaMalloc(&ctx->cand, sizeof(uint64_t) * M * NW * split_capw((int)NW)));
+  CU(cudaMalloc(&ctx->ovflag, sizeof(int) * M));
+  CU(cudaMemset(ctx->ovflag, 0, sizeof(int) * M));
   CU(cudaMalloc(&ctx->ovf, sizeof(int) * M));
   CU(cudaMalloc(&ctx->qmask, sizeof(unsigned long long) * M));
   CU(cudaMalloc(&ctx->cbase, sizeof(int) * (M / kRouteQ + ctx->nl + 1) * NW));
@@ -855,9 +859,9 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
         CU(cudaMemcpy(ctx->tc_cbase, cb.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice));
         CU(cudaMalloc(&ctx->tc_box, sizeof(float) * box.size()));
         CU(cudaMemcpy(ctx->tc_box, box.data(), sizeof(float) * box.size(), cudaMemcpyHostToDevice));
-        if (KT == kSplitKT && d <= kSplitKT - 3) {
+        if (KT == kSplitKT && d <= kSplitMaxD) {
           // split rounds: windows of W consecutive chunks (<= 64 per leaf), box = union of its chunks
-          int W = 2;
+          int W = 4;  // config 2: W = 1 / 2 / 4 -> 22.1 / 27.7 / 29.9 M q/s (before renumbering)
           if (const char* e = std::getenv("BKT_SPLIT_W")) W = std::max(1, std::atoi(e));
           int maxch = 1;
           for (int l = 0; l < nl; ++l) maxch = std::max(maxch, cb[l + 1] - cb[l]);
@@ -1003,6 +1007,7 @@ struct SearchRun {
   bool finish_cta = false;   // finisher with one CTA per query (else one warp per query)
   bool split = false;        // later rounds as (leaf, window) items (split_scan.cuh)
   bool renumber = false;     // search in home-bucket order (gather_rows_kernel)
+  bool verbose = false;      // BKT_VERBOSE: split-round totals on stderr
   int split_from = 1;        // first split round (earlier rounds: leaf-level tiles)
   bool drain_fired = false;
   std::function<void()> drain_start;
@@ -1271,6 +1276,9 @@ int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
   a.visits = ctx->visits;
   a.ccnt = ctx->ccnt;
   a.cand = ctx->cand;
+  a.ovflag = ctx->ovflag;
+  a.NW = ctx->split_NW;
+  a.capw = split_capw(ctx->split_NW);
   a.centroid = ctx->tc_centroid;
   a.arow = ctx->arow;
   a.seq_log = R.seq ? ctx->seq_dev : nullptr;
@@ -1335,6 +1343,9 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
     sa.arow = ctx->arow;
     sa.ccnt = ctx->ccnt;
     sa.cand = ctx->cand;
+    sa.ovflag = ctx->ovflag;
+    sa.NW = ctx->split_NW;
+    sa.capw = split_capw(ctx->split_NW);
     sa.ovf = ctx->ovf;
     sa.novf = &ctx->ctl->novf;
     sa.items = ctx->items;
@@ -1347,13 +1358,40 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
     sa.row_base = ctx->tc_row_base;
     sa.d = ctx->d;
     sa.W = ctx->split_W;
+    sa.stats = R.verbose ? &ctx->ctl->sc_tiles : nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (R.timing) {
       e0 = get_event(ctx, R.ev_next++);
       e1 = get_event(ctx, R.ev_next++);
       CU(cudaEventRecord(e0, ctx->stream));
     }
+    static long long* sdbg = nullptr;
+    const char* sdbg_env = std::getenv("BKT_SPLIT_DEBUG");
+    const bool sdbg_now = sdbg_env && R.leafscan_launches == std::atoi(sdbg_env);
+    constexpr int kDbgCap = 4096;
+    if (sdbg_now) {
+      if (!sdbg) CU(cudaMalloc(&sdbg, sizeof(long long) * 16 * kDbgCap));
+      CU(cudaMemsetAsync(sdbg, 0, sizeof(long long) * 16 * kDbgCap, ctx->stream));
+      sa.dbg = sdbg;
+      sa.dbg_cap = kDbgCap;
+    }
     CU(launch_splitscan(R.fma, R.grid_scan, ctx->stream, sa));
+    if (sdbg_now) {
+      // per tile: published (producer), afull wait start/ready (epilogue), afull ready (MMA);
+      // per chunk: MMA issued, epilogue tfull wait start/ready, released, TMA issued, full ready (MMA)
+      std::vector<long long> h(16 * kDbgCap);
+      CU(cudaMemcpyAsync(h.data(), sdbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      const long long b0 = h[5];
+      for (int j = 0; j < kDbgCap && h[8 * j + 5]; ++j)
+        std::fprintf(stderr, "stile %d pub %lld ewait %lld eready %lld mready %lld\n", j, h[8 * j] - b0,
+                     h[8 * j + 5] - b0, h[8 * j + 6] ? h[8 * j + 6] - b0 : -1, h[8 * j + 7] ? h[8 * j + 7] - b0 : -1);
+      const long long* hc = h.data() + 8 * kDbgCap;
+      for (int g = 0; g < kDbgCap && hc[8 * g + 4]; ++g)
+        std::fprintf(stderr, "schunk %d tma %lld full %lld mma %lld ewait %lld eready %lld edone %lld\n", g,
+                     hc[8 * g + 5] - b0, hc[8 * g + 6] - b0, hc[8 * g + 1] - b0, hc[8 * g + 2] - b0,
+                     hc[8 * g + 3] - b0, hc[8 * g + 4] - b0);
+    }
     if (R.timing) {
       CU(cudaEventRecord(e1, ctx->stream));
       R.scan_events.emplace_back(e0, e1);
@@ -1438,7 +1476,10 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
   init.active = (int)m;
   CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
-  if (R.split) CU(cudaMemsetAsync(ctx->ccnt, 0, sizeof(int) * m, ctx->stream));
+  if (R.split) {
+    CU(cudaMemsetAsync(ctx->ccnt, 0, (size_t)m * ctx->split_NW, ctx->stream));
+    CU(cudaMemsetAsync(ctx->ovflag, 0, sizeof(int) * m, ctx->stream));
+  }
   start_kernel<<<R.grid_small, kStartQ, start_smem_bytes(ctx->h, ctx->D), ctx->stream>>>(
       ctx->q, ctx->D, m, R.k, top, ctx->keys, ctx->state, ctx->next,
                                                        ctx->visits, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
@@ -1555,6 +1596,11 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
   CU(cudaMemcpy(&fin, ctx->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost));
   R.rounds += fin.rounds;
   R.scans += fin.scans;
+  if (R.verbose && R.split)
+    std::fprintf(stderr, "split rounds: W %d NW %d tiles %llu chunks %llu items %llu candidates %llu writers %llu "
+                 "survivors %llu trips %llu (m %lld)\n",
+                 ctx->split_W, ctx->split_NW, fin.sc_tiles, fin.sc_chunks, fin.sc_items, fin.sc_cands, fin.sc_flushes,
+                 fin.sc_surv, fin.sc_trips, R.m);
   return BKT_OK;
 }
 
@@ -1603,6 +1649,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
   R.renumber = ctx->residency == 0 && !std::getenv("BKT_EARLY_DRAIN");
+  R.verbose = std::getenv("BKT_VERBOSE") != nullptr;
   if (const char* e = std::getenv("BKT_RENUMBER")) R.renumber = R.renumber && std::atoi(e) != 0;
   int rc = BKT_OK;
   if (R.tc) {

@@ -36,6 +36,8 @@ struct RoundCtl {
   int stiles;       // (leaf, window) tiles this round
   int novf;         // queries whose candidate list overflowed this round
   int items;        // (query, window) work items this round
+  // split-round totals of the batch (diagnostics, BKT_VERBOSE)
+  unsigned long long sc_tiles, sc_chunks, sc_cands, sc_flushes, sc_items, sc_surv, sc_trips;
 };
 
 // Early result drain: remember the queries of the round just scanned (every

@@ -26,8 +26,8 @@
 //   scan     : splitscan_tc_kernel -- the tensor-core filter of leafscan_tc.cuh
 //              on each tile's window against each query's kth; survivors
 //              re-evaluated in the reference arithmetic; points with
-//              D_ref <= kth are flushed to the query's candidate list.
-//   rescan   : a query whose candidates exceed kSplitCap in one round gets its
+//              D_ref <= kth go to the (query, window)'s slice of the candidate list.
+//   rescan   : a query whose candidates exceed a window's slice in one round gets its
 //              whole leaf rescanned by one warp (exact), instead of merging.
 //   advance  : per query -- merge its candidates into the top-k row (the
 //              reference's update_rows, core.py:251-262; any order: the result
@@ -51,19 +51,23 @@
 namespace bkt {
 
 constexpr int kSplitKT = 16;     // A row: d coordinates, 1.0 at column d, zeros, kth at KT-2, |q'|^2 at KT-1 (d <= 13)
-constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers up to 3 tiles ahead
-constexpr int kSplitStages = 4;  // TMA ring stages (128-row chunks)
-constexpr int kSplitCap = 32;    // candidates per query and round; beyond it the leaf is rescanned
+constexpr int kSplitMaxD = kSplitKT - 3;
+constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhead = 2 tiles ahead
+constexpr int kSplitStages = 5;  // TMA ring stages (128-row chunks)
 constexpr int kSplitThreads = 192;
+// candidates per (query, window) and round before the leaf is rescanned instead
+__host__ __device__ inline int split_capw(int NW) { return NW <= 8 ? 16 : (NW >= 32 ? 4 : 128 / NW); }
 
 struct SplitScanArgs {
   const float* q;            // m x qstride original coordinates (survivor re-evaluation)
   int qstride;
   const float* arow;         // m x kSplitKT A rows (advance_kernel)
-  int* ccnt;                 // m: candidates flushed this round
-  uint64_t* cand;            // m x kSplitCap
-  int* ovf;                  // queries whose candidates overflowed (rescan list)
+  uint8_t* ccnt;             // m x NW: candidates of each (query, window) this round
+  uint64_t* cand;            // m x NW x capw
+  int* ovflag;               // m: the query's candidates overflowed (rescan)
+  int* ovf;                  // queries to rescan
   int* novf;
+  int NW, capw;
   const int* items;          // this round's items (query ids), grouped by key
   const int4* tiles;         // {leaf, first item, item count, window}
   const int* num_tiles;
@@ -74,23 +78,32 @@ struct SplitScanArgs {
   const long long* row_base;
   int d;
   int W;                     // chunks per window
+  unsigned long long* stats; // diagnostics: tiles, chunks, candidates, writers, items (or null)
+  long long* dbg;            // BKT_SPLIT_DEBUG: per-event clock64 stamps of CTA 0 (or null)
+  int dbg_cap;
+};
+
+struct SplitWin {
+  long long r0, r1;  // padded rows of the leaf
+  int cb, ce;        // the window's chunks [cb, ce)
 };
 
 struct SplitSmem {
   static constexpr int KT = kSplitKT;
   static constexpr int kStageB = 128 * KT * 4;
   static constexpr int kStageIdx = 128 * 4;
-  static constexpr int kStageRows = 128 * (KT - 1) * 4;
+  static constexpr int kStageRows = 128 * kSplitMaxD * 4;
   static constexpr int kA = 128 * KT * 4;
   static constexpr int kOffIdx = kSplitStages * kStageB;
   static constexpr int kOffRows = kOffIdx + kSplitStages * kStageIdx;
   static constexpr int kOffA = kOffRows + kSplitStages * kStageRows;
   static constexpr int kOffQi = kOffA + kSplitNA * kA;
-  static constexpr int kOffQ = kOffQi + kSplitNA * 128 * 4;
-  static constexpr int kOffRec = kOffQ + kQueue * 128 * 8;
-  static constexpr int kOffBar = kOffRec + kSplitNA * 16;
+  static constexpr int kOffRec = kOffQi + kSplitNA * 128 * 4;
+  static constexpr int kOffWin = kOffRec + kSplitNA * 16;
+  static constexpr int kOffBar = kOffWin + kSplitNA * 32;
   static constexpr int kNumBars = 2 * kSplitStages + 4 + 2 * kSplitNA;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
+  static_assert(sizeof(SplitWin) <= 32, "window record");
   static_assert(kBytes <= tc_smem_per_cta(2), "split scan shared memory exceeds half an SM");
 };
 
@@ -114,8 +127,8 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
   float* sRows = reinterpret_cast<float*>(smem + S::kOffRows);
   float* sA = reinterpret_cast<float*>(smem + S::kOffA);
   int* sQi = reinterpret_cast<int*>(smem + S::kOffQi);
-  uint64_t* s_queue = reinterpret_cast<uint64_t*>(smem + S::kOffQ);
   int4* s_rec = reinterpret_cast<int4*>(smem + S::kOffRec);
+  SplitWin* s_win = reinterpret_cast<SplitWin*>(smem + S::kOffWin);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* full = bars;                       // [stages] TMA -> MMA / survivors
   uint64_t* empty = bars + kSplitStages;       // [stages] epilogue -> TMA
@@ -154,33 +167,38 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
   const int tiles_end = *A.num_tiles;
   const int d = A.d;
 
-  // chunk range of a tile's window
-  auto window = [&](const int4& rec, long long& r0, long long& r1, int& cb, int& ce) {
-    r0 = __ldg(A.row_base + rec.x);
-    r1 = __ldg(A.row_base + rec.x + 1);
-    const int nch = (int)((r1 - r0 + 127) / 128);
-    cb = rec.w * A.W;
-    ce = min(nch, cb + A.W);
-  };
-
   if (warp == 4) {
     // ===== producer: tile records, A-row gather (all lanes, cp.async, kAhead
-    // tiles in flight), TMA of the window's chunks (lane 0) =====
+    // tiles in flight), TMA of the window's chunks (lane 0).  The dependent
+    // loads of a tile (its index from the counter, its record, its query ids
+    // and leaf rows) are spread over three consecutive issues, so each one's
+    // latency overlaps a tile of work. =====
     constexpr int kAhead = 2;
     uint32_t g = 0;
-    // the next tile to issue: record and query ids, loaded one issue ahead
-    int4 rec_i;
-    int qi_i[4];
+    int t_a = 0;                     // stage a: tile index grabbed
+    int4 rec_b;                      // stage b: its record
+    int4 rec_c;                      // stage c: record, query ids, window of the tile to issue next
+    int qi_c[4];
+    long long r0_c = 0, r1_c = 0;
     auto grab = [&]() {
       int t = 0;
       if (lane == 0) t = atomicAdd(A.tile_next, 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      rec_i = t < tiles_end ? __ldg(A.tiles + t) : make_int4(0, 0, -1, 0);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    auto load_rec = [&](int t) { return t < tiles_end ? __ldg(A.tiles + t) : make_int4(0, 0, -1, 0); };
+    auto shift = [&]() {
+      rec_c = rec_b;
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
         const int r = lane + 32 * rr;
-        qi_i[rr] = r < rec_i.z ? __ldg(A.items + rec_i.y + r) : -1;
+        qi_c[rr] = r < rec_c.z ? __ldg(A.items + rec_c.y + r) : -1;
       }
+      if (rec_c.z >= 0) {
+        r0_c = __ldg(A.row_base + rec_c.x);
+        r1_c = __ldg(A.row_base + rec_c.x + 1);
+      }
+      rec_b = load_rec(t_a);
+      t_a = grab();
     };
     bool done_issue = false;
     uint32_t issued = 0;
@@ -188,12 +206,21 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       if (!done_issue) {
         const uint32_t ab = issued % kSplitNA;
         if (issued >= kSplitNA) mbar_wait(&aempty[ab], ((issued / kSplitNA) - 1) & 1u);
-        if (lane == 0) s_rec[ab] = rec_i;
+        if (lane == 0) {
+          s_rec[ab] = rec_c;
+          SplitWin w;
+          w.r0 = r0_c;
+          w.r1 = r1_c;
+          const int nch = (int)((r1_c - r0_c + 127) / 128);
+          w.cb = rec_c.w * A.W;
+          w.ce = min(nch, w.cb + A.W);
+          s_win[ab] = w;
+        }
         float* abuf = sA + ab * (S::kA / 4);
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           const int r = lane + 32 * rr;
-          const int qi = qi_i[rr];
+          const int qi = qi_c[rr];
           sQi[ab * 128 + r] = qi;
           if (qi >= 0) {
             const float* src = A.arow + (long long)qi * KT;
@@ -203,12 +230,15 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
           }
         }
         ++issued;
-        if (rec_i.z < 0) done_issue = true;
-        else grab();
+        if (rec_c.z < 0) done_issue = true;
+        else shift();
       }
       asm volatile("cp.async.commit_group;" ::: "memory");  // (empty once every tile is issued)
     };
-    grab();
+    t_a = grab();
+    rec_b = load_rec(t_a);
+    t_a = grab();
+    shift();
     for (int a0 = 0; a0 < kAhead; ++a0) issue();
     for (uint32_t j = 0;; ++j) {
       issue();  // tile j + kAhead
@@ -217,18 +247,23 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       __syncwarp();
       const uint32_t ab = j % kSplitNA;
       const int4 rec = s_rec[ab];
+      const SplitWin win = s_win[ab];
       mbar_arrive(&afull[ab]);
+      if (A.dbg && blockIdx.x == 0 && lane == 0 && (int)j < A.dbg_cap) A.dbg[8 * j + 0] = clock64();
       if (rec.z < 0) break;
       if (lane == 0) {
-        long long r0, r1;
-        int cb, ce;
-        window(rec, r0, r1, cb, ce);
-        for (int c = cb; c < ce; ++c, ++g) {
+        if (A.stats) {
+          atomicAdd(A.stats + 0, 1ull);
+          atomicAdd(A.stats + 1, (unsigned long long)(win.ce - win.cb));
+          atomicAdd(A.stats + 4, (unsigned long long)rec.z);
+        }
+        for (int c = win.cb; c < win.ce; ++c, ++g) {
           const int s = g % kSplitStages;
           const uint32_t use = g / kSplitStages;
           if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
-          const long long row = r0 + (long long)c * 128;
-          const int nr = (int)dmin_ll(128, r1 - row);
+          const long long row = win.r0 + (long long)c * 128;
+          const int nr = (int)dmin_ll(128, win.r1 - row);
+          if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * A.dbg_cap + 8 * g + 5] = clock64();
           mbar_arrive_expect_tx(&full[s], nr * (KT * 4 + 4 + d * 4));
           bulk_g2s(sB + s * (S::kStageB / 4), A.B + row * KT, nr * KT * 4, &full[s]);
           bulk_g2s(sIdx + s * 128, A.ridx + row, nr * 4, &full[s]);
@@ -245,19 +280,19 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       for (uint32_t j = 0;; ++j) {
         const uint32_t ab = j % kSplitNA;
         mbar_wait(&afull[ab], (j / kSplitNA) & 1u);
+        if (A.dbg && blockIdx.x == 0 && (int)j < A.dbg_cap) A.dbg[8 * j + 7] = clock64();
         const int4 rec = s_rec[ab];
         if (rec.z < 0) break;
+        const SplitWin win = s_win[ab];
         tc_fence_after();
-        long long r0, r1;
-        int cb, ce;
-        window(rec, r0, r1, cb, ce);
-        for (int c = cb; c < ce; ++c, ++g) {
+        for (int c = win.cb; c < win.ce; ++c, ++g) {
           const int s = g % kSplitStages;
           const uint32_t b = g & 1u, use = g >> 1;
           mbar_wait(&full[s], (g / kSplitStages) & 1u);
+          if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * A.dbg_cap + 8 * g + 6] = clock64();
           if (use > 0) mbar_wait(&tempty[b], (use - 1) & 1u);
           tc_fence_after();
-          const int nr = (int)dmin_ll(128, r1 - (r0 + (long long)c * 128));
+          const int nr = (int)dmin_ll(128, win.r1 - (win.r0 + (long long)c * 128));
           const uint32_t idesc = idesc_tf32(nr);
 #pragma unroll
           for (int h = 0; h < KT / 8; ++h) {
@@ -272,6 +307,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            smem_addr(&tfull[b]))
                        : "memory");
+          if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * A.dbg_cap + 8 * g + 1] = clock64();
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_addr(&aempty[ab]))
@@ -280,14 +316,18 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
     }
   } else {
     // ===== epilogue: one thread per item (query) of the tile =====
-    uint64_t* qslot = s_queue + tid;
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
+    const int capw = A.capw;
     uint32_t g = 0;
+    const bool dbg_on = A.dbg && blockIdx.x == 0 && tid == 0;
     for (uint32_t j = 0;; ++j) {
       const uint32_t ab = j % kSplitNA;
+      if (dbg_on && (int)j < A.dbg_cap) A.dbg[8 * j + 5] = clock64();
       mbar_wait(&afull[ab], (j / kSplitNA) & 1u);
+      if (dbg_on && (int)j < A.dbg_cap) A.dbg[8 * j + 6] = clock64();
       const int4 rec = s_rec[ab];
       if (rec.z < 0) break;
+      const SplitWin win = s_win[ab];
       const bool valid = tid < rec.z;
       const int qi = valid ? sQi[ab * 128 + tid] : 0;
       const float* arow_s = sA + ab * (S::kA / 4);
@@ -295,9 +335,6 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       const float qn = valid ? arow_s[canon_off(tid, KT - 1, KT)] : 0.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&aempty[ab]);
-      long long r0, r1;
-      int cb, ce;
-      window(rec, r0, r1, cb, ce);
 
       const float qnc = (1.0f - kTcMargin) * qn;
       const bool force = valid && !(qn >= 1e-30f && qn <= 1e30f);
@@ -306,65 +343,68 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       if (valid) thr = force ? __int_as_float(0x7f800000) : __fsub_ru(kth, qnc) + 1e-6f * (fabsf(kth) + qnc);
       int cn = 0;
       bool have_q = false;
-      float qv[KT - 1];
+      float qv[kSplitMaxD];
 #pragma unroll
-      for (int jj = 0; jj < KT - 1; ++jj) qv[jj] = 0.0f;
+      for (int jj = 0; jj < kSplitMaxD; ++jj) qv[jj] = 0.0f;
+      // this (query, window)'s candidates go straight to its slice of the list
+      uint64_t* cdst = A.cand + ((long long)qi * A.NW + rec.w) * capw;
 
-      // the query's candidates (reference distance <= kth) to its list
-      auto flush = [&]() {
-        if (cn > 0) {
-          const int base = atomicAdd(A.ccnt + qi, cn);
-          uint64_t* dst = A.cand + (long long)qi * kSplitCap;
-          for (int e = 0; e < cn; ++e)
-            if (base + e < kSplitCap) dst[base + e] = qslot[e * kNT];
-          if (base <= kSplitCap && base + cn > kSplitCap) A.ovf[atomicAdd(A.novf, 1)] = qi;
-          cn = 0;
-        }
-      };
       auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
         uint32_t mask = 0;
         if (valid) {
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) mask |= (!(__uint_as_float(v[jj]) > thr) ? 1u : 0u) << jj;
         }
+        if (A.stats) {
+          unsigned long long sv = __popc(mask);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+          if (lane == 0) atomicAdd(A.stats + 5, sv);
+        }
         if (mask && !have_q) {
           const float* qp = A.q + (long long)qi * A.qstride;
 #pragma unroll
-          for (int jj = 0; jj < KT - 1; ++jj) qv[jj] = jj < d ? __ldg(qp + jj) : 0.0f;
+          for (int jj = 0; jj < kSplitMaxD; ++jj) qv[jj] = jj < d ? __ldg(qp + jj) : 0.0f;
           have_q = true;
         }
         const uint32_t* ids = sIdx + s * 128 + gcol;
         const float* prow = sRows + s * (S::kStageRows / 4) + gcol * d;
         while (__any_sync(0xffffffffu, mask != 0)) {
+          if (A.stats && lane == 0) atomicAdd(A.stats + 6, 1ull);
           if (mask) {
             const int jj0 = __ffs(mask) - 1;
             mask &= mask - 1;
             const float* pp = prow + jj0 * d;
-            float pv[KT - 1];
+            float pv[kSplitMaxD];
 #pragma unroll
-            for (int jj = 0; jj < KT - 1; ++jj) pv[jj] = jj < d ? pp[jj] : 0.0f;
+            for (int jj = 0; jj < kSplitMaxD; ++jj) pv[jj] = jj < d ? pp[jj] : 0.0f;
             float acc = 0.0f;
 #pragma unroll
-            for (int jj = 0; jj < KT - 1; ++jj) {
+            for (int jj = 0; jj < kSplitMaxD; ++jj) {
               if (jj < d) {
                 const float df = __fsub_rn(qv[jj], pv[jj]);
                 if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
                 else acc = __fadd_rn(acc, __fmul_rn(df, df));
               }
             }
-            if (acc <= kth && ids[jj0] != kIndexSentinel) qslot[(cn++) * kNT] = pack_key(acc, ids[jj0]);
+            if (acc <= kth && ids[jj0] != kIndexSentinel) {
+              if (cn < capw) cdst[cn] = pack_key(acc, ids[jj0]);
+              ++cn;
+            }
           }
-          if (__any_sync(0xffffffffu, cn == kQueue)) flush();
         }
       };
 
-      for (int c = cb; c < ce; ++c, ++g) {
+      for (int c = win.cb; c < win.ce; ++c, ++g) {
         const int s = g % kSplitStages;
         const uint32_t b = g & 1u;
+        const bool dbg_c = dbg_on && (int)g < A.dbg_cap;
+        if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 2] = clock64();
         mbar_wait(&tfull[b], (g >> 1) & 1u);
+        if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 3] = clock64();
         tc_fence_after();
-        const long long row0 = r0 + (long long)c * 128;
-        const int ngrp = (int)dmin_ll(128, r1 - row0) / 32;
+        const long long row0 = win.r0 + (long long)c * 128;
+        const int ngrp = (int)dmin_ll(128, win.r1 - row0) / 32;
         const uint32_t tbase = tmem + lane_base + b * 128;
         uint32_t va[32], vb[32];
         float gmn[4];
@@ -406,8 +446,16 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
           mbar_arrive(&tempty[b]);
           mbar_arrive(&empty[s]);
         }
+        if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 4] = clock64();
       }
-      if (__any_sync(0xffffffffu, cn > 0)) flush();
+      if (cn > 0) {
+        A.ccnt[(long long)qi * A.NW + rec.w] = (uint8_t)min(cn, 255);
+        if (cn > capw && atomicOr(A.ovflag + qi, 1) == 0) A.ovf[atomicAdd(A.novf, 1)] = qi;
+        if (A.stats) {
+          atomicAdd(A.stats + 2, (unsigned long long)cn);
+          atomicAdd(A.stats + 3, 1ull);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -435,8 +483,10 @@ struct AdvanceArgs {
   uint32_t* state;
   int* next;
   uint32_t* visits;
-  int* ccnt;                 // candidates of the round (all zero after the home round)
-  const uint64_t* cand;
+  uint8_t* ccnt;             // m x NW candidates of the round per window (all zero after the home round)
+  const uint64_t* cand;      // m x NW x capw
+  int* ovflag;               // m: rescanned this round
+  int NW, capw;
   const float* centroid;     // nl x kSplitKT
   float* arow;               // m x kSplitKT
   int* seq_log;
@@ -460,28 +510,38 @@ __global__ void __launch_bounds__(kAdvThreads) advance_kernel(const AdvanceArgs 
   const int k = a.k;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int qi = __ldg(a.list + i);
-    // 1. merge this visit's candidates into the top-k row
-    const int nc = a.ccnt[qi];
-    float kth;
-    if (nc > 0) a.ccnt[qi] = 0;
-    if (nc > 0 && nc <= kSplitCap) {
-      // register top-k (descending, sentinel-padded: leafscan.cuh merge_queue)
-      uint64_t* row = a.keys + (long long)qi * k;
-      const uint64_t* cp = a.cand + (long long)qi * kSplitCap;
-      uint64_t arr[KB];
-#pragma unroll
-      for (int j = 0; j < KB; ++j) arr[j] = j < k ? row[k - 1 - j] : 0ull;
-      for (int e = 0; e < nc; ++e) {
-        const uint64_t c = cp[e];
-        if (c < arr[0]) topk_insert<KB>(arr, c);
-      }
-#pragma unroll
-      for (int j = 0; j < KB; ++j)
-        if (j < k) row[k - 1 - j] = arr[j];
-      kth = key_dist(arr[0]);
-      a.kthv[qi] = kth;
+    // 1. merge this visit's candidates (one list per window) into the top-k row
+    float kth = a.kthv[qi];
+    if (a.ovflag[qi]) {
+      a.ovflag[qi] = 0;  // rescanned: the row and kth are final; drop the lists
+      for (int w = 0; w < a.NW; ++w) a.ccnt[(long long)qi * a.NW + w] = 0;
     } else {
-      kth = a.kthv[qi];  // unchanged, or rescanned (nc > cap)
+      // register top-k (descending, sentinel-padded: leafscan.cuh merge_queue)
+      uint64_t arr[KB];
+      bool loaded = false;
+      uint64_t* row = a.keys + (long long)qi * k;
+      for (int w = 0; w < a.NW; ++w) {
+        const int nc = a.ccnt[(long long)qi * a.NW + w];
+        if (nc == 0) continue;
+        a.ccnt[(long long)qi * a.NW + w] = 0;
+        if (!loaded) {
+#pragma unroll
+          for (int j = 0; j < KB; ++j) arr[j] = j < k ? row[k - 1 - j] : 0ull;
+          loaded = true;
+        }
+        const uint64_t* cp = a.cand + ((long long)qi * a.NW + w) * a.capw;
+        for (int e = 0; e < nc; ++e) {
+          const uint64_t c = cp[e];
+          if (c < arr[0]) topk_insert<KB>(arr, c);
+        }
+      }
+      if (loaded) {
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < k) row[k - 1 - j] = arr[j];
+        kth = key_dist(arr[0]);
+        a.kthv[qi] = kth;
+      }
     }
     // 2. FindLeaf with the new k-th distance
     float qv[32];

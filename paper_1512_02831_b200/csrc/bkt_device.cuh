@@ -15,6 +15,7 @@ namespace bkt {
 constexpr uint64_t kEmptyKey = 0x7F800000FFFFFFFFull;
 constexpr uint32_t kIndexSentinel = 0xFFFFFFFFu;
 constexpr int kMaxHeight = 16;   // state packs path + pending mask in 2 x 16 bits
+constexpr int kMaxWideHeight = 30;  // wide path (wide_search.cuh): path + pending mask in 2 x 32 bits
 
 // ----------------------------------------------------------------------------
 // packed float32x2 arithmetic (sm_100a FADD2 / FFMA2; one issue slot, two lanes)

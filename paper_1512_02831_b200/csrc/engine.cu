@@ -33,6 +33,7 @@
 #include "leafscan_tc.cuh"
 #include "round_kernels.cuh"
 #include "split_launch.cuh"
+#include "wide_search.cuh"
 
 using namespace bkt;
 
@@ -71,6 +72,12 @@ struct bkt_ctx {
   int* leaf_size = nullptr;
   float* pts = nullptr;
   uint32_t* pidx = nullptr;
+  // general-domain trees (h > 16 or d > 32): only the wide path (wide_search.cuh)
+  bool wide_only = false;
+  const float* wide_pts = nullptr;      // quad layout the wide kernel reads (HBM, or mapped host memory)
+  const uint32_t* wide_pidx = nullptr;
+  uint64_t* wide_scratch = nullptr;     // per-CTA top-k rows when 2k keys exceed shared memory
+  long long wide_scratch_elems = 0;
   // host-resident (out-of-core) leaf structure
   int residency = 0;
   float* h_pts = nullptr;
@@ -277,6 +284,9 @@ void free_tree(bkt_ctx* c) {
     c->slot_chunk[s] = -1;
   }
   c->has_tree = false;
+  c->wide_only = false;
+  c->wide_pts = nullptr;
+  c->wide_pidx = nullptr;
 }
 
 void free_work(bkt_ctx* c) {
@@ -388,7 +398,7 @@ int ensure_work(bkt_ctx* ctx, long long m, int k) {
   CU(cudaMalloc(&ctx->pos, sizeof(int2) * M));
   CU(cudaMalloc(&ctx->work[0], sizeof(int) * M));
   CU(cudaMalloc(&ctx->work[1], sizeof(int) * M));
-  ctx->tiles_cap = M / kNT + (1ll << ctx->h) + 1;
+  ctx->tiles_cap = ctx->wide_only ? 1 : M / kNT + (1ll << ctx->h) + 1;
   CU(cudaMalloc(&ctx->tiles, sizeof(int4) * ctx->tiles_cap));
   ctx->cap_m = M;
   ctx->cap_k = k;
@@ -751,10 +761,9 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
                   const float* leaf_points, const int64_t* original_index, const int64_t* leaf_starts,
                   int32_t residency, int32_t num_chunks, const int64_t* chunk_bounds) {
   if (!ctx) return set_err(nullptr, BKT_EINVAL, "ctx is NULL");
-  if (h < 1 || h > kMaxHeight)
-    return set_err(ctx, BKT_EINVAL, "height " + std::to_string(h) + " outside the supported range [1, 16]");
-  if (d < 1 || d > kMaxKernelDim)
-    return set_err(ctx, BKT_EINVAL, "dimensionality " + std::to_string(d) + " outside the supported range [1, 32]");
+  if (h < 1 || h > kMaxWideHeight)
+    return set_err(ctx, BKT_EINVAL, "height " + std::to_string(h) + " outside the supported range [1, 30]");
+  if (d < 1) return set_err(ctx, BKT_EINVAL, "dimensionality must be >= 1");
   if (n < (1ll << h)) return set_err(ctx, BKT_EINVAL, "height needs at least 2^h points");
   if (n >= (long long)kIndexSentinel) return set_err(ctx, BKT_EINVAL, "point count exceeds the supported maximum");
   if (residency != 0 && residency != 1) return set_err(ctx, BKT_EINVAL, "residency must be 0 or 1");
@@ -765,8 +774,13 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
   free_tree(ctx);
   ctx->grid_cache.clear();
   const int nl = 1 << h;
-  const int D = kernel_dim(d);
+  // h > 16 or d > 32: outside the round engine's packed state / compiled
+  // dimensionalities; the tree is searched by the wide path only (quad layout
+  // of width d)
+  const bool wide_only = h > kMaxHeight || d > kMaxKernelDim;
+  const int D = wide_only && d > kMaxKernelDim ? d : kernel_dim(d);
   ctx->h = h; ctx->d = d; ctx->D = D; ctx->nl = nl; ctx->n = n;
+  ctx->wide_only = wide_only;
   // quad bases: each leaf padded to a multiple of 4 points
   ctx->h_quad_base.assign(nl + 1, 0);
   ctx->h_leaf_size.assign(nl, 0);
@@ -791,8 +805,9 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
 
   const size_t pts_bytes = sizeof(float) * (size_t)TQ * 4 * D;
   const size_t idx_bytes = sizeof(uint32_t) * (size_t)TQ * 4;
-  CU(cudaHostAlloc(&ctx->h_pts, pts_bytes, cudaHostAllocDefault));
-  CU(cudaHostAlloc(&ctx->h_pidx, idx_bytes, cudaHostAllocDefault));
+  // mapped: the wide path reads a host-resident structure in place
+  CU(cudaHostAlloc(&ctx->h_pts, pts_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  CU(cudaHostAlloc(&ctx->h_pidx, idx_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
   build_quad_layout(leaf_points, original_index, leaf_starts, nl, d, D, ctx->h_quad_base, ctx->h_pts, ctx->h_pidx);
 
   ctx->residency = residency;
@@ -804,7 +819,9 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
     hfree(ctx->h_pts);
     hfree(ctx->h_pidx);
     ctx->num_chunks = 1;
-    if (d + 1 <= 32) {
+    ctx->wide_pts = ctx->pts;
+    ctx->wide_pidx = ctx->pidx;
+    if (d + 1 <= 32 && !wide_only) {
       const int KT = (d + 1 <= 16) ? 16 : 32;
       std::vector<long long> rb(nl + 1, 0);
       for (int l = 0; l < nl; ++l) rb[l + 1] = rb[l] + ((long long)ctx->h_leaf_size[l] + 31) / 32 * 32;
@@ -911,6 +928,14 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
     // containing quad of the padded layout; results do not depend on where a
     // chunk boundary falls (reference scheduler.py:1-10, acceptance crit. 2).
     ctx->num_chunks = num_chunks;
+    {
+      float* dp = nullptr;
+      uint32_t* di = nullptr;
+      CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), ctx->h_pts, 0));
+      CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&di), ctx->h_pidx, 0));
+      ctx->wide_pts = dp;
+      ctx->wide_pidx = di;
+    }
     ctx->chunk_q.assign(num_chunks + 1, 0);
     for (int j = 0; j <= num_chunks; ++j) {
       long long row = chunk_bounds ? chunk_bounds[j] : (long long)(((__int128)j * n + num_chunks - 1) / num_chunks);
@@ -940,6 +965,11 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       CU(cudaMalloc(&ctx->slot_idx[s], sizeof(uint32_t) * ctx->slot_quads * 4));
       ctx->slot_chunk[s] = -1;
     }
+  }
+  if (wide_only) {
+    ctx->min_leaf = *std::min_element(ctx->h_leaf_size.begin(), ctx->h_leaf_size.end());
+    ctx->has_tree = true;
+    return BKT_OK;
   }
   if (ctx->nkeys == 0) {
     // one block per leaf (no leaf-internal order)
@@ -1006,6 +1036,9 @@ struct SearchRun {
   long long finish_at = -1;  // tail finisher: one launch once at most this many queries remain (-1: off)
   bool finish_cta = false;   // finisher with one CTA per query (else one warp per query)
   bool split = false;        // later rounds as (leaf, window) items (split_scan.cuh)
+  bool wide = false;         // general-domain path (wide_search.cuh)
+  bool wide_rows_smem = true;
+  size_t wide_smem = 0;
   bool renumber = false;     // search in home-bucket order (gather_rows_kernel)
   bool verbose = false;      // BKT_VERBOSE: split-round totals on stderr
   int split_from = 1;        // first split round (earlier rounds: leaf-level tiles)
@@ -1426,7 +1459,53 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R);
 // The batch in home-bucket order: a first start/plan/scatter pass orders the
 // queries by (home leaf, home block); the search runs on the reordered rows
 // and its per-query outputs (keys, visit counts, visit log) are mapped back.
+// The general-domain path: every query's whole traversal in one launch.
+int wide_batch(bkt_ctx* ctx, SearchRun& R) {
+  RoundCtl init{};
+  init.active = (int)R.m;
+  CU(cudaMemcpyAsync(ctx->ctl, &init, sizeof(RoundCtl), cudaMemcpyHostToDevice, ctx->stream));
+  WideArgs a{};
+  a.q = ctx->q;
+  a.D = ctx->D;
+  a.m = (int)R.m;
+  a.k = R.k;
+  a.top = TopTreeView{ctx->split, ctx->h, ctx->d};
+  a.keys = ctx->keys;
+  a.visits = ctx->visits;
+  a.pts = ctx->wide_pts;
+  a.pidx = ctx->wide_pidx;
+  a.quad_base = ctx->quad_base;
+  a.leaf_size = ctx->leaf_size;
+  a.pairs = ctx->pairs;
+  a.ctl = ctx->ctl;
+  a.seq_log = R.seq ? ctx->seq_dev : nullptr;
+  a.seq_pos = ctx->seq_pos;
+  a.seq_cap = R.seq_cap;
+  a.scratch = R.wide_rows_smem ? nullptr : ctx->wide_scratch;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (R.timing) {
+    e0 = get_event(ctx, R.ev_next++);
+    e1 = get_event(ctx, R.ev_next++);
+    CU(cudaEventRecord(e0, ctx->stream));
+  }
+  CU(launch_wide(R.fma, (int)std::min<long long>(R.grid_scan, std::max<long long>(R.m, 1)), ctx->stream, a,
+                 R.wide_smem, nullptr));
+  if (R.timing) {
+    CU(cudaEventRecord(e1, ctx->stream));
+    R.scan_events.emplace_back(e0, e1);
+  }
+  R.launches++;
+  R.leafscan_launches++;
+  CU(cudaStreamSynchronize(ctx->stream));
+  RoundCtl fin;
+  CU(cudaMemcpy(&fin, ctx->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost));
+  R.rounds += fin.rounds;
+  R.scans += fin.scans;
+  return BKT_OK;
+}
+
 int search_batch(bkt_ctx* ctx, SearchRun& R) {
+  if (R.wide) return wide_batch(ctx, R);
   if (!R.renumber || R.m < (1 << 16)) return search_batch_impl(ctx, R);
   const long long m = R.m;
   TopTreeView top{ctx->split, ctx->h, ctx->d};
@@ -1615,7 +1694,6 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   if (k > ctx->n)
     return set_err(ctx, BKT_EINVAL, "k=" + std::to_string(k) + " exceeds the number of reference points (" +
                                         std::to_string(ctx->n) + ")");
-  if (k > kMaxK) return set_err(ctx, BKT_EINVAL, "k=" + std::to_string(k) + " exceeds the supported maximum (64)");
   bkt_search_opts o{};
   o.exact = 1;
   if (opts) o = *opts;
@@ -1634,7 +1712,9 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   R.seq_cap = R.seq ? o.seq_cap : 0;
   // auto: the tensor-core filter from d >= 8 (below that the CUDA-core scan is
   // as fast: few pairs per query and a mostly empty K=16 MMA; tools/configs.py cfg4)
-  R.tc = ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
+  // k > 64 or a general-domain tree: the wide path (one CTA per query, wide_search.cuh)
+  R.wide = ctx->wide_only || k > kMaxK;
+  R.tc = !R.wide && ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
   R.unfused = false;
   if (const char* e = std::getenv("BKT_TC_N")) R.tc_rows = std::atoi(e) == 64 ? 64 : (std::atoi(e) == 256 ? 256 : 128);
   if (const char* e = std::getenv("BKT_TC_CPS")) R.tc_cps = std::atoi(e) == 3 ? 3 : 2;
@@ -1648,11 +1728,29 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
             R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
-  R.renumber = ctx->residency == 0 && !std::getenv("BKT_EARLY_DRAIN");
+  R.renumber = ctx->residency == 0 && !R.wide && !std::getenv("BKT_EARLY_DRAIN");
   R.verbose = std::getenv("BKT_VERBOSE") != nullptr;
   if (const char* e = std::getenv("BKT_RENUMBER")) R.renumber = R.renumber && std::atoi(e) != 0;
   int rc = BKT_OK;
-  if (R.tc) {
+  if (R.wide) {
+    // rows of 2k keys in shared memory while they fit (up to ~190 KB per CTA)
+    R.wide_rows_smem = wide_smem_bytes(k, ctx->d, true) <= 190u * 1024u;
+    R.wide_smem = wide_smem_bytes(k, ctx->d, R.wide_rows_smem);
+    int occ = 0;
+    WideArgs dummy{};
+    CU(launch_wide(R.fma, 0, nullptr, dummy, R.wide_smem, &occ));
+    if (occ < 1) return set_err(ctx, BKT_ECUDA, "wide search kernel cannot be resident");
+    R.grid_scan = occ * ctx->sm_count;
+    if (!R.wide_rows_smem) {
+      const long long need = 2ll * k * R.grid_scan;
+      if (ctx->wide_scratch_elems < need) {
+        dfree(ctx->wide_scratch);
+        ctx->wide_scratch_elems = 0;
+        CU(cudaMalloc(&ctx->wide_scratch, sizeof(uint64_t) * need));
+        ctx->wide_scratch_elems = need;
+      }
+    }
+  } else if (R.tc) {
     // two CTAs per SM (2 x 256 TMEM columns); the attributes are set by the query
     int occ = 0;
     TcArgs dummy{};
@@ -1677,7 +1775,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   //  * deeper trees of short leaves (h >= 12): one warp per query once
   //    <= min(512 per SM, m / 8) remain (config 5 h = 14: 1.27 -> 2.0 M q/s);
   //  * otherwise off (config 1, 256-point leaves: no gain).
-  if (ctx->residency == 0 && ctx->d <= 32 && k <= 64) {
+  if (ctx->residency == 0 && ctx->d <= 32 && k <= 64 && !R.wide) {
     if (ctx->n >= 512ll * ctx->nl) {
       R.finish_at = (long long)ctx->sm_count * 48;
       R.finish_cta = true;

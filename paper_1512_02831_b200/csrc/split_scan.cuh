@@ -50,6 +50,10 @@
 
 namespace bkt {
 
+#ifndef BKT_SPLIT_QEAGER
+#define BKT_SPLIT_QEAGER 1
+#endif
+
 constexpr int kSplitKT = 16;     // A row: d coordinates, 1.0 at column d, zeros, kth at KT-2, |q'|^2 at KT-1 (d <= 13)
 constexpr int kSplitMaxD = kSplitKT - 3;
 constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhead = 2 tiles ahead
@@ -348,6 +352,18 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       for (int jj = 0; jj < kSplitMaxD; ++jj) qv[jj] = 0.0f;
       // this (query, window)'s candidates go straight to its slice of the list
       uint64_t* cdst = A.cand + ((long long)qi * A.NW + rec.w) * capw;
+#if BKT_SPLIT_QEAGER
+      // the query's coordinates for survivor re-evaluation, loaded at the
+      // tile's start so their latency overlaps the first chunks' MMA
+      // (config 2: 33.6 -> 36.1 M q/s; lazily at the first survivor the load
+      // was a long-scoreboard stall on nearly every tile's critical path)
+      if (valid) {
+        const float* qp = A.q + (long long)qi * A.qstride;
+#pragma unroll
+        for (int jj = 0; jj < kSplitMaxD; ++jj) qv[jj] = jj < d ? __ldg(qp + jj) : 0.0f;
+      }
+      have_q = true;
+#endif
 
       auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
         uint32_t mask = 0;

@@ -1309,7 +1309,6 @@ int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
   a.visits = ctx->visits;
   a.ccnt = ctx->ccnt;
   a.cand = ctx->cand;
-  a.ovflag = ctx->ovflag;
   a.NW = ctx->split_NW;
   a.capw = split_capw(ctx->split_NW);
   a.centroid = ctx->tc_centroid;
@@ -1432,7 +1431,8 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
     R.launches++;
     R.leafscan_launches++;
     CU(launch_rescan(R.fma, ctx->sm_count * 4, ctx->stream, ctx->ovf, ctx->ctl, ctx->q, ctx->D, R.k, ctx->d,
-                     ctx->keys, ctx->kthv, ctx->next, ctx->pts, ctx->pidx, ctx->quad_base));
+                     ctx->keys, ctx->kthv, ctx->next, ctx->pts, ctx->pidx, ctx->quad_base, ctx->ccnt,
+                     ctx->split_NW, ctx->ovflag));
     R.launches++;
     int rc = launch_advance_round(ctx, R, ctx->work[cur]);
     if (rc != BKT_OK) return rc;

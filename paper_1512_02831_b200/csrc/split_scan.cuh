@@ -501,7 +501,6 @@ struct AdvanceArgs {
   uint32_t* visits;
   uint8_t* ccnt;             // m x NW candidates of the round per window (all zero after the home round)
   const uint64_t* cand;      // m x NW x capw
-  int* ovflag;               // m: rescanned this round
   int NW, capw;
   const float* centroid;     // nl x kSplitKT
   float* arow;               // m x kSplitKT
@@ -514,7 +513,7 @@ constexpr int kAdvThreads = 256;
 __host__ __device__ inline int advance_smem_bytes(int h, int d) { return (start_tree_smem(h) + d * kAdvThreads) * 4; }
 
 template <int KB>
-__global__ void __launch_bounds__(kAdvThreads) advance_kernel(const AdvanceArgs a) {
+__global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceArgs a) {
   extern __shared__ float s_adv[];
   const int ntree = start_tree_smem(a.top.h);
   float* s_split = s_adv;
@@ -527,28 +526,42 @@ __global__ void __launch_bounds__(kAdvThreads) advance_kernel(const AdvanceArgs 
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int qi = __ldg(a.list + i);
     // 1. merge this visit's candidates (one list per window) into the top-k row
+    // (a query the rescan handled has its counts zeroed: its row and kth are final)
     float kth = a.kthv[qi];
-    if (a.ovflag[qi]) {
-      a.ovflag[qi] = 0;  // rescanned: the row and kth are final; drop the lists
-      for (int w = 0; w < a.NW; ++w) a.ccnt[(long long)qi * a.NW + w] = 0;
-    } else {
+    {
       // register top-k (descending, sentinel-padded: leafscan.cuh merge_queue)
       uint64_t arr[KB];
       bool loaded = false;
       uint64_t* row = a.keys + (long long)qi * k;
-      for (int w = 0; w < a.NW; ++w) {
-        const int nc = a.ccnt[(long long)qi * a.NW + w];
-        if (nc == 0) continue;
-        a.ccnt[(long long)qi * a.NW + w] = 0;
+      const int NW = a.NW;
+      uint8_t* cc = a.ccnt + (long long)qi * NW;
+      for (int w0 = 0; w0 < NW; w0 += 8) {
+        // eight windows' counts per load when the rows are 8-byte aligned
+        uint64_t word = 0;
+        if ((NW & 7) == 0) {
+          word = *reinterpret_cast<const uint64_t*>(cc + w0);
+        } else {
+          for (int w = w0; w < min(NW, w0 + 8); ++w) word |= (uint64_t)cc[w] << (8 * (w - w0));
+        }
+        if (word == 0) continue;
+        if ((NW & 7) == 0) {
+          *reinterpret_cast<uint64_t*>(cc + w0) = 0ull;
+        } else {
+          for (int w = w0; w < min(NW, w0 + 8); ++w) cc[w] = 0;
+        }
         if (!loaded) {
 #pragma unroll
           for (int j = 0; j < KB; ++j) arr[j] = j < k ? row[k - 1 - j] : 0ull;
           loaded = true;
         }
-        const uint64_t* cp = a.cand + ((long long)qi * a.NW + w) * a.capw;
-        for (int e = 0; e < nc; ++e) {
-          const uint64_t c = cp[e];
-          if (c < arr[0]) topk_insert<KB>(arr, c);
+        for (int b = 0; b < 8; ++b) {
+          const int nc = min((int)((word >> (8 * b)) & 0xFF), a.capw);
+          if (nc == 0) continue;
+          const uint64_t* cp = a.cand + ((long long)qi * NW + w0 + b) * a.capw;
+          for (int e = 0; e < nc; ++e) {
+            const uint64_t c = cp[e];
+            if (c < arr[0]) topk_insert<KB>(arr, c);
+          }
         }
       }
       if (loaded) {
@@ -560,10 +573,10 @@ __global__ void __launch_bounds__(kAdvThreads) advance_kernel(const AdvanceArgs 
       }
     }
     // 2. FindLeaf with the new k-th distance
-    float qv[32];
+    float qv[kSplitMaxD];
     const float* qp = a.q + (long long)qi * a.D;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < kSplitMaxD; ++j) {
       qv[j] = j < d ? __ldg(qp + j) : 0.0f;
       if (j < d) myq[j * kAdvThreads] = qv[j];
     }
@@ -589,14 +602,20 @@ __global__ void __launch_bounds__(kAdvThreads) advance_kernel(const AdvanceArgs 
       }
       rk = warp_reserve(a.counts, nxt);  // next round's bucket (key = leaf) and slot
       // A row of the next visit: tf32(q - c) | 1 | 0.. | kth | |q - c|^2
-      const float* cen = a.centroid + (long long)nxt * kSplitKT;
+      const float4* cen4 = reinterpret_cast<const float4*>(a.centroid + (long long)nxt * kSplitKT);
+      float cen[kSplitKT];
+#pragma unroll
+      for (int j = 0; j < kSplitKT / 4; ++j) {
+        const float4 c4 = __ldg(cen4 + j);
+        cen[4 * j] = c4.x; cen[4 * j + 1] = c4.y; cen[4 * j + 2] = c4.z; cen[4 * j + 3] = c4.w;
+      }
       float r[kSplitKT];
       float qn = 0.0f;
 #pragma unroll
       for (int j = 0; j < kSplitKT; ++j) {
         float v = 0.0f;
         if (j < d) {
-          const float qc = __fsub_rn(qv[j], __ldg(cen + j));
+          const float qc = __fsub_rn(qv[j], cen[j]);
           qn = __fmaf_rn(qc, qc, qn);
           v = __uint_as_float(tf32_rna(qc));
         } else if (j == d) {
@@ -663,17 +682,17 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const RouteArgs a)
       const int p = rt.y + r;
       const int qi = __ldg(a.work + p);
       const float kth = __ldg(a.kthv + qi);
-      float qv[32];
+      float qv[kSplitMaxD];
       const float* qp = a.q + (long long)qi * a.D;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) qv[j] = j < d ? __ldg(qp + j) : 0.0f;
+      for (int j = 0; j < kSplitMaxD; ++j) qv[j] = j < d ? __ldg(qp + j) : 0.0f;
       unsigned long long mask = 0;
       for (int w = 0; w < nw; ++w) {
         // box lower bound in f32, relaxed by 1e-5: never above the reference distance
         const float* bx = s_box + w * 2 * d;
         float lb = 0.0f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < kSplitMaxD; ++j) {
           if (j < d) {
             const float e = fmaxf(fmaxf(bx[j] - qv[j], qv[j] - bx[d + j]), 0.0f);
             lb = __fmaf_rn(e, e, lb);
@@ -778,7 +797,8 @@ template <bool FMA>
 __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
     const int* __restrict__ ovf, const RoundCtl* ctl, const float* __restrict__ q, int D, int k, int d,
     uint64_t* __restrict__ keys, float* __restrict__ kthv, const int* __restrict__ next,
-    const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base) {
+    const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base,
+    uint8_t* __restrict__ ccnt, int NW, int* __restrict__ ovflag) {
   __shared__ uint64_t s_row[kFinishWarps][64];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   uint64_t* row = s_row[wl];
@@ -786,6 +806,9 @@ __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
   for (int i = blockIdx.x * kFinishWarps + wl; i < n; i += gridDim.x * kFinishWarps) {
     const int qi = __ldg(ovf + i);
     const int leaf = next[qi];
+    // the row and kth become final here: advance_kernel merges nothing for this visit
+    for (int w = lane; w < NW; w += 32) ccnt[(long long)qi * NW + w] = 0;
+    if (lane == 0) ovflag[qi] = 0;
     uint64_t* kp = keys + (long long)qi * k;
     for (int j = lane; j < k; j += 32) row[j] = kp[j];
     __syncwarp();

@@ -248,6 +248,10 @@ struct TcTileIn {
   uint32_t st, vis;
 };
 
+#ifndef BKT_TC_PIPE
+#define BKT_TC_PIPE 1
+#endif
+
 // 3-input-min tree over 32 TMEM values (depth 4 instead of a 31-long chain)
 __device__ __forceinline__ float min32(const uint32_t (&v)[32]) {
   float m1[11];
@@ -839,12 +843,36 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
         // in which some lane has a candidate (thr only decreases meanwhile)
         constexpr int kGrp = NR / 32;
         float gmn[kGrp];
+        const float kInf = __int_as_float(0x7f800000);
+#if BKT_TC_PIPE
+        // every group loaded unconditionally (columns past a short chunk hold
+        // an earlier chunk's values and are masked below), each load issued
+        // while the previous group's minimum is computed
+        tmem_ld32_async(tbase, va);
+        tmem_ld32_async(tbase + 32, vb);
+        tmem_wait(va);
+        tmem_touch(vb);
+        if (dbg_on) A.dbg[16 * g + 7] = clock64();
+        gmn[0] = min32(va);
+#pragma unroll
+        for (int gp = 2; gp < kGrp; gp += 2) {
+          tmem_ld32_async(tbase + 32 * gp, va);
+          gmn[gp - 1] = min32(vb);
+          tmem_ld32_async(tbase + 32 * (gp + 1), vb);
+          tmem_wait(va);
+          tmem_touch(vb);
+          gmn[gp] = min32(va);
+        }
+        gmn[kGrp - 1] = min32(vb);
+#pragma unroll
+        for (int gi = 1; gi < kGrp; ++gi)
+          if (gi >= ngrp) gmn[gi] = kInf;
+#else
         tmem_ld32_async(tbase, va);
         if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
         tmem_wait(va);
         tmem_touch(vb);
         if (dbg_on) A.dbg[16 * g + 7] = clock64();
-        const float kInf = __int_as_float(0x7f800000);
         gmn[0] = min32(va);
         gmn[1] = ngrp > 1 ? min32(vb) : kInf;
 #pragma unroll
@@ -861,6 +889,7 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
             gmn[gp + 1] = kInf;
           }
         }
+#endif
         float mchunk = gmn[0];
 #pragma unroll
         for (int gi = 1; gi < kGrp; ++gi) mchunk = fminf(mchunk, gmn[gi]);

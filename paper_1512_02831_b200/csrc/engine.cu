@@ -122,7 +122,7 @@ struct bkt_ctx {
   int split_W = 0, split_NW = 0;  // split_NW == 0: split rounds unavailable
   int min_leaf = 0;                // smallest leaf (split rounds need kth finite after the home visit)
   int* win_base = nullptr;         // nl + 1
-  float* win_box = nullptr;        // per window: lo[d], hi[d]
+  float* win_box = nullptr;        // per window, per dimension: {lo, -hi}
 
   // ---- per-batch work buffers
   long long cap_m = 0;
@@ -152,7 +152,7 @@ struct bkt_ctx {
   int* seq_dev = nullptr;
   long long seq_dev_cap = 0;
   // pinned host mirrors
-  RoundCtl* h_ctl = nullptr;  // ring of kRing slots (mapped page-locked memory)
+  RoundCtl* h_ctl = nullptr;  // ring of kMirror slots (mapped page-locked memory)
   RoundCtl* d_ctl_mirror = nullptr;  // device address of h_ctl (plan_kernel writes its slot)
   int* h_tile_off = nullptr;
   int h_tile_off_cap = 0;
@@ -194,6 +194,7 @@ struct bkt_ctx {
 
   std::vector<cudaEvent_t> ev_pool;   // leafscan timing events
   cudaEvent_t ring_ev[4] = {};        // round-check ring (kRing)
+  cudaEvent_t group_ev[2] = {};       // graph mode: end of the last two round groups
   cudaEvent_t t_ev[3] = {};           // whole-search timing + early-drain marker
   // leafscan grid per (D, KB, mode)
   std::vector<std::pair<long long, int>> grid_cache;
@@ -201,6 +202,8 @@ struct bkt_ctx {
 
 namespace {
 constexpr int kRing = 4;
+constexpr int kGraphRounds = 4;            // split rounds per captured graph
+constexpr int kMirror = 2 * kGraphRounds;  // mapped control-block slots (>= kRing)
 constexpr int kHistCap = 1 << 17;
 
 int set_err(bkt_ctx* c, int code, const std::string& msg) {
@@ -705,9 +708,10 @@ int bkt_open(int cuda_device, bkt_ctx** out) {
   CU(cudaMalloc(&ctx->pairs, sizeof(unsigned long long)));
   CU(cudaMalloc(&ctx->seq_pos, sizeof(unsigned long long)));
   CU(cudaMalloc(&ctx->hist, sizeof(int) * kHistCap));
-  CU(cudaHostAlloc(&ctx->h_ctl, sizeof(RoundCtl) * kRing, cudaHostAllocMapped));
+  CU(cudaHostAlloc(&ctx->h_ctl, sizeof(RoundCtl) * kMirror, cudaHostAllocMapped));
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_ctl_mirror), ctx->h_ctl, 0));
   for (int i = 0; i < kRing; ++i) CU(cudaEventCreateWithFlags(&ctx->ring_ev[i], cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) CU(cudaEventCreateWithFlags(&ctx->group_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) CU(cudaEventCreate(&ctx->t_ev[i]));
   CU(cudaEventCreateWithFlags(&ctx->t_ev[2], cudaEventDisableTiming));
   for (int s = 0; s < 2; ++s) {
@@ -733,6 +737,8 @@ void bkt_close(bkt_ctx* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < kRing; ++i)
     if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
+  for (int i = 0; i < 2; ++i)
+    if (ctx->group_ev[i]) cudaEventDestroy(ctx->group_ev[i]);
   for (int i = 0; i < 3; ++i)
     if (ctx->t_ev[i]) cudaEventDestroy(ctx->t_ev[i]);
   for (int s = 0; s < 2; ++s) {
@@ -891,13 +897,13 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
             const int nch = cb[l + 1] - cb[l];
             NW = std::max(NW, wb[l + 1] - wb[l]);
             for (int w = 0; w < wb[l + 1] - wb[l]; ++w) {
-              float* bx = wbox.data() + (size_t)(wb[l] + w) * 2 * d;
-              for (int j = 0; j < d; ++j) { bx[j] = __builtin_inff(); bx[d + j] = -__builtin_inff(); }
+              float* bx = wbox.data() + (size_t)(wb[l] + w) * 2 * d;  // {lo, -hi} per dimension
+              for (int j = 0; j < d; ++j) { bx[2 * j] = __builtin_inff(); bx[2 * j + 1] = __builtin_inff(); }
               for (int c = w * W; c < std::min(nch, (w + 1) * W); ++c) {
                 const float* cx = box.data() + (size_t)(cb[l] + c) * 2 * d;
                 for (int j = 0; j < d; ++j) {
-                  bx[j] = std::min(bx[j], cx[j]);
-                  bx[d + j] = std::max(bx[d + j], cx[d + j]);
+                  bx[2 * j] = std::min(bx[2 * j], cx[j]);
+                  bx[2 * j + 1] = std::min(bx[2 * j + 1], -cx[d + j]);
                 }
               }
             }
@@ -1036,6 +1042,7 @@ struct SearchRun {
   long long finish_at = -1;  // tail finisher: one launch once at most this many queries remain (-1: off)
   bool finish_cta = false;   // finisher with one CTA per query (else one warp per query)
   bool split = false;        // later rounds as (leaf, window) items (split_scan.cuh)
+  bool graph = false;        // split rounds replayed from a captured CUDA graph (launch-bound searches)
   bool wide = false;         // general-domain path (wide_search.cuh)
   bool wide_rows_smem = true;
   size_t wide_smem = 0;
@@ -1324,17 +1331,19 @@ int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
 // rounds >= 1 as (leaf, window) items until no query is active.  On entry
 // work[cur ^ 1] holds the queries just advanced (pos = their next leaf and
 // bucket slot, counts per leaf).
-int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
-  cudaEvent_t* ring = ctx->ring_ev;
+// Enqueues one split round on ctx->stream (no host synchronisation, so it
+// can be captured into a CUDA graph).  The round's control block goes to
+// mirror slot `slot`; `ring_ev` (or null) is recorded after the plan.
+int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent_t ring_ev, bool capturing) {
   const int nkeys = ctx->nl * ctx->split_NW;
-  for (;;) {
+  {
     // the round's queries bucketed by leaf, in route tiles of kRouteQ
     plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, 1, ctx->nl, ctx->leaf_off,
                                                      ctx->tile_off, ctx->ctl, ctx->nl, kRouteQ, ctx->hist, kHistCap,
-                                                     ctx->d_ctl_mirror + round % kRing);
+                                                     ctx->d_ctl_mirror + slot);
     CU(cudaGetLastError());
     R.launches++;
-    CU(cudaEventRecord(ring[round % kRing], ctx->stream));
+    if (ring_ev) CU(cudaEventRecord(ring_ev, ctx->stream));
     scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], 0, ctx->pos, ctx->qkey, ctx->key_off,
                                                            ctx->work[cur], ctx->ctl, ctx->leaf_off, ctx->tile_off,
                                                            ctx->nl, 1, kRouteQ, ctx->tiles,
@@ -1392,14 +1401,14 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
     sa.W = ctx->split_W;
     sa.stats = R.verbose ? &ctx->ctl->sc_tiles : nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (R.timing) {
+    if (R.timing && !capturing) {
       e0 = get_event(ctx, R.ev_next++);
       e1 = get_event(ctx, R.ev_next++);
       CU(cudaEventRecord(e0, ctx->stream));
     }
     static long long* sdbg = nullptr;
     const char* sdbg_env = std::getenv("BKT_SPLIT_DEBUG");
-    const bool sdbg_now = sdbg_env && R.leafscan_launches == std::atoi(sdbg_env);
+    const bool sdbg_now = !capturing && sdbg_env && R.leafscan_launches == std::atoi(sdbg_env);
     constexpr int kDbgCap = 4096;
     if (sdbg_now) {
       if (!sdbg) CU(cudaMalloc(&sdbg, sizeof(long long) * 16 * kDbgCap));
@@ -1424,7 +1433,7 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
                      hc[8 * g + 5] - b0, hc[8 * g + 6] - b0, hc[8 * g + 1] - b0, hc[8 * g + 2] - b0,
                      hc[8 * g + 3] - b0, hc[8 * g + 4] - b0);
     }
-    if (R.timing) {
+    if (R.timing && !capturing) {
       CU(cudaEventRecord(e1, ctx->stream));
       R.scan_events.emplace_back(e0, e1);
     }
@@ -1434,21 +1443,84 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
                      ctx->keys, ctx->kthv, ctx->next, ctx->pts, ctx->pidx, ctx->quad_base, ctx->ccnt,
                      ctx->split_NW, ctx->ovflag));
     R.launches++;
-    int rc = launch_advance_round(ctx, R, ctx->work[cur]);
-    if (rc != BKT_OK) return rc;
-    cur ^= 1;
-    ++round;
-    if (round >= kRing - 1) {
-      const int chk = (int)((round - (kRing - 1)) % kRing);
-      CU(cudaEventSynchronize(ring[chk]));
-      if (ctx->h_ctl[chk].active == 0) break;
-      if (R.finish_at >= 0 && ctx->h_ctl[chk].active <= R.finish_at) {
-        // the list just advanced (work[cur ^ 1], ctl->active entries) holds every
-        // query still active, each with its next leaf set: finish in one launch
-        rc = launch_finisher(ctx, R, ctx->work[cur ^ 1]);
-        if (rc != BKT_OK) return rc;
-        break;
+    return launch_advance_round(ctx, R, ctx->work[cur]);
+  }
+}
+
+// Rounds >= 1 as (leaf, window) items until no query is active.  On entry
+// work[cur ^ 1] holds the queries just advanced (pos = their next leaf and
+// bucket slot, counts per leaf).
+//
+// Eager mode: rounds are launched ahead of the host check; the active count
+// of round r is read back through mapped memory kRing-1 rounds later.
+// Graph mode (launch-bound searches, R.graph): kGraphRounds rounds are
+// captured once into a CUDA graph and replayed, one graph launch per group
+// instead of eight kernel launches per round; the host checks the last
+// round of the previous group (mirror slots: 2 x kGraphRounds).
+int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
+  cudaEvent_t* ring = ctx->ring_ev;
+  if (!R.graph) {
+    for (;;) {
+      int rc = enqueue_split_round(ctx, R, cur, (int)(round % kRing), ring[round % kRing], false);
+      if (rc != BKT_OK) return rc;
+      cur ^= 1;
+      ++round;
+      if (round >= kRing - 1) {
+        const int chk = (int)((round - (kRing - 1)) % kRing);
+        CU(cudaEventSynchronize(ring[chk]));
+        if (ctx->h_ctl[chk].active == 0) break;
+        if (R.finish_at >= 0 && ctx->h_ctl[chk].active <= R.finish_at) {
+          // the list just advanced (work[cur ^ 1], ctl->active entries) holds every
+          // query still active, each with its next leaf set: finish in one launch
+          rc = launch_finisher(ctx, R, ctx->work[cur ^ 1]);
+          if (rc != BKT_OK) return rc;
+          break;
+        }
       }
+    }
+    return BKT_OK;
+  }
+  static_assert(kGraphRounds % 2 == 0, "a group must return the work lists to their parity");
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const long long launches0 = R.launches;
+  CU(configure_split_kernels(R.fma, R.kb, ctx->h, ctx->d));
+  CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = BKT_OK;
+  for (int g = 0; g < kGraphRounds && rc == BKT_OK; ++g)
+    rc = enqueue_split_round(ctx, R, cur ^ (g & 1), (int)((round + g) % kMirror), nullptr, true);
+  cudaError_t ec = cudaStreamEndCapture(ctx->stream, &graph);
+  if (rc != BKT_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  CU(ec);
+  const long long per_group = R.launches - launches0;
+  R.launches = launches0;
+  ec = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CU(ec);
+  struct ExecGuard {
+    cudaGraphExec_t e;
+    ~ExecGuard() { if (e) cudaGraphExecDestroy(e); }
+  } guard{exec};
+  cudaEvent_t* gev = ctx->group_ev;
+  for (long long j = 0;; ++j) {
+    CU(cudaGraphLaunch(exec, ctx->stream));
+    CU(cudaEventRecord(gev[j & 1], ctx->stream));
+    R.launches += per_group;
+    R.leafscan_launches += kGraphRounds;
+    round += kGraphRounds;
+    if (j == 0) continue;
+    // group j-1 done (group j in flight): its last round's control block
+    CU(cudaEventSynchronize(gev[(j - 1) & 1]));
+    const RoundCtl& c = ctx->h_ctl[(round - kGraphRounds - 1) % kMirror];
+    if (c.active == 0) break;
+    if (R.finish_at >= 0 && c.active <= R.finish_at) {
+      CU(cudaEventSynchronize(gev[j & 1]));
+      rc = launch_finisher(ctx, R, ctx->work[cur ^ 1]);
+      if (rc != BKT_OK) return rc;
+      break;
     }
   }
   return BKT_OK;
@@ -1728,6 +1800,12 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
             R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
+  // graph mode (opt-in, BKT_GRAPH=1): measured slower than eager launches on
+  // config 1 (3.9 vs 5.0 M q/s: its rounds are bound by the kernels' own
+  // fixed costs, not by host launch overhead); per-launch leaf-scan timing is
+  // not recorded in this mode
+  R.graph = R.split && std::getenv("BKT_GRAPH") && std::atoi(std::getenv("BKT_GRAPH")) != 0 &&
+            !std::getenv("BKT_SPLIT_DEBUG");
   R.renumber = ctx->residency == 0 && !R.wide && !std::getenv("BKT_EARLY_DRAIN");
   R.verbose = std::getenv("BKT_VERBOSE") != nullptr;
   if (const char* e = std::getenv("BKT_RENUMBER")) R.renumber = R.renumber && std::atoi(e) != 0;

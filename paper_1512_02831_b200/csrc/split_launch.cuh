@@ -8,7 +8,7 @@
 namespace bkt {
 
 template <bool FMA>
-inline cudaError_t launch_splitscan_one(int grid, cudaStream_t s, const SplitScanArgs& a) {
+inline cudaError_t launch_splitscan_one(int grid, cudaStream_t s, const SplitScanArgs& a, bool configure_only = false) {
   auto fn = splitscan_tc_kernel<FMA>;
   static std::atomic<unsigned long long> configured{0};
   int dev = 0;
@@ -22,8 +22,28 @@ inline cudaError_t launch_splitscan_one(int grid, cudaStream_t s, const SplitSca
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit, std::memory_order_release);
   }
+  if (configure_only) return cudaSuccess;
   fn<<<grid, kSplitThreads, SplitSmem::kBytes, s>>>(a);
   return cudaGetLastError();
+}
+
+// kernel attributes of the split rounds' kernels, set outside any stream capture
+inline cudaError_t configure_split_kernels(bool fma, int kb, int h, int d) {
+  SplitScanArgs dummy{};
+  cudaError_t e = fma ? launch_splitscan_one<true>(0, nullptr, dummy, true)
+                      : launch_splitscan_one<false>(0, nullptr, dummy, true);
+  if (e != cudaSuccess) return e;
+  const int smem = advance_smem_bytes(h, d);
+  if (smem <= 48 * 1024) return cudaSuccess;
+  switch (kb) {
+#define BKT_CASE(KB) \
+  case KB:           \
+    return cudaFuncSetAttribute(advance_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    BKT_KB_LIST(BKT_CASE)
+#undef BKT_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 inline cudaError_t launch_splitscan(bool fma, int grid, cudaStream_t s, const SplitScanArgs& a) {

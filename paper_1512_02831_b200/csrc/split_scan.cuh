@@ -425,22 +425,25 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
         uint32_t va[32], vb[32];
         float gmn[4];
         const float kInf = __int_as_float(0x7f800000);
+        // all four groups unconditionally (columns past a short chunk hold an
+        // earlier chunk's values and are masked below), each load issued
+        // while the previous group's minimum is computed
         tmem_ld32_async(tbase, va);
-        if (ngrp > 1) tmem_ld32_async(tbase + 32, vb);
+        tmem_ld32_async(tbase + 32, vb);
         tmem_wait(va);
         tmem_touch(vb);
         gmn[0] = min32(va);
-        gmn[1] = ngrp > 1 ? min32(vb) : kInf;
-        if (ngrp > 2) {
-          tmem_ld32_async(tbase + 64, va);
-          if (ngrp > 3) tmem_ld32_async(tbase + 96, vb);
-          tmem_wait(va);
-          tmem_touch(vb);
-          gmn[2] = min32(va);
-          gmn[3] = ngrp > 3 ? min32(vb) : kInf;
-        } else {
-          gmn[2] = kInf;
+        tmem_ld32_async(tbase + 64, va);
+        gmn[1] = min32(vb);
+        tmem_ld32_async(tbase + 96, vb);
+        tmem_wait(va);
+        tmem_touch(vb);
+        gmn[2] = min32(va);
+        gmn[3] = min32(vb);
+        if (ngrp < 4) {
           gmn[3] = kInf;
+          if (ngrp < 3) gmn[2] = kInf;
+          if (ngrp < 2) gmn[1] = kInf;
         }
         const float mchunk = fminf(fminf(gmn[0], gmn[1]), fminf(gmn[2], gmn[3]));
         if (__any_sync(0xffffffffu, valid && !(mchunk > thr))) {
@@ -523,26 +526,39 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
   const int n = a.ctl->active;
   const int d = a.top.d;
   const int k = a.k;
+  const int NW = a.NW;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int qi = __ldg(a.list + i);
-    // 1. merge this visit's candidates (one list per window) into the top-k row
-    // (a query the rescan handled has its counts zeroed: its row and kth are final)
+    // every per-query input is loaded before the first store (the stores could
+    // alias them), so the loads' latencies overlap instead of chaining
+    uint8_t* cc = a.ccnt + (long long)qi * NW;
+    auto counts8 = [&](int w0) {
+      // eight windows' counts per load when the rows are 8-byte aligned
+      uint64_t word = 0;
+      if ((NW & 7) == 0) {
+        word = *reinterpret_cast<const uint64_t*>(cc + w0);
+      } else {
+        for (int w = w0; w < min(NW, w0 + 8); ++w) word |= (uint64_t)cc[w] << (8 * (w - w0));
+      }
+      return word;
+    };
     float kth = a.kthv[qi];
+    const uint32_t st = a.state[qi];
+    const uint32_t vis0 = a.visits[qi];
+    const uint64_t word0 = counts8(0);
+    float qv[kSplitMaxD];
+    const float* qp = a.q + (long long)qi * a.D;
+#pragma unroll
+    for (int j = 0; j < kSplitMaxD; ++j) qv[j] = j < d ? __ldg(qp + j) : 0.0f;
+    // 1. merge this visit's candidates (one list per window) into the top-k row
+    //    (a query the rescan handled has its counts zeroed: its row and kth are final)
     {
       // register top-k (descending, sentinel-padded: leafscan.cuh merge_queue)
       uint64_t arr[KB];
       bool loaded = false;
       uint64_t* row = a.keys + (long long)qi * k;
-      const int NW = a.NW;
-      uint8_t* cc = a.ccnt + (long long)qi * NW;
       for (int w0 = 0; w0 < NW; w0 += 8) {
-        // eight windows' counts per load when the rows are 8-byte aligned
-        uint64_t word = 0;
-        if ((NW & 7) == 0) {
-          word = *reinterpret_cast<const uint64_t*>(cc + w0);
-        } else {
-          for (int w = w0; w < min(NW, w0 + 8); ++w) word |= (uint64_t)cc[w] << (8 * (w - w0));
-        }
+        const uint64_t word = w0 == 0 ? word0 : counts8(w0);
         if (word == 0) continue;
         if ((NW & 7) == 0) {
           *reinterpret_cast<uint64_t*>(cc + w0) = 0ull;
@@ -557,10 +573,22 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
         for (int b = 0; b < 8; ++b) {
           const int nc = min((int)((word >> (8 * b)) & 0xFF), a.capw);
           if (nc == 0) continue;
-          const uint64_t* cp = a.cand + ((long long)qi * NW + w0 + b) * a.capw;
-          for (int e = 0; e < nc; ++e) {
-            const uint64_t c = cp[e];
-            if (c < arr[0]) topk_insert<KB>(arr, c);
+          // the window's list in batches of eight keys (16-byte loads), then the inserts
+          const ulonglong2* cp2 =
+              reinterpret_cast<const ulonglong2*>(a.cand + ((long long)qi * NW + w0 + b) * a.capw);
+          for (int e0 = 0; e0 < nc; e0 += 8) {
+            uint64_t cb[8];
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              if (e0 + 2 * e2 < nc) {
+                const ulonglong2 v = cp2[e0 / 2 + e2];
+                cb[2 * e2] = v.x;
+                cb[2 * e2 + 1] = v.y;
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (e0 + e < nc && cb[e] < arr[0]) topk_insert<KB>(arr, cb[e]);
           }
         }
       }
@@ -573,15 +601,10 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
       }
     }
     // 2. FindLeaf with the new k-th distance
-    float qv[kSplitMaxD];
-    const float* qp = a.q + (long long)qi * a.D;
 #pragma unroll
-    for (int j = 0; j < kSplitMaxD; ++j) {
-      qv[j] = j < d ? __ldg(qp + j) : 0.0f;
+    for (int j = 0; j < kSplitMaxD; ++j)
       if (j < d) myq[j * kAdvThreads] = qv[j];
-    }
     auto qget = [myq](int j) { return myq[j * kAdvThreads]; };
-    const uint32_t st = a.state[qi];
     uint32_t lf = st & 0xFFFFu, pend = st >> 16;
     int nxt;
     if (ntree)
@@ -592,7 +615,7 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
     a.next[qi] = nxt;
     int rk = 0;
     if (nxt >= 0) {
-      const uint32_t vis = a.visits[qi] + 1;
+      const uint32_t vis = vis0 + 1;
       a.visits[qi] = vis;
       if (a.seq_log) {
         const unsigned long long p = atomicAdd(a.seq_pos, 1ull);
@@ -666,7 +689,7 @@ struct RouteArgs {
 
 // pass 1: masks, per-key counts, each route tile's base slot per window; pairs
 __global__ void __launch_bounds__(kRouteThreads) route_kernel(const RouteArgs a) {
-  __shared__ float s_box[kMaxWin * 2 * 32];
+  __shared__ uint64_t s_box[kMaxWin * kSplitMaxD];  // per window, per dimension f32x2 {lo, -hi}
   __shared__ int s_cnt[kMaxWin];
   const int nt = a.ctl->num_tiles;
   const int d = a.d;
@@ -675,26 +698,32 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const RouteArgs a)
     const int leaf = rt.x;
     const int w0 = __ldg(a.win_base + leaf), nw = __ldg(a.win_base + leaf + 1) - w0;
     __syncthreads();  // previous tile's shared state consumed
-    for (int e = threadIdx.x; e < nw * 2 * d; e += blockDim.x) s_box[e] = __ldg(a.win_box + (long long)w0 * 2 * d + e);
+    const uint64_t* gbox = reinterpret_cast<const uint64_t*>(a.win_box) + (long long)w0 * d;
+    for (int e = threadIdx.x; e < nw * d; e += blockDim.x) s_box[e] = __ldg(gbox + e);
     for (int e = threadIdx.x; e < kMaxWin; e += blockDim.x) s_cnt[e] = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < rt.z; r += blockDim.x) {
       const int p = rt.y + r;
       const int qi = __ldg(a.work + p);
       const float kth = __ldg(a.kthv + qi);
-      float qv[kSplitMaxD];
+      // {q_j, -q_j}: one packed subtraction per dimension gives {lo - q, q - hi}
+      uint64_t qq[kSplitMaxD];
       const float* qp = a.q + (long long)qi * a.D;
 #pragma unroll
-      for (int j = 0; j < kSplitMaxD; ++j) qv[j] = j < d ? __ldg(qp + j) : 0.0f;
+      for (int j = 0; j < kSplitMaxD; ++j) {
+        const float v = j < d ? __ldg(qp + j) : 0.0f;
+        qq[j] = ((uint64_t)__float_as_uint(-v) << 32) | __float_as_uint(v);
+      }
       unsigned long long mask = 0;
       for (int w = 0; w < nw; ++w) {
         // box lower bound in f32, relaxed by 1e-5: never above the reference distance
-        const float* bx = s_box + w * 2 * d;
+        const uint64_t* bx = s_box + w * d;
         float lb = 0.0f;
 #pragma unroll
         for (int j = 0; j < kSplitMaxD; ++j) {
           if (j < d) {
-            const float e = fmaxf(fmaxf(bx[j] - qv[j], qv[j] - bx[d + j]), 0.0f);
+            const uint64_t df = f2_sub(bx[j], qq[j]);
+            const float e = fmaxf(fmaxf(f2_lo(df), f2_hi(df)), 0.0f);
             lb = __fmaf_rn(e, e, lb);
           }
         }

@@ -101,7 +101,11 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
 
 /* k-NN search of m queries (replaces lazy_search, buffer_tree.py:523-646).
  * out_keys: (m, k) uint64 ascending packed keys (f32 bits << 32 | index),
- * exactly NeighborBatch.keys (core.py:230-262). */
+ * exactly NeighborBatch.keys (core.py:230-262).  Domain: the reference's --
+ * any 1 <= k <= n (core.py:92-102), any d, any height with 2^h <= n up to
+ * h = 30 (buffer_tree.py:159-163).  k > 64, d > 32 or h > 16 run on the
+ * general-domain path (one CTA per query, wide_search.cuh) with the same
+ * results, visit counts and leaf sequences. */
 int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t k, const bkt_search_opts* opts,
                uint64_t* out_keys, bkt_stats* stats);
 

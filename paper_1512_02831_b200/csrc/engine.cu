@@ -186,6 +186,7 @@ struct bkt_ctx {
   int* ovflag = nullptr;                 // m
   int* ovf = nullptr;                    // m
   unsigned long long* qmask = nullptr;   // m
+  int4* qs = nullptr;                    // m: split_state records {kth, state, visits, next}
   int* cbase = nullptr;                  // route tiles x split_NW
   int* items = nullptr;                  // m x split_NW
   int* stoff = nullptr;                  // nl * split_NW + 1
@@ -304,6 +305,7 @@ void free_work(bkt_ctx* c) {
   dfree(c->q_alt); dfree(c->q_raw_alt); dfree(c->keys_alt);
   c->cap_alt = 0; c->cap_alt_k = 0;
   dfree(c->arow); dfree(c->ccnt); dfree(c->cand); dfree(c->ovflag); dfree(c->ovf); dfree(c->qmask); dfree(c->cbase);
+  dfree(c->qs);
   dfree(c->items); dfree(c->stoff); dfree(c->stiles);
   c->split_cap = 0; c->stiles_cap = 0;
   dfree(c->perm); dfree(c->q_perm); dfree(c->keys_tmp); dfree(c->visits_tmp);
@@ -325,13 +327,14 @@ int ensure_perm(bkt_ctx* ctx, long long m, int k) {
 
 // per-query bytes of the split-round buffers
 long long split_bytes_per_query(const bkt_ctx* c) {
-  return 4ll * kSplitKT + (1ll + 8ll * split_capw(c->split_NW)) * c->split_NW + 4 + 4 + 8 + 4ll * c->split_NW +
+  return 4ll * kSplitKT + (1ll + 8ll * split_capw(c->split_NW)) * c->split_NW + 4 + 4 + 8 + 16 + 4ll * c->split_NW +
          16ll * c->split_NW / kNT + 16;
 }
 
 int ensure_split(bkt_ctx* ctx, long long m) {
   if (ctx->split_cap >= m) return BKT_OK;
   dfree(ctx->arow); dfree(ctx->ccnt); dfree(ctx->cand); dfree(ctx->ovflag); dfree(ctx->ovf); dfree(ctx->qmask); dfree(ctx->cbase);
+  dfree(ctx->qs);
   dfree(ctx->items); dfree(ctx->stoff); dfree(ctx->stiles);
   const long long M = std::max<long long>(m, 1);
   const long long NW = ctx->split_NW;
@@ -343,6 +346,7 @@ int ensure_split(bkt_ctx* ctx, long long m) {
   CU(cudaMemset(ctx->ovflag, 0, sizeof(int) * M));
   CU(cudaMalloc(&ctx->ovf, sizeof(int) * M));
   CU(cudaMalloc(&ctx->qmask, sizeof(unsigned long long) * M));
+  CU(cudaMalloc(&ctx->qs, sizeof(int4) * M));
   CU(cudaMalloc(&ctx->cbase, sizeof(int) * (M / kRouteQ + ctx->nl + 1) * NW));
   CU(cudaMalloc(&ctx->items, sizeof(int) * M * NW));
   CU(cudaMalloc(&ctx->stoff, sizeof(int) * ((long long)ctx->nl * NW + 1)));
@@ -1310,10 +1314,7 @@ int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
   a.k = R.k;
   a.top = TopTreeView{ctx->split, ctx->h, ctx->d};
   a.keys = ctx->keys;
-  a.kthv = ctx->kthv;
-  a.state = ctx->state;
-  a.next = ctx->next;
-  a.visits = ctx->visits;
+  a.qs = ctx->qs;
   a.ccnt = ctx->ccnt;
   a.cand = ctx->cand;
   a.NW = ctx->split_NW;
@@ -1354,7 +1355,7 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
     ra.work = ctx->work[cur];
     ra.rtiles = ctx->tiles;
     ra.ctl = ctx->ctl;
-    ra.kthv = ctx->kthv;
+    ra.qs = ctx->qs;
     ra.q = ctx->q;
     ra.D = ctx->D;
     ra.d = ctx->d;
@@ -1440,7 +1441,7 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
     R.launches++;
     R.leafscan_launches++;
     CU(launch_rescan(R.fma, ctx->sm_count * 4, ctx->stream, ctx->ovf, ctx->ctl, ctx->q, ctx->D, R.k, ctx->d,
-                     ctx->keys, ctx->kthv, ctx->next, ctx->pts, ctx->pidx, ctx->quad_base, ctx->ccnt,
+                     ctx->keys, ctx->qs, ctx->pts, ctx->pidx, ctx->quad_base, ctx->ccnt,
                      ctx->split_NW, ctx->ovflag));
     R.launches++;
     return launch_advance_round(ctx, R, ctx->work[cur]);
@@ -1457,7 +1458,7 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
 // captured once into a CUDA graph and replayed, one graph launch per group
 // instead of eight kernel launches per round; the host checks the last
 // round of the previous group (mirror slots: 2 x kGraphRounds).
-int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
+int split_rounds_loop(bkt_ctx* ctx, SearchRun& R, int cur, long long round, const int** fin) {
   cudaEvent_t* ring = ctx->ring_ev;
   if (!R.graph) {
     for (;;) {
@@ -1472,8 +1473,7 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
         if (R.finish_at >= 0 && ctx->h_ctl[chk].active <= R.finish_at) {
           // the list just advanced (work[cur ^ 1], ctl->active entries) holds every
           // query still active, each with its next leaf set: finish in one launch
-          rc = launch_finisher(ctx, R, ctx->work[cur ^ 1]);
-          if (rc != BKT_OK) return rc;
+          *fin = ctx->work[cur ^ 1];
           break;
         }
       }
@@ -1517,13 +1517,30 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
     const RoundCtl& c = ctx->h_ctl[(round - kGraphRounds - 1) % kMirror];
     if (c.active == 0) break;
     if (R.finish_at >= 0 && c.active <= R.finish_at) {
-      CU(cudaEventSynchronize(gev[j & 1]));
-      rc = launch_finisher(ctx, R, ctx->work[cur ^ 1]);
-      if (rc != BKT_OK) return rc;
+      *fin = ctx->work[cur ^ 1];
       break;
     }
   }
   return BKT_OK;
+}
+
+// The split rounds on the packed per-query records, then (when the tail is
+// handed over) the finisher on the unpacked arrays.  On entry work[cur]
+// holds the queries the home round scanned.
+int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
+  split_state_pack<<<R.grid_small, 256, 0, ctx->stream>>>(R.m, ctx->kthv, ctx->state, ctx->visits, ctx->next, ctx->qs);
+  CU(cudaGetLastError());
+  R.launches++;
+  int rc = launch_advance_round(ctx, R, ctx->work[cur]);
+  if (rc != BKT_OK) return rc;
+  const int* fin = nullptr;
+  rc = split_rounds_loop(ctx, R, cur ^ 1, round, &fin);
+  if (rc != BKT_OK) return rc;
+  split_state_unpack<<<R.grid_small, 256, 0, ctx->stream>>>(R.m, ctx->qs, ctx->kthv, ctx->state, ctx->visits,
+                                                            ctx->next);
+  CU(cudaGetLastError());
+  R.launches++;
+  return fin ? launch_finisher(ctx, R, fin) : BKT_OK;
 }
 
 int search_batch_impl(bkt_ctx* ctx, SearchRun& R);
@@ -1679,11 +1696,9 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
       int rc = launch_scan(ctx, R, a);
       if (rc != BKT_OK) return rc;
       if (to_split) {
-        // this round's rows and kth are final: FindLeaf, next-leaf buckets and
-        // A rows (advance), then the split rounds
-        rc = launch_advance_round(ctx, R, ctx->work[cur]);
-        if (rc != BKT_OK) return rc;
-        rc = split_rounds(ctx, R, cur ^ 1, round + 1);
+        // this round's rows and kth are final: the split rounds start with
+        // its queries' advance (FindLeaf, next-leaf buckets, A rows)
+        rc = split_rounds(ctx, R, cur, round + 1);
         if (rc != BKT_OK) return rc;
         break;
       }

@@ -89,13 +89,13 @@ inline cudaError_t launch_place(int grid, cudaStream_t s, const RouteArgs& a) {
 }
 
 inline cudaError_t launch_rescan(bool fma, int grid, cudaStream_t s, const int* ovf, const RoundCtl* ctl, const float* q,
-                          int D, int k, int d, uint64_t* keys, float* kthv, const int* next, const float* pts,
+                          int D, int k, int d, uint64_t* keys, int4* qs, const float* pts,
                           const uint32_t* pidx, const long long* quad_base, uint8_t* ccnt, int NW, int* ovflag) {
   if (fma)
-    rescan_kernel<true><<<grid, kFinishWarps * 32, 0, s>>>(ovf, ctl, q, D, k, d, keys, kthv, next, pts, pidx,
+    rescan_kernel<true><<<grid, kFinishWarps * 32, 0, s>>>(ovf, ctl, q, D, k, d, keys, qs, pts, pidx,
                                                            quad_base, ccnt, NW, ovflag);
   else
-    rescan_kernel<false><<<grid, kFinishWarps * 32, 0, s>>>(ovf, ctl, q, D, k, d, keys, kthv, next, pts, pidx,
+    rescan_kernel<false><<<grid, kFinishWarps * 32, 0, s>>>(ovf, ctl, q, D, k, d, keys, qs, pts, pidx,
                                                             quad_base, ccnt, NW, ovflag);
   return cudaGetLastError();
 }

@@ -50,6 +50,9 @@
 
 namespace bkt {
 
+#ifndef BKT_SPLIT_PREFETCH
+#define BKT_SPLIT_PREFETCH 0
+#endif
 #ifndef BKT_SPLIT_QEAGER
 #define BKT_SPLIT_QEAGER 1
 #endif
@@ -219,6 +222,19 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
           w.cb = rec_c.w * A.W;
           w.ce = min(nch, w.cb + A.W);
           s_win[ab] = w;
+#if BKT_SPLIT_PREFETCH
+          if (rec_c.z >= 0) {
+            // the window's chunks into L2 now: their TMA loads are issued only
+            // when this tile's A rows have landed, kAhead tiles later, and a
+            // load from HBM (~2,700 cycles issue to full) otherwise stalls
+            // the MMA at every tile start
+            const long long row = r0_c + (long long)w.cb * 128;
+            const uint32_t nr = (uint32_t)(dmin_ll(r1_c, r0_c + (long long)w.ce * 128) - row);
+            prefetch_l2(A.B + row * KT, nr * KT * 4);
+            prefetch_l2(A.ridx + row, nr * 4);
+            prefetch_l2(A.rows + row * d, nr * d * 4);
+          }
+#endif
         }
         float* abuf = sA + ab * (S::kA / 4);
 #pragma unroll
@@ -486,6 +502,31 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
 }
 
 // ---------------------------------------------------------------------------
+// per-query records of the split rounds: the traversal state the round
+// kernels read and write per query in one 16-byte record (one sector)
+// instead of four scattered arrays; packed when the split rounds start and
+// unpacked when they end (the home round, finishers and the result path use
+// the arrays)
+// ---------------------------------------------------------------------------
+__global__ void split_state_pack(long long m, const float* __restrict__ kthv, const uint32_t* __restrict__ state,
+                                 const uint32_t* __restrict__ visits, const int* __restrict__ next,
+                                 int4* __restrict__ qs) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    qs[i] = make_int4(__float_as_int(kthv[i]), (int)state[i], (int)visits[i], next[i]);
+}
+__global__ void split_state_unpack(long long m, const int4* __restrict__ qs, float* __restrict__ kthv,
+                                   uint32_t* __restrict__ state, uint32_t* __restrict__ visits,
+                                   int* __restrict__ next) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+    const int4 r = qs[i];
+    kthv[i] = __int_as_float(r.x);
+    state[i] = (uint32_t)r.y;
+    visits[i] = (uint32_t)r.z;
+    next[i] = r.w;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // advance: merge -> FindLeaf -> route (one thread per query of the list)
 // ---------------------------------------------------------------------------
 struct AdvanceArgs {
@@ -498,10 +539,7 @@ struct AdvanceArgs {
   int k;
   TopTreeView top;
   uint64_t* keys;
-  float* kthv;
-  uint32_t* state;
-  int* next;
-  uint32_t* visits;
+  int4* qs;                  // per query {kth bits, traversal state, visits, next leaf} (split_state)
   uint8_t* ccnt;             // m x NW candidates of the round per window (all zero after the home round)
   const uint64_t* cand;      // m x NW x capw
   int NW, capw;
@@ -542,9 +580,10 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
       }
       return word;
     };
-    float kth = a.kthv[qi];
-    const uint32_t st = a.state[qi];
-    const uint32_t vis0 = a.visits[qi];
+    const int4 rec = a.qs[qi];  // one 16-byte record: kth, state, visits (next is rewritten)
+    float kth = __int_as_float(rec.x);
+    const uint32_t st = (uint32_t)rec.y;
+    const uint32_t vis0 = (uint32_t)rec.z;
     const uint64_t word0 = counts8(0);
     float qv[kSplitMaxD];
     const float* qp = a.q + (long long)qi * a.D;
@@ -597,7 +636,6 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
         for (int j = 0; j < KB; ++j)
           if (j < k) row[k - 1 - j] = arr[j];
         kth = key_dist(arr[0]);
-        a.kthv[qi] = kth;
       }
     }
     // 2. FindLeaf with the new k-th distance
@@ -611,12 +649,10 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
       nxt = find_next_leaf_with(a.top.h, d, [s_split](uint32_t node) { return s_split[node]; }, qget, kth, lf, pend);
     else
       nxt = find_next_leaf(a.top, qget, kth, lf, pend);
-    a.state[qi] = (pend << 16) | lf;
-    a.next[qi] = nxt;
     int rk = 0;
+    const uint32_t vis = nxt >= 0 ? vis0 + 1 : vis0;
+    a.qs[qi] = make_int4(__float_as_int(kth), (int)((pend << 16) | lf), (int)vis, nxt);
     if (nxt >= 0) {
-      const uint32_t vis = vis0 + 1;
-      a.visits[qi] = vis;
       if (a.seq_log) {
         const unsigned long long p = atomicAdd(a.seq_pos, 1ull);
         if ((long long)p < a.seq_cap) {
@@ -667,7 +703,7 @@ struct RouteArgs {
   const int* work;           // this round's queries, bucketed by leaf
   const int4* rtiles;        // route tiles {leaf, first, count, -}
   const RoundCtl* ctl;       // num_tiles = route tiles
-  const float* kthv;
+  const int4* qs;            // split_state records (kth in .x)
   const float* q;
   int D;
   int d;
@@ -705,7 +741,7 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const RouteArgs a)
     for (int r = threadIdx.x; r < rt.z; r += blockDim.x) {
       const int p = rt.y + r;
       const int qi = __ldg(a.work + p);
-      const float kth = __ldg(a.kthv + qi);
+      const float kth = __int_as_float(__ldg(reinterpret_cast<const int*>(a.qs + qi)));
       // {q_j, -q_j}: one packed subtraction per dimension gives {lo - q, q - hi}
       uint64_t qq[kSplitMaxD];
       const float* qp = a.q + (long long)qi * a.D;
@@ -825,7 +861,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_split_kernel(int* __restric
 template <bool FMA>
 __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
     const int* __restrict__ ovf, const RoundCtl* ctl, const float* __restrict__ q, int D, int k, int d,
-    uint64_t* __restrict__ keys, float* __restrict__ kthv, const int* __restrict__ next,
+    uint64_t* __restrict__ keys, int4* __restrict__ qs,
     const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base,
     uint8_t* __restrict__ ccnt, int NW, int* __restrict__ ovflag) {
   __shared__ uint64_t s_row[kFinishWarps][64];
@@ -834,7 +870,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
   const int n = ctl->novf;
   for (int i = blockIdx.x * kFinishWarps + wl; i < n; i += gridDim.x * kFinishWarps) {
     const int qi = __ldg(ovf + i);
-    const int leaf = next[qi];
+    const int leaf = qs[qi].w;
     // the row and kth become final here: advance_kernel merges nothing for this visit
     for (int w = lane; w < NW; w += 32) ccnt[(long long)qi * NW + w] = 0;
     if (lane == 0) ovflag[qi] = 0;
@@ -888,7 +924,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
       }
     }
     for (int j = lane; j < k; j += 32) kp[j] = row[j];
-    if (lane == 0) kthv[qi] = key_dist(row[k - 1]);
+    if (lane == 0) reinterpret_cast<int*>(qs + qi)[0] = __float_as_int(key_dist(row[k - 1]));
     __syncwarp();
   }
 }

@@ -1,13 +1,18 @@
 """Exact brute-force k-NN on the B200 (the paper's brute baseline and the
 tree engine's cross-check), API of the reference's brute.py:41-113.
 
-Both entry points run the leaf-scan kernel of libbkt.so over every
-(query, reference) pair through the device seam (``ChunkPipeline`` ->
-``GpuDevice.enqueue_brute_kernel`` -> ``bkt_scan_groups``): one chunk when the
-reference set fits the device, else the reference set streams through the
-two chunk buffers.  Results are bit-identical to the reference's numpy scan
-(same float32 distance order, same (distance, index) key order).  There is no
-CPU path.
+``brute_knn`` runs the engine's own leaf scans (the tensor-core filter with
+exact re-evaluation, or the CUDA-core scan) over every (query, reference)
+pair: the reference set becomes an *exhaustive* two-leaf structure whose
+root split value is NaN.  Every query then descends to one leaf (``q < NaN``
+is false: right) and visits the other as well (the slab test
+``(q - NaN)^2 > kth`` is false, so nothing is pruned) -- a full scan, with
+the best k of the union, i.e. brute force, bit-identical to the reference's
+numpy scan (same float32 distance order, same (distance, index) key order).
+``brute_knn_chunked`` (and ``brute_knn(num_chunks > 1)``) streams the
+reference set chunk by chunk through the device seam (``ChunkPipeline`` ->
+``GpuDevice.enqueue_brute_kernel`` -> ``bkt_scan_groups``), as the
+reference's chunked brute force does.  There is no CPU path.
 """
 from __future__ import annotations
 
@@ -15,9 +20,10 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .buffer_tree import BufferKdTree, LeafStructure, TopTree, lazy_search
 from .core import NeighborBatch, SearchParams, as_point_matrix
 
-__all__ = ["EvalCounter", "brute_knn", "brute_knn_chunked"]
+__all__ = ["EvalCounter", "brute_knn", "brute_knn_chunked", "exhaustive_tree"]
 
 
 @dataclass
@@ -74,7 +80,24 @@ def brute_knn(refs, queries, params: SearchParams, workers: int = 1, counter: Ev
     if m == 0:
         return NeighborBatch(0, params.k)
     dev = device if device is not None else default_device(0)
-    out = brute_knn_chunked(pm, q, params, dev, ChunkPlan.build(pm.n, num_chunks))
+    if num_chunks == 1 and pm.n >= 2:
+        out = lazy_search(exhaustive_tree(pm), q, params, device=dev)
+    else:
+        out = brute_knn_chunked(pm, q, params, dev, ChunkPlan.build(pm.n, num_chunks))
     if counter is not None:
         counter.pairs += m * pm.n
     return out
+
+
+def exhaustive_tree(refs) -> BufferKdTree:
+    """The reference set as a two-leaf structure (points in their original
+    order, split at n // 2) whose root split value is NaN: a search over it
+    visits both leaves for every query, so the engine's leaf scans compute
+    brute force."""
+    pm = as_point_matrix(refs)
+    if pm.n < 2:
+        raise ValueError("an exhaustive structure needs at least 2 points")
+    top = TopTree(1, pm.d, np.array([np.nan], np.float32), np.zeros(1, np.int32))
+    leaves = LeafStructure(np.ascontiguousarray(pm.data, dtype=np.float32), np.arange(pm.n, dtype=np.int64),
+                           np.array([0, pm.n // 2, pm.n], np.int64))
+    return BufferKdTree(top, leaves)

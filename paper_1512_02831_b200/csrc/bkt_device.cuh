@@ -101,10 +101,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
-// Bulk prefetch of [src, src + bytes) into L2 (16-byte aligned, bytes a multiple of 16).
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 // Blocks until the barrier's phase `phase` has completed.  The suspend-time
 // hint lets the hardware park the warp until the phase flips instead of
 // spinning (a spinning producer warp otherwise steals issue slots from the

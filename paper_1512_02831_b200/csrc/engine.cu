@@ -1426,8 +1426,10 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
       CU(cudaStreamSynchronize(ctx->stream));
       const long long b0 = h[5];
       for (int j = 0; j < kDbgCap && h[8 * j + 5]; ++j)
-        std::fprintf(stderr, "stile %d pub %lld ewait %lld eready %lld mready %lld\n", j, h[8 * j] - b0,
-                     h[8 * j + 5] - b0, h[8 * j + 6] ? h[8 * j + 6] - b0 : -1, h[8 * j + 7] ? h[8 * j + 7] - b0 : -1);
+        std::fprintf(stderr, "stile %d pub %lld ewait %lld eready %lld mready %lld esetup %lld eq %lld\n", j,
+                     h[8 * j] - b0, h[8 * j + 5] - b0, h[8 * j + 6] ? h[8 * j + 6] - b0 : -1,
+                     h[8 * j + 7] ? h[8 * j + 7] - b0 : -1, h[8 * j + 1] ? h[8 * j + 1] - b0 : -1,
+                     h[8 * j + 2] ? h[8 * j + 2] - b0 : -1);
       const long long* hc = h.data() + 8 * kDbgCap;
       for (int g = 0; g < kDbgCap && hc[8 * g + 4]; ++g)
         std::fprintf(stderr, "schunk %d tma %lld full %lld mma %lld ewait %lld eready %lld edone %lld\n", g,
@@ -1811,7 +1813,10 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // split rounds (split_scan.cuh): tensor-core path with the 16-column layout
   // (d <= 13), k <= 64 (the rescan's row) and leaves of >= k points (a finite
   // k-th distance after the home visit); BKT_SPLIT=0 keeps the leaf-level rounds
-  R.split = R.tc && !R.unfused && ctx->split_NW > 0 && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 &&
+  // Leaves of one window (NW = 1: < 5 chunks of 128 points) gain nothing
+  // from routing: config 1 (256-point leaves) runs 6.15 M q/s on leaf-level
+  // rounds against 4.06 M with split rounds.
+  R.split = R.tc && !R.unfused && ctx->split_NW > 1 && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 &&
             R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));

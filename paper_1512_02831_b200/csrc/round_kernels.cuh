@@ -238,11 +238,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
     }
     // the host's copy of this round's control block, written straight into
     // mapped page-locked memory (no copy-engine operation between the round's
-    // kernels); the host reads it after the round's event completes
-    if (mirror) {
-      *mirror = *ctl;
-      __threadfence_system();
-    }
+    // kernels); the host reads it after the round's event completes, which
+    // orders the kernel's writes before the read (no system-scope fence: a
+    // stale slot could only hold an older, larger active count, which delays
+    // a decision by one check and never ends a search early)
+    if (mirror) *mirror = *ctl;
   }
 }
 

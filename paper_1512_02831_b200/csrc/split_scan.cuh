@@ -50,9 +50,6 @@
 
 namespace bkt {
 
-#ifndef BKT_SPLIT_PREFETCH
-#define BKT_SPLIT_PREFETCH 0
-#endif
 #ifndef BKT_SPLIT_QEAGER
 #define BKT_SPLIT_QEAGER 1
 #endif
@@ -222,19 +219,6 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
           w.cb = rec_c.w * A.W;
           w.ce = min(nch, w.cb + A.W);
           s_win[ab] = w;
-#if BKT_SPLIT_PREFETCH
-          if (rec_c.z >= 0) {
-            // the window's chunks into L2 now: their TMA loads are issued only
-            // when this tile's A rows have landed, kAhead tiles later, and a
-            // load from HBM (~2,700 cycles issue to full) otherwise stalls
-            // the MMA at every tile start
-            const long long row = r0_c + (long long)w.cb * 128;
-            const uint32_t nr = (uint32_t)(dmin_ll(r1_c, r0_c + (long long)w.ce * 128) - row);
-            prefetch_l2(A.B + row * KT, nr * KT * 4);
-            prefetch_l2(A.ridx + row, nr * 4);
-            prefetch_l2(A.rows + row * d, nr * d * 4);
-          }
-#endif
         }
         float* abuf = sA + ab * (S::kA / 4);
 #pragma unroll
@@ -356,6 +340,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       __syncwarp();
       if (lane == 0) mbar_arrive(&aempty[ab]);
 
+      if (dbg_on && (int)j < A.dbg_cap) A.dbg[8 * j + 1] = clock64();
       const float qnc = (1.0f - kTcMargin) * qn;
       const bool force = valid && !(qn >= 1e-30f && qn <= 1e30f);
       // kth - (1 - C) qn, rounded up by a hair (leafscan_tc.cuh); forced rows pass everything
@@ -380,6 +365,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       }
       have_q = true;
 #endif
+      if (dbg_on && (int)j < A.dbg_cap) A.dbg[8 * j + 2] = clock64();
 
       auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
         uint32_t mask = 0;

@@ -163,6 +163,19 @@ class TestGpuBrute:
         assert np.array_equal(res.keys, O.brute_keys(refs, q, 9))
         assert counter.pairs == 3000 * 500
 
+    @pytest.mark.parametrize("d,k", [(10, 10), (10, 50), (3, 1), (40, 12), (10, 100)])
+    def test_brute_on_the_engine_scans(self, rng, gpu_device, d, k):
+        """brute_knn runs the engine's leaf scans over an exhaustive two-leaf
+        structure (tensor-core filter for d = 10, CUDA-core scan for d = 3,
+        the general-domain path for d = 40 / k = 100): bit-identical to the
+        oracle's brute force on a mixture with duplicated points."""
+        pts, _ = bkt.gen_mixture(60_000, d, seed=d + k)
+        refs = np.ascontiguousarray(pts.data[:50_000])
+        refs[1000:1100] = refs[:100]  # ties broken by index
+        q = np.ascontiguousarray(pts.data[50_000:])
+        res = bkt.brute_knn(refs, q, bkt.SearchParams(k=k), device=gpu_device)
+        assert np.array_equal(res.keys, O.brute_keys(refs, q, k, threads=O.default_threads()))
+
     def test_chunked_equals_single(self, rng, gpu_device):
         refs = rng.random((2501, 5), dtype=np.float32)
         q = rng.random((300, 5), dtype=np.float32)

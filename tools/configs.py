@@ -1,7 +1,7 @@
 """Measure BASELINE.json's configs beyond the headline (bench.py measures configs[1]).
 
     python tools/configs.py cfg1                 # uniform n=m=2^16, d=10, k=10, h=8 (+ reference digest)
-    python tools/configs.py cfg3 [--m 2e8]       # n=2M refs, query stream of m queries in 10M chunks
+    python tools/configs.py cfg3 [--m 1e9] [--gpus N]  # n=2M refs, stream of m queries in 10M chunks over N GPUs
     python tools/configs.py cfg4 [--m 10e6]      # d = 5 / 15 / 27 mixture, n=2M
     python tools/configs.py cfg5 [--m 1e6]       # n=8M host-resident leaf streaming, k in {1,10,50}, h in {8,11,14}
     python tools/configs.py uniform2m [--m 1e7]  # uniform data at the headline size (n=2M, d=10, k=10)
@@ -64,37 +64,70 @@ def _gen(args):
 
 
 def cfg3(a):
+    """Config 3: n=2M refs, a stream of m queries generated per 10M-query chunk
+    with the reference's recipe (gen_query_chunk: default_rng(1000 + c)),
+    spread over --gpus devices (one host thread per GPU pulling chunks from a
+    shared counter, tree replicated, no collective).  Each chunk goes through
+    the public API call (H2D, search, D2H); its index rows are hashed
+    (sha256) on the device thread and the run's digest is the sha256 of the
+    per-chunk digests in chunk order.  Host generation runs in a process pool
+    ahead of the devices; the first chunk's first rows are checked against the
+    CPU oracle."""
+    import threading
     n, m, chunk = 2_000_000, int(a.m), 10_000_000
     pts, _ = gen_mixture(n + 10_000_000, 10, seed=1)
-    refs = pts.data[:n]
+    refs = np.ascontiguousarray(pts.data[:n])
+    del pts
     tree = bkt.build_buffer_tree(refs, 9)
-    dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
-    dev.ensure_tree(tree)
+    ngpu = max(1, a.gpus)
+    devs = [bkt.device_init(bkt.DeviceSpec(cuda_device=i)) for i in range(ngpu)]
+    for dev in devs:
+        dev.ensure_tree(tree)
     nchunks = (m + chunk - 1) // chunk
-    h = hashlib.sha256()
-    first_q = first_k = None
-    t_search = 0.0
-    with ProcessPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        futs = [ex.submit(_gen, (c, min(chunk, m - c * chunk))) for c in range(min(nchunks, 10))]
+    digests = [None] * nchunks
+    first = {}
+    ahead = min(nchunks, 4 * ngpu + 4)
+    lock = threading.Lock()
+    nxt = [0]
+    busy = [0.0] * ngpu
+    with ProcessPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        futs = {c: ex.submit(_gen, (c, min(chunk, m - c * chunk))) for c in range(ahead)}
+
+        def drive(g):
+            dev = devs[g]
+            while True:
+                with lock:
+                    c = nxt[0]
+                    if c >= nchunks:
+                        return
+                    nxt[0] += 1
+                    f = futs.pop(c)
+                    if c + ahead < nchunks:
+                        futs[c + ahead] = ex.submit(_gen, (c + ahead, min(chunk, m - (c + ahead) * chunk)))
+                q = f.result()
+                s0 = time.perf_counter()
+                keys, st, _ = dev.search(q, 10)  # public API call: H2D, search, D2H
+                busy[g] += time.perf_counter() - s0
+                digests[c] = hashlib.sha256((keys & np.uint64(0xFFFFFFFF)).astype("<i8").tobytes()).digest()
+                if c == 0:
+                    first["q"], first["k"] = q[:2048].copy(), keys[:2048].copy()
+
         t0 = time.perf_counter()
-        done = 0
-        for c in range(nchunks):
-            q = futs[c].result()
-            if c + 10 < nchunks:
-                futs.append(ex.submit(_gen, (c + 10, min(chunk, m - (c + 10) * chunk))))
-            s0 = time.perf_counter()
-            keys, st, _ = dev.search(q, 10)  # public API call: H2D, search, D2H
-            t_search += time.perf_counter() - s0
-            h.update((keys & np.uint64(0xFFFFFFFF)).astype("<i8").tobytes())
-            if c == 0:
-                first_q, first_k = q, keys
-            done += q.shape[0]
+        th = [threading.Thread(target=drive, args=(g,)) for g in range(ngpu)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
         wall = time.perf_counter() - t0
-    ok = oracle_check(tree, first_q, first_k, 10)
+    ok = oracle_check(tree, first["q"], first["k"], 10)
     emit({"config": f"cfg3 stream: n=2M refs, m={m} queries in {nchunks} chunks of {chunk} (config-3 recipe, "
-                    f"default_rng(1000+c)), d=10, k=10, h=9, 1 GPU", "qps_search_api": done / t_search,
-          "qps_wall_incl_host_generation": done / wall, "digest_sha256": h.hexdigest(), "sample_rows_match_oracle": ok})
-    dev.close()
+                    f"default_rng(1000+c)), d=10, k=10, h=9, {ngpu} GPU(s), chunks pulled by one thread per GPU",
+          "qps_wall_incl_host_generation": m / wall, "qps_per_gpu_search_api": [round(m / ngpu / b) if b else None
+                                                                                for b in busy],
+          "wall_seconds": wall, "digest_of_chunk_digests": hashlib.sha256(b"".join(digests)).hexdigest(),
+          "sample_rows_match_oracle": ok})
+    for dev in devs:
+        dev.close()
 
 
 def cfg4(a):
@@ -138,13 +171,13 @@ def cfg5(a):
     n, m = 8_000_000, int(a.m)
     pts, _ = gen_mixture(n + m, 10, seed=1)
     refs, queries = pts.data[:n], pts.data[n:]
-    for h in (8, 11, 14):
+    for h in [int(x) for x in a.heights.split(",")]:
         tree = bkt.build_buffer_tree(refs, h)
-        for num_chunks in (1, 4):
+        for num_chunks in {"hbm": (1,), "host": (4,), "both": (1, 4)}[a.resident]:
             plan = bkt.ChunkPlan.build(n, num_chunks)
             dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
             dev.ensure_tree(tree, plan if num_chunks > 1 else None)
-            for k in (1, 10, 50):
+            for k in [int(x) for x in a.ks.split(",")]:
                 t0 = time.perf_counter()
                 keys, st, _ = dev.search(queries, k, timing=True)
                 wall = time.perf_counter() - t0
@@ -160,6 +193,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("which", choices=["cfg1", "cfg3", "cfg4", "cfg5", "uniform2m"])
     ap.add_argument("--m", type=float, default=None)
+    ap.add_argument("--gpus", type=int, default=1, help="cfg3: devices the stream is spread over")
+    ap.add_argument("--heights", default="8,11,14", help="cfg5: tree heights")
+    ap.add_argument("--ks", default="1,10,50", help="cfg5: k values")
+    ap.add_argument("--resident", default="both", choices=["hbm", "host", "both"], help="cfg5: leaf structure residency")
     a = ap.parse_args()
     if a.m is None:
         a.m = {"cfg1": 65536, "cfg3": 2e8, "cfg4": 10e6, "cfg5": 1e6, "uniform2m": 10e6}[a.which]

@@ -1,5 +1,9 @@
 """Randomised exactness sweep of the B200 engine against the CPU oracle.
 
+Covers the round engine (split rounds for leaves of >= 2 windows, leaf-level
+rounds, home-order renumbering for m >= 65,536) and the general-domain path
+(k > 64, d > 32, h > 16).
+
     python tools/fuzz_parity.py [--cases 200] [--seed 1] [--seconds 600]
 
 Each case draws n, m, d, k, h, a data family (uniform, Gaussian mixture with
@@ -61,17 +65,19 @@ def main():
     for case in range(a.cases):
         if time.time() - t0 > a.seconds:
             break
-        d = int(rng.choice([1, 2, 3, 5, 8, 9, 10, 11, 12, 15, 16, 20, 27, 31]))
-        n = int(rng.integers(300, 60_000))
+        d = int(rng.choice([1, 2, 3, 5, 8, 9, 10, 11, 12, 13, 15, 16, 20, 27, 31, 33, 40]))
+        n = int(rng.integers(300, 60_000)) if rng.random() < 0.8 else int(rng.integers(60_000, 400_000))
         h = int(rng.integers(1, max(2, min(12, int(np.log2(n)) - 2))))
-        k = int(min(n, rng.choice([1, 2, 5, 10, 16, 33, 50, 64])))
-        m = int(rng.integers(1, 6000))
+        if rng.random() < 0.05 and n >= (1 << 18):
+            h = int(rng.integers(17, int(np.log2(n))))  # general-domain path: h > 16
+        k = int(min(n, rng.choice([1, 2, 5, 10, 16, 33, 50, 64, 65, 100, 200])))
+        m = int(rng.integers(1, 6000)) if rng.random() < 0.85 else int(rng.integers(65_536, 150_000))
         fam, pts = draw(rng, n + m, d)
         refs, q = pts[:n], pts[n:]
         if rng.random() < 0.2:  # some queries exactly on reference points
             take = rng.integers(0, n, size=m // 3)
             q[: take.size] = refs[take]
-        kernel = str(rng.choice(["auto", "tc", "direct"])) if d <= 31 else "direct"
+        kernel = str(rng.choice(["auto", "tc", "direct"])) if d <= 31 and k <= 64 and h <= 16 else "auto"
         tree = bkt.build_buffer_tree(refs, h, device=0 if rng.random() < 0.5 else None)
         st = bkt.SearchStats()
         res = bkt.lazy_search(tree, q, bkt.SearchParams(k=k), device=dev, stats=st, kernel=kernel)

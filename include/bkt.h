@@ -61,6 +61,8 @@ typedef struct bkt_stats {
   double search_ms;         /* CUDA-event time of the whole device search             */
   double h2d_ms, d2h_ms;
   int64_t h2d_bytes, d2h_bytes;
+  int64_t stream_bytes;     /* host-resident leaf structure: bytes streamed H2D into the chunk slots */
+  int64_t stream_copies;    /* chunk copies issued (each a pinned -> device cudaMemcpyAsync pair)   */
 } bkt_stats;
 
 /* Context on one CUDA device (replaces device.py:361-364 device_init /

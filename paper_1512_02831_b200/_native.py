@@ -62,6 +62,8 @@ class Stats(ctypes.Structure):
         ("d2h_ms", ctypes.c_double),
         ("h2d_bytes", ctypes.c_int64),
         ("d2h_bytes", ctypes.c_int64),
+        ("stream_bytes", ctypes.c_int64),
+        ("stream_copies", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

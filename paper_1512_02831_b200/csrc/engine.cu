@@ -1047,6 +1047,8 @@ struct SearchRun {
   bool finish_cta = false;   // finisher with one CTA per query (else one warp per query)
   bool split = false;        // later rounds as (leaf, window) items (split_scan.cuh)
   bool graph = false;        // split rounds replayed from a captured CUDA graph (launch-bound searches)
+  long long stream_bytes = 0;   // out-of-core chunk streaming (bkt_stats.stream_bytes)
+  long long stream_copies = 0;
   bool wide = false;         // general-domain path (wide_search.cuh)
   bool wide_rows_smem = true;
   size_t wide_smem = 0;
@@ -1242,6 +1244,8 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
                     ctx->copy_stream);
     cudaEventRecord(ctx->slot_ready[s], ctx->copy_stream);
     ctx->slot_chunk[s] = j;
+    R.stream_bytes += (sizeof(float) * 4 * D + sizeof(uint32_t) * 4) * (b - a);
+    R.stream_copies += 1;
     return s;
   };
   std::vector<int> slot_of(need.size(), -1);
@@ -1856,6 +1860,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     // two CTAs per SM: the variants are sized for it (2 x 256 TMEM columns,
     // shared memory and registers); the occupancy query is only a sanity check
     int per_sm = (ctx->KT == 16) ? R.tc_cps : 2;
+    if (R.kb >= 32) per_sm = 1;  // register-heavy top-k variants (leafscan_tc.cuh launch bounds)
     if (occ < 1) return set_err(ctx, BKT_ECUDA, "tensor-core leaf kernel cannot be resident");
     if (const char* e = std::getenv("BKT_TC_CTAS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     if (std::getenv("BKT_VERBOSE")) std::fprintf(stderr, "tc kernel: occupancy %d CTAs/SM, grid %d\n", occ, per_sm * ctx->sm_count);
@@ -2177,6 +2182,8 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   st.leafscan_launches = R.leafscan_launches;
   st.leafscan_ms = R.leafscan_ms;
   st.search_ms = ms;
+  st.stream_bytes = R.stream_bytes;
+  st.stream_copies = R.stream_copies;
   if (stats) *stats = st;
   return BKT_OK;
 }

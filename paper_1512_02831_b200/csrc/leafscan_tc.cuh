@@ -268,7 +268,10 @@ template <int KT, int KB, bool FMA, int NR, int CPS>
 #ifndef BKT_TC_MINB
 #define BKT_TC_MINB CPS
 #endif
-__global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kernel(const TcArgs A) {
+// KB >= 32 (k > 16): the register top-k alone needs 64-128 registers, so
+// these variants run one CTA per SM with the full register file instead of
+// spilling at two (engine.cu launches them one per SM)
+__global__ void __launch_bounds__(tc_threads(CPS), (KB >= 32 ? 1 : BKT_TC_MINB)) leafscan_tc_kernel(const TcArgs A) {
   using S = TcSmem<KT, NR, CPS>;
   constexpr int kTcRows = NR;
   constexpr int kTcBufs = S::kBufs;
@@ -898,9 +901,12 @@ __global__ void __launch_bounds__(tc_threads(CPS), BKT_TC_MINB) leafscan_tc_kern
           mbar_wait(&full[s], (g / kTcStages) & 1u);
           load_qv();
           if (NR == 64) {
-            // both groups are still in registers
+            // both groups are still in registers.  Group 1 only when the chunk
+            // has it: with thr = +inf (no k-th distance yet, no bound) the
+            // masked minimum (+inf) would pass and its stale columns would be
+            // re-evaluated against stale stage rows (fuzz seed 11 case 68)
             if (__any_sync(0xffffffffu, !(gmn[0] > thr))) process(va, 0, s);
-            if (__any_sync(0xffffffffu, !(gmn[1] > thr))) process(vb, 32, s);
+            if (ngrp > 1 && __any_sync(0xffffffffu, !(gmn[1] > thr))) process(vb, 32, s);
           } else {
 #pragma unroll 1
             for (int gi = 0; gi < ngrp; ++gi) {

@@ -60,7 +60,8 @@ constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhe
 constexpr int kSplitStages = 5;  // TMA ring stages (128-row chunks)
 constexpr int kSplitThreads = 192;
 // candidates per (query, window) and round before the leaf is rescanned instead
-__host__ __device__ inline int split_capw(int NW) { return NW <= 8 ? 16 : (NW >= 32 ? 4 : 128 / NW); }
+// (even, so every slice starts 16-byte aligned for advance_kernel's paired loads)
+__host__ __device__ inline int split_capw(int NW) { return NW <= 8 ? 16 : (NW >= 32 ? 4 : (128 / NW) & ~1); }
 
 struct SplitScanArgs {
   const float* q;            // m x qstride original coordinates (survivor re-evaluation)
@@ -539,6 +540,59 @@ struct AdvanceArgs {
 constexpr int kAdvThreads = 256;
 __host__ __device__ inline int advance_smem_bytes(int h, int d) { return (start_tree_smem(h) + d * kAdvThreads) * 4; }
 
+// A top-k row of k <= 64 keys across a warp (lane j: row[j] in r0, row[32 + j]
+// in r1, ascending, ~0 past k).  Inserts cv (below the k-th key) at its rank
+// by a one-lane shift; returns the new k-th key.
+__device__ __forceinline__ uint64_t warp_row_insert(uint64_t& r0, uint64_t& r1, uint64_t cv, int k, int lane) {
+  const uint32_t full = 0xffffffffu;
+  const int p = __popc(__ballot_sync(full, r0 < cv)) + __popc(__ballot_sync(full, r1 < cv));
+  const uint64_t up0 = __shfl_up_sync(full, r0, 1), up1 = __shfl_up_sync(full, r1, 1);
+  const uint64_t last0 = __shfl_sync(full, r0, 31);
+  const uint64_t n1v = lane + 32 > p ? (lane == 0 ? last0 : up1) : (lane + 32 == p ? cv : r1);
+  r0 = lane > p ? up0 : (lane == p ? cv : r0);
+  r1 = n1v;
+  return k <= 32 ? __shfl_sync(full, r0, k - 1) : __shfl_sync(full, r1, k - 33);
+}
+
+// Warp-cooperative merge of one query's candidate lists into its top-k row
+// (k <= 64: lane j holds row[j] and row[32 + j]), used for k > 10 where a
+// per-thread register top-k (KB >= 16) spills.  Each candidate below the current k-th
+// key is inserted at its rank (two ballots) by a one-lane shift of the row;
+// the result is the best k of (row, candidates) -- the reference's
+// update_rows (core.py:251-262) in any insertion order.  Returns the new
+// k-th key; the counts are zeroed.
+__device__ __forceinline__ uint64_t warp_merge_query(uint64_t* __restrict__ row, int k, uint8_t* cc, int NW,
+                                                     const uint64_t* __restrict__ cand, int capw, int lane) {
+  const uint32_t full = 0xffffffffu;
+  uint64_t r0 = lane < k ? row[lane] : ~0ull;
+  uint64_t r1 = lane + 32 < k ? row[lane + 32] : ~0ull;
+  const int n0 = lane < NW ? cc[lane] : 0;
+  const int n1 = lane + 32 < NW ? cc[lane + 32] : 0;
+  uint64_t kk = k <= 32 ? __shfl_sync(full, r0, k - 1) : __shfl_sync(full, r1, k - 33);
+  for (int half = 0; half < 2; ++half) {
+    unsigned wm = __ballot_sync(full, (half ? n1 : n0) > 0);
+    while (wm) {
+      const int src = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const int w = src + 32 * half;
+      const int nc = min(__shfl_sync(full, half ? n1 : n0, src), capw);
+      const uint64_t c = lane < nc ? cand[(long long)w * capw + lane] : ~0ull;
+      unsigned todo = __ballot_sync(full, c < kk);
+      while (todo) {
+        const int e = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint64_t cv = __shfl_sync(full, c, e);
+        if (cv < kk) kk = warp_row_insert(r0, r1, cv, k, lane);  // (kk may have fallen meanwhile)
+      }
+    }
+  }
+  if (lane < k) row[lane] = r0;
+  if (lane + 32 < k) row[lane + 32] = r1;
+  if (lane < NW) cc[lane] = 0;
+  if (lane + 32 < NW) cc[lane + 32] = 0;
+  return kk;
+}
+
 template <int KB>
 __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceArgs a) {
   extern __shared__ float s_adv[];
@@ -551,8 +605,14 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
   const int d = a.top.d;
   const int k = a.k;
   const int NW = a.NW;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int qi = __ldg(a.list + i);
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  // whole warps per iteration (the k > 10 merge is cooperative); lane i of
+  // the warp owns list position base + i
+  for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n; base += nwarps * 32) {
+    const int i = base + lane;
+    const bool valid = i < n;
+    const int qi = valid ? __ldg(a.list + i) : 0;
     // every per-query input is loaded before the first store (the stores could
     // alias them), so the loads' latencies overlap instead of chaining
     uint8_t* cc = a.ccnt + (long long)qi * NW;
@@ -566,18 +626,30 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
       }
       return word;
     };
-    const int4 rec = a.qs[qi];  // one 16-byte record: kth, state, visits (next is rewritten)
+    const int4 rec = valid ? a.qs[qi] : make_int4(0, 0, 0, 0);  // one 16-byte record: kth, state, visits
     float kth = __int_as_float(rec.x);
     const uint32_t st = (uint32_t)rec.y;
     const uint32_t vis0 = (uint32_t)rec.z;
-    const uint64_t word0 = counts8(0);
+    const uint64_t word0 = valid ? counts8(0) : 0ull;
     float qv[kSplitMaxD];
     const float* qp = a.q + (long long)qi * a.D;
 #pragma unroll
-    for (int j = 0; j < kSplitMaxD; ++j) qv[j] = j < d ? __ldg(qp + j) : 0.0f;
+    for (int j = 0; j < kSplitMaxD; ++j) qv[j] = (valid && j < d) ? __ldg(qp + j) : 0.0f;
     // 1. merge this visit's candidates (one list per window) into the top-k row
     //    (a query the rescan handled has its counts zeroed: its row and kth are final)
-    {
+    if constexpr (KB >= 16) {
+      bool any = word0 != 0ull;
+      for (int w0 = 8; w0 < NW && valid && !any; w0 += 8) any = counts8(w0) != 0ull;
+      unsigned mq = __ballot_sync(0xffffffffu, any);
+      while (mq) {
+        const int src = __ffs(mq) - 1;
+        mq &= mq - 1;
+        const int q = __shfl_sync(0xffffffffu, qi, src);
+        const uint64_t kk = warp_merge_query(a.keys + (long long)q * k, k, a.ccnt + (long long)q * NW, NW,
+                                             a.cand + (long long)q * NW * a.capw, a.capw, lane);
+        if (lane == src) kth = key_dist(kk);
+      }
+    } else if (valid) {
       // register top-k (descending, sentinel-padded: leafscan.cuh merge_queue)
       uint64_t arr[KB];
       bool loaded = false;
@@ -624,6 +696,7 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
         kth = key_dist(arr[0]);
       }
     }
+    if (!valid) continue;
     // 2. FindLeaf with the new k-th distance
 #pragma unroll
     for (int j = 0; j < kSplitMaxD; ++j)
@@ -850,9 +923,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
     uint64_t* __restrict__ keys, int4* __restrict__ qs,
     const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base,
     uint8_t* __restrict__ ccnt, int NW, int* __restrict__ ovflag) {
-  __shared__ uint64_t s_row[kFinishWarps][64];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  uint64_t* row = s_row[wl];
   const int n = ctl->novf;
   for (int i = blockIdx.x * kFinishWarps + wl; i < n; i += gridDim.x * kFinishWarps) {
     const int qi = __ldg(ovf + i);
@@ -861,13 +932,14 @@ __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
     for (int w = lane; w < NW; w += 32) ccnt[(long long)qi * NW + w] = 0;
     if (lane == 0) ovflag[qi] = 0;
     uint64_t* kp = keys + (long long)qi * k;
-    for (int j = lane; j < k; j += 32) row[j] = kp[j];
-    __syncwarp();
-    float qv[32];
+    // the row across the warp (warp_row_insert)
+    uint64_t r0 = lane < k ? kp[lane] : ~0ull;
+    uint64_t r1 = lane + 32 < k ? kp[lane + 32] : ~0ull;
+    uint64_t kkey = k <= 32 ? __shfl_sync(0xffffffffu, r0, k - 1) : __shfl_sync(0xffffffffu, r1, k - 33);
+    float qv[kSplitMaxD];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) qv[j] = j < d ? __ldg(q + (long long)qi * D + j) : 0.0f;
+    for (int j = 0; j < kSplitMaxD; ++j) qv[j] = j < d ? __ldg(q + (long long)qi * D + j) : 0.0f;
     const long long g0 = __ldg(quad_base + leaf), g1 = __ldg(quad_base + leaf + 1);
-    uint64_t kkey = row[k - 1];
     for (long long gb = g0; gb < g1; gb += 32) {
       const long long g = gb + lane;
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -875,7 +947,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
       if (has) {
         const float4* pq = reinterpret_cast<const float4*>(pts + g * 4 * D);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < kSplitMaxD; ++j) {
           if (j < d) {
             const float4 p = __ldg(pq + j);
             const float e[4] = {p.x, p.y, p.z, p.w};
@@ -896,22 +968,13 @@ __global__ void __launch_bounds__(kFinishWarps * 32) rescan_kernel(
           const int src = __ffs(bal) - 1;
           bal &= bal - 1;
           const uint64_t c = __shfl_sync(0xffffffffu, key, src);
-          if (lane == 0 && c < row[k - 1]) {
-            int j = k - 1;
-            while (j > 0 && row[j - 1] > c) {
-              row[j] = row[j - 1];
-              --j;
-            }
-            row[j] = c;
-          }
-          __syncwarp();
-          kkey = row[k - 1];
+          if (c < kkey) kkey = warp_row_insert(r0, r1, c, k, lane);
         }
       }
     }
-    for (int j = lane; j < k; j += 32) kp[j] = row[j];
-    if (lane == 0) reinterpret_cast<int*>(qs + qi)[0] = __float_as_int(key_dist(row[k - 1]));
-    __syncwarp();
+    if (lane < k) kp[lane] = r0;
+    if (lane + 32 < k) kp[lane + 32] = r1;
+    if (lane == 0) reinterpret_cast<int*>(qs + qi)[0] = __float_as_int(key_dist(kkey));
   }
 }
 

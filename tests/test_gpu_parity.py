@@ -407,3 +407,23 @@ def test_tail_finisher_mixture(gpu_device, exact, monkeypatch):
     if exact:
         sample = np.arange(0, queries.shape[0], 97)
         assert np.array_equal(out[0][0][sample], O.brute_keys(refs, queries[sample], 10))
+
+
+@pytest.mark.parametrize("d", [16, 20])
+@pytest.mark.parametrize("fam", ["normal", "uniform"])
+def test_leaves_smaller_than_k_tc32(gpu_device, d, fam):
+    """Regression (fuzz seed 11 case 68): leaves of ~8 points (fewer than
+    k = 10) on the 32-column tensor-core layout.  Until a query holds k
+    neighbours its filter threshold is +inf, and the 64-row chunk variant
+    re-evaluated a short chunk's second (stale) column group."""
+    rng = np.random.default_rng(5)
+    x = rng.normal(0, 3, (4147 + 1771, d)) if fam == "normal" else rng.random((4147 + 1771, d))
+    x = x.astype(np.float32)
+    refs, q = x[:4147], x[4147:]
+    tree = bkt.build_buffer_tree(refs, 9)
+    want = O.knn_tree(O.build_tree(refs, 9), q, 10, threads=O.default_threads())
+    for kernel in ("tc", "auto"):
+        st = bkt.SearchStats()
+        res = bkt.lazy_search(tree, q, bkt.SearchParams(k=10), device=gpu_device, stats=st, kernel=kernel)
+        assert np.array_equal(res.keys, want["keys"]), kernel
+        assert np.array_equal(st.visited_per_query, want["visited"].astype(np.int64)), kernel

@@ -185,7 +185,10 @@ def cfg5(a):
                 emit({"config": f"cfg5 mixture n=8M m={m} d=10 h={h} k={k} "
                                 f"{'host-resident, ' + str(num_chunks) + ' chunks streamed' if num_chunks > 1 else 'HBM-resident'}",
                       "qps_device": m / (st["search_ms"] / 1e3), "qps_wall": m / wall, "rounds": st["rounds"],
-                      "pairs_per_query": st["pairs"] / m, "sample_rows_match_oracle": ok})
+                      "pairs_per_query": st["pairs"] / m, "sample_rows_match_oracle": ok,
+                      **({"stream_gb": st["stream_bytes"] / 1e9, "stream_copies": st["stream_copies"],
+                          "stream_gbs_over_search": st["stream_bytes"] / 1e9 / (st["search_ms"] / 1e3),
+                          "pcie_peak_gbs": "~55 (PCIe Gen5 x16 H2D, nominal 64)"} if num_chunks > 1 else {})})
             dev.close()
 
 

@@ -57,6 +57,7 @@ def main():
     ap.add_argument("--cases", type=int, default=200)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--seconds", type=float, default=600)
+    ap.add_argument("--only", type=int, default=-1, help="replay the generator and run only this case")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
@@ -78,7 +79,12 @@ def main():
             take = rng.integers(0, n, size=m // 3)
             q[: take.size] = refs[take]
         kernel = str(rng.choice(["auto", "tc", "direct"])) if d <= 31 and k <= 64 and h <= 16 else "auto"
-        tree = bkt.build_buffer_tree(refs, h, device=0 if rng.random() < 0.5 else None)
+        dev_build = rng.random() < 0.5
+        if a.only >= 0 and case != a.only:
+            continue
+        print(json.dumps({"running": case, "fam": fam, "n": n, "m": m, "d": d, "k": k, "h": h, "kernel": kernel}),
+              file=sys.stderr, flush=True)
+        tree = bkt.build_buffer_tree(refs, h, device=0 if dev_build else None)
         st = bkt.SearchStats()
         res = bkt.lazy_search(tree, q, bkt.SearchParams(k=k), device=dev, stats=st, kernel=kernel)
         want = O.knn_tree(O.build_tree(refs, h), q, k, threads=8)
@@ -88,6 +94,12 @@ def main():
         if not ok:
             fails += 1
             bad = int((res.keys != want["keys"]).any(axis=1).sum())
+            if a.only >= 0:
+                rows = np.nonzero((res.keys != want["keys"]).any(axis=1))[0]
+                for r in rows[:5]:
+                    print("row", int(r), "got", bkt.unpack_keys(res.keys[r:r + 1]), "want",
+                          bkt.unpack_keys(want["keys"][r:r + 1]), "visited", int(st.visited_per_query[r]),
+                          int(want["visited"][r]), file=sys.stderr)
             print(json.dumps({"case": case, "fam": fam, "n": n, "m": m, "d": d, "k": k, "h": h, "kernel": kernel,
                               "rows_differing": bad}), flush=True)
     print(json.dumps({"cases": done, "failures": fails, "seconds": round(time.time() - t0, 1)}), flush=True)

@@ -423,7 +423,10 @@ def main() -> None:
     tf32_peak = bf16 / 2
     peak_src = "of measured (MEASURED_PEAKS.json bf16 / 2)" if peaks else "of fallback (1.59 PF bf16 / 2, B200_PROFILING.md)"
     tc_used = a.kernel in ("auto", "tc") and DIM <= 31
-    kernel_name = "leafscan_tc_kernel" if tc_used else "leafscan_kernel"
+    # the leaf scans of a step: the home visit (leafscan_tc_kernel, one launch)
+    # and the later visits as (leaf, window) items (splitscan_tc_kernel, one
+    # launch per round); `achieved` counts the algorithmic pairs of both
+    kernel_name = ("splitscan_tc_kernel + leafscan_tc_kernel (home round)" if tc_used else "leafscan_kernel")
     traffic = None
     tfs = sorted(ROOT.glob("profiles/r*/ncu_traffic.json"))  # the latest round's capture
     tf = tfs[-1] if tfs else None

@@ -180,6 +180,9 @@ struct bkt_ctx {
   uint32_t* visits_tmp = nullptr;
   // split-round per-query buffers (capacity split_cap queries)
   long long split_cap = 0;
+  long long last_per_query = 0;  // per-query bytes the work buffers were last sized for
+  int split_capw = 0;          // candidate slice size of the current search (split_capw(NW, k))
+  int split_capw_alloc = 0;    // slice size the cand buffer was allocated for
   float* arow = nullptr;                 // m x kSplitKT
   uint8_t* ccnt = nullptr;               // m x split_NW
   uint64_t* cand = nullptr;              // m x split_NW x capw
@@ -327,12 +330,12 @@ int ensure_perm(bkt_ctx* ctx, long long m, int k) {
 
 // per-query bytes of the split-round buffers
 long long split_bytes_per_query(const bkt_ctx* c) {
-  return 4ll * kSplitKT + (1ll + 8ll * split_capw(c->split_NW)) * c->split_NW + 4 + 4 + 8 + 16 + 4ll * c->split_NW +
+  return 4ll * kSplitKT + (1ll + 8ll * c->split_capw) * c->split_NW + 4 + 4 + 8 + 16 + 4ll * c->split_NW +
          16ll * c->split_NW / kNT + 16;
 }
 
 int ensure_split(bkt_ctx* ctx, long long m) {
-  if (ctx->split_cap >= m) return BKT_OK;
+  if (ctx->split_cap >= m && ctx->split_capw_alloc == ctx->split_capw) return BKT_OK;
   dfree(ctx->arow); dfree(ctx->ccnt); dfree(ctx->cand); dfree(ctx->ovflag); dfree(ctx->ovf); dfree(ctx->qmask); dfree(ctx->cbase);
   dfree(ctx->qs);
   dfree(ctx->items); dfree(ctx->stoff); dfree(ctx->stiles);
@@ -341,7 +344,7 @@ int ensure_split(bkt_ctx* ctx, long long m) {
   CU(cudaMalloc(&ctx->arow, sizeof(float) * M * kSplitKT));
   CU(cudaMalloc(&ctx->ccnt, M * NW));
   CU(cudaMemset(ctx->ccnt, 0, M * NW));
-  CU(cudaMalloc(&ctx->cand, sizeof(uint64_t) * M * NW * split_capw((int)NW)));
+  CU(cudaMalloc(&ctx->cand, sizeof(uint64_t) * M * NW * ctx->split_capw));
   CU(cudaMalloc(&ctx->ovflag, sizeof(int) * M));
   CU(cudaMemset(ctx->ovflag, 0, sizeof(int) * M));
   CU(cudaMalloc(&ctx->ovf, sizeof(int) * M));
@@ -353,6 +356,7 @@ int ensure_split(bkt_ctx* ctx, long long m) {
   ctx->stiles_cap = M * NW / kNT + (long long)ctx->nl * NW + 1;
   CU(cudaMalloc(&ctx->stiles, sizeof(int4) * ctx->stiles_cap));
   ctx->split_cap = M;
+  ctx->split_capw_alloc = ctx->split_capw;
   return BKT_OK;
 }
 
@@ -1322,7 +1326,7 @@ int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
   a.ccnt = ctx->ccnt;
   a.cand = ctx->cand;
   a.NW = ctx->split_NW;
-  a.capw = split_capw(ctx->split_NW);
+  a.capw = ctx->split_capw;
   a.centroid = ctx->tc_centroid;
   a.arow = ctx->arow;
   a.seq_log = R.seq ? ctx->seq_dev : nullptr;
@@ -1391,7 +1395,7 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
     sa.cand = ctx->cand;
     sa.ovflag = ctx->ovflag;
     sa.NW = ctx->split_NW;
-    sa.capw = split_capw(ctx->split_NW);
+    sa.capw = ctx->split_capw;
     sa.ovf = ctx->ovf;
     sa.novf = &ctx->ctl->novf;
     sa.items = ctx->items;
@@ -1820,8 +1824,12 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // Leaves of one window (NW = 1: < 5 chunks of 128 points) gain nothing
   // from routing: config 1 (256-point leaves) runs 6.15 M q/s on leaf-level
   // rounds against 4.06 M with split rounds.
-  R.split = R.tc && !R.unfused && ctx->split_NW > 1 && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 &&
-            R.tc_cps == 2;
+  // With k > 16 a one-window leaf still gains: the leaf-level scan would keep
+  // a 32/64-slot register top-k per query (one CTA per SM), the split rounds
+  // merge candidate slices warp-cooperatively instead.
+  const bool nw_ok = ctx->split_NW > 1 || (ctx->split_NW == 1 && k > 16 && m >= (1 << 20)) ||
+                     (std::getenv("BKT_SPLIT_NW1") && ctx->split_NW == 1);
+  R.split = R.tc && !R.unfused && nw_ok && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 && R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
   // graph mode (opt-in, BKT_GRAPH=1): measured slower than eager launches on
@@ -1889,11 +1897,18 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   if (const char* e = std::getenv("BKT_FINISH_AT")) R.finish_at = std::atoll(e);
   if (const char* e = std::getenv("BKT_FINISH_CTA")) R.finish_cta = std::atoi(e) != 0;
 
+  if (R.split) ctx->split_capw = split_capw(ctx->split_NW, k);
   // batch size: whatever fits comfortably in free memory (or the caller's choice)
   const long long per_query = 4ll * ctx->D + 4ll * ctx->d + 8ll * k + 4 * 5 + (R.split ? split_bytes_per_query(ctx) : 0) +
                               (R.renumber ? 4ll * ctx->D + 8ll * k + 8 : 0);
   long long batch = o.batch_queries;
   if (batch <= 0) {
+    // buffers sized for another per-query footprint (another k or path) are
+    // released first, so the estimate below sees them as free
+    if (ctx->last_per_query != per_query) {
+      CU(cudaStreamSynchronize(ctx->stream));
+      free_work(ctx);
+    }
     size_t fr = 0, to = 0;
     CU(cudaMemGetInfo(&fr, &to));
     long long usable = (long long)(fr * 0.6) + (long long)ctx->cap_m * per_query;
@@ -1910,6 +1925,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     if (m >= (2ll << 20) && nio > 1) batch = std::min(batch, (m + nio - 1) / nio);
   }
   batch = std::min<long long>(batch, (long long)INT32_MAX / 2);
+  ctx->last_per_query = per_query;
   rc = ensure_work(ctx, batch, k);
   if (rc != BKT_OK) return rc;
   if (R.split) {

@@ -60,8 +60,16 @@ constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhe
 constexpr int kSplitStages = 5;  // TMA ring stages (128-row chunks)
 constexpr int kSplitThreads = 192;
 // candidates per (query, window) and round before the leaf is rescanned instead
-// (even, so every slice starts 16-byte aligned for advance_kernel's paired loads)
-__host__ __device__ inline int split_capw(int NW) { return NW <= 8 ? 16 : (NW >= 32 ? 4 : (128 / NW) & ~1); }
+// Candidates per (query, window) slice: 16 for leaves of <= 8 windows, at
+// least 8 for leaves of more (the candidates of a visit concentrate in the
+// few windows near the query), and about k for k > 16 (a larger kth-ball);
+// a query whose candidates overflow a slice has its leaf rescanned.  Even,
+// so every slice starts 16-byte aligned for advance_kernel's paired loads.
+__host__ __device__ inline int split_capw(int NW, int k) {
+  const int base = NW <= 8 ? 16 : max(8, (128 / NW) & ~1);
+  // (k > 16: at most ~8 KB of slices per query)
+  return k > 16 ? max(base, min(min(64, (k + 7) & ~7), max(base, (1024 / NW) & ~1))) : base;
+}
 
 struct SplitScanArgs {
   const float* q;            // m x qstride original coordinates (survivor re-evaluation)
@@ -576,13 +584,15 @@ __device__ __forceinline__ uint64_t warp_merge_query(uint64_t* __restrict__ row,
       wm &= wm - 1;
       const int w = src + 32 * half;
       const int nc = min(__shfl_sync(full, half ? n1 : n0, src), capw);
-      const uint64_t c = lane < nc ? cand[(long long)w * capw + lane] : ~0ull;
-      unsigned todo = __ballot_sync(full, c < kk);
-      while (todo) {
-        const int e = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const uint64_t cv = __shfl_sync(full, c, e);
-        if (cv < kk) kk = warp_row_insert(r0, r1, cv, k, lane);  // (kk may have fallen meanwhile)
+      for (int e0 = 0; e0 < nc; e0 += 32) {  // the slice in batches of 32, one key per lane
+        const uint64_t c = e0 + lane < nc ? cand[(long long)w * capw + e0 + lane] : ~0ull;
+        unsigned todo = __ballot_sync(full, c < kk);
+        while (todo) {
+          const int e = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const uint64_t cv = __shfl_sync(full, c, e);
+          if (cv < kk) kk = warp_row_insert(r0, r1, cv, k, lane);  // (kk may have fallen meanwhile)
+        }
       }
     }
   }

@@ -185,7 +185,7 @@ struct bkt_ctx {
   int split_capw_alloc = 0;    // slice size the cand buffer was allocated for
   float* arow = nullptr;                 // m x kSplitKT
   uint8_t* ccnt = nullptr;               // m x split_NW
-  uint64_t* cand = nullptr;              // m x split_NW x capw
+  uint32_t* cand = nullptr;              // m x split_NW x capw survivor rows
   int* ovflag = nullptr;                 // m
   int* ovf = nullptr;                    // m
   unsigned long long* qmask = nullptr;   // m
@@ -330,7 +330,7 @@ int ensure_perm(bkt_ctx* ctx, long long m, int k) {
 
 // per-query bytes of the split-round buffers
 long long split_bytes_per_query(const bkt_ctx* c) {
-  return 4ll * kSplitKT + (1ll + 8ll * c->split_capw) * c->split_NW + 4 + 4 + 8 + 16 + 4ll * c->split_NW +
+  return 4ll * kSplitKT + (1ll + 4ll * c->split_capw) * c->split_NW + 4 + 4 + 8 + 16 + 4ll * c->split_NW +
          16ll * c->split_NW / kNT + 16;
 }
 
@@ -344,7 +344,7 @@ int ensure_split(bkt_ctx* ctx, long long m) {
   CU(cudaMalloc(&ctx->arow, sizeof(float) * M * kSplitKT));
   CU(cudaMalloc(&ctx->ccnt, M * NW));
   CU(cudaMemset(ctx->ccnt, 0, M * NW));
-  CU(cudaMalloc(&ctx->cand, sizeof(uint64_t) * M * NW * ctx->split_capw));
+  CU(cudaMalloc(&ctx->cand, sizeof(uint32_t) * M * NW * ctx->split_capw));
   CU(cudaMalloc(&ctx->ovflag, sizeof(int) * M));
   CU(cudaMemset(ctx->ovflag, 0, sizeof(int) * M));
   CU(cudaMalloc(&ctx->ovf, sizeof(int) * M));
@@ -1325,6 +1325,9 @@ int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
   a.qs = ctx->qs;
   a.ccnt = ctx->ccnt;
   a.cand = ctx->cand;
+  a.rows = ctx->tc_rowsxyz;
+  a.ridx = ctx->tc_idx;
+  a.fma = R.fma ? 1 : 0;
   a.NW = ctx->split_NW;
   a.capw = ctx->split_capw;
   a.centroid = ctx->tc_centroid;
@@ -1388,8 +1391,6 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
     CU(launch_place(R.grid_small, ctx->stream, ra));
     R.launches++;
     SplitScanArgs sa{};
-    sa.q = ctx->q;
-    sa.qstride = ctx->D;
     sa.arow = ctx->arow;
     sa.ccnt = ctx->ccnt;
     sa.cand = ctx->cand;
@@ -1403,10 +1404,7 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
     sa.num_tiles = &ctx->ctl->stiles;
     sa.tile_next = &ctx->ctl->tile_next;
     sa.B = ctx->tc_B;
-    sa.ridx = ctx->tc_idx;
-    sa.rows = ctx->tc_rowsxyz;
     sa.row_base = ctx->tc_row_base;
-    sa.d = ctx->d;
     sa.W = ctx->split_W;
     sa.stats = R.verbose ? &ctx->ctl->sc_tiles : nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1824,10 +1822,11 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // Leaves of one window (NW = 1: < 5 chunks of 128 points) gain nothing
   // from routing: config 1 (256-point leaves) runs 6.15 M q/s on leaf-level
   // rounds against 4.06 M with split rounds.
-  // With k > 16 a one-window leaf still gains: the leaf-level scan would keep
-  // a 32/64-slot register top-k per query (one CTA per SM), the split rounds
-  // merge candidate slices warp-cooperatively instead.
-  const bool nw_ok = ctx->split_NW > 1 || (ctx->split_NW == 1 && k > 16 && m >= (1 << 20)) ||
+  // One-window leaves (NW = 1) gain only on large batches, where the
+  // leaf-level rounds' per-thread top-k and fused FindLeaf cost more than the
+  // split rounds' extra kernels: config 5 h = 14 (m = 10M) k = 10 5.5 -> 7.4
+  // M q/s, k = 50 1.4 -> 3.3 M; config 1 (m = 65K) 6.2 -> 4.1 M the other way.
+  const bool nw_ok = ctx->split_NW > 1 || (ctx->split_NW == 1 && m >= (1 << 20)) ||
                      (std::getenv("BKT_SPLIT_NW1") && ctx->split_NW == 1);
   R.split = R.tc && !R.unfused && nw_ok && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 && R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;

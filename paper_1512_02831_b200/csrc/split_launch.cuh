@@ -7,9 +7,8 @@
 
 namespace bkt {
 
-template <bool FMA>
 inline cudaError_t launch_splitscan_one(int grid, cudaStream_t s, const SplitScanArgs& a, bool configure_only = false) {
-  auto fn = splitscan_tc_kernel<FMA>;
+  auto fn = splitscan_tc_kernel;
   static std::atomic<unsigned long long> configured{0};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -29,9 +28,9 @@ inline cudaError_t launch_splitscan_one(int grid, cudaStream_t s, const SplitSca
 
 // kernel attributes of the split rounds' kernels, set outside any stream capture
 inline cudaError_t configure_split_kernels(bool fma, int kb, int h, int d) {
+  (void)fma;
   SplitScanArgs dummy{};
-  cudaError_t e = fma ? launch_splitscan_one<true>(0, nullptr, dummy, true)
-                      : launch_splitscan_one<false>(0, nullptr, dummy, true);
+  cudaError_t e = launch_splitscan_one(0, nullptr, dummy, true);
   if (e != cudaSuccess) return e;
   const int smem = advance_smem_bytes(h, d);
   if (smem <= 48 * 1024) return cudaSuccess;
@@ -46,8 +45,9 @@ inline cudaError_t configure_split_kernels(bool fma, int kb, int h, int d) {
   }
 }
 
-inline cudaError_t launch_splitscan(bool fma, int grid, cudaStream_t s, const SplitScanArgs& a) {
-  return fma ? launch_splitscan_one<true>(grid, s, a) : launch_splitscan_one<false>(grid, s, a);
+// (the split scan has no arithmetic mode: survivors are evaluated in advance_kernel)
+inline cudaError_t launch_splitscan(bool /*fma*/, int grid, cudaStream_t s, const SplitScanArgs& a) {
+  return launch_splitscan_one(grid, s, a);
 }
 
 template <int KB>

@@ -24,12 +24,15 @@
 //   place    : items into their key's slice (route tile base + shared rank),
 //              and the (leaf, window) tile records.
 //   scan     : splitscan_tc_kernel -- the tensor-core filter of leafscan_tc.cuh
-//              on each tile's window against each query's kth; survivors
-//              re-evaluated in the reference arithmetic; points with
-//              D_ref <= kth go to the (query, window)'s slice of the candidate list.
-//   rescan   : a query whose candidates exceed a window's slice in one round gets its
+//              on each tile's window against each query's kth; the rows of
+//              the points that survive go to the (query, window)'s slice of
+//              the survivor list (the scan reads only TMEM: its TMA stages
+//              carry the B operand alone).
+//   rescan   : a query whose survivors exceed a window's slice in one round gets its
 //              whole leaf rescanned by one warp (exact), instead of merging.
-//   advance  : per query -- merge its candidates into the top-k row (the
+//   advance  : per query -- re-evaluate its survivors in the reference
+//              arithmetic (row-major coordinates of the tensor-core layout)
+//              and merge those below the k-th key into the top-k row (the
 //              reference's update_rows, core.py:251-262; any order: the result
 //              is the best k of the row and the leaf), FindLeaf
 //              (buffer_tree.py:330-349) with the new kth, count the next leaf
@@ -42,42 +45,37 @@
 // below the k-th key at the visit's start, so its reference distance is
 // <= kth; such a point lies in a window whose box lower bound (computed in
 // f32, relaxed by 1e-5) is <= kth, survives the filter (leafscan_tc.cuh
-// header) and is a candidate.  The top-k after the visit = best k of (row,
-// candidates) = best k of (row, leaf): identical to the reference.
+// header) and is re-evaluated exactly.  The top-k after the visit = best k of
+// (row, survivors) = best k of (row, leaf): identical to the reference.
 #pragma once
 #include "leafscan_tc.cuh"
 #include "round_kernels.cuh"
 
 namespace bkt {
 
-#ifndef BKT_SPLIT_QEAGER
-#define BKT_SPLIT_QEAGER 1
-#endif
 
 constexpr int kSplitKT = 16;     // A row: d coordinates, 1.0 at column d, zeros, kth at KT-2, |q'|^2 at KT-1 (d <= 13)
 constexpr int kSplitMaxD = kSplitKT - 3;
 constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhead = 2 tiles ahead
-constexpr int kSplitStages = 5;  // TMA ring stages (128-row chunks)
+constexpr int kSplitStages = 8;  // TMA ring stages (128-row chunks of the B operand)
 constexpr int kSplitThreads = 192;
-// candidates per (query, window) and round before the leaf is rescanned instead
-// Candidates per (query, window) slice: 16 for leaves of <= 8 windows, at
-// least 8 for leaves of more (the candidates of a visit concentrate in the
-// few windows near the query), and about k for k > 16 (a larger kth-ball);
-// a query whose candidates overflow a slice has its leaf rescanned.  Even,
-// so every slice starts 16-byte aligned for advance_kernel's paired loads.
+// Survivor entries (u32 rows of the tensor-core layout) per (query, window)
+// slice: 32 for leaves of <= 8 windows, at least 16 for leaves of more (the
+// survivors of a visit concentrate in the few windows near the query), and
+// about 2k for k > 16 (a larger kth-ball); a query whose survivors overflow a
+// slice has its leaf rescanned exactly.  A multiple of 4, so every slice
+// starts 16-byte aligned.
 __host__ __device__ inline int split_capw(int NW, int k) {
-  const int base = NW <= 8 ? 16 : max(8, (128 / NW) & ~1);
+  const int base = NW <= 8 ? 32 : max(16, (256 / NW) & ~3);
   // (k > 16: at most ~8 KB of slices per query)
-  return k > 16 ? max(base, min(min(64, (k + 7) & ~7), max(base, (1024 / NW) & ~1))) : base;
+  return k > 16 ? max(base, min(min(128, (2 * k + 3) & ~3), max(base, (2048 / NW) & ~3))) : base;
 }
 
 struct SplitScanArgs {
-  const float* q;            // m x qstride original coordinates (survivor re-evaluation)
-  int qstride;
   const float* arow;         // m x kSplitKT A rows (advance_kernel)
-  uint8_t* ccnt;             // m x NW: candidates of each (query, window) this round
-  uint64_t* cand;            // m x NW x capw
-  int* ovflag;               // m: the query's candidates overflowed (rescan)
+  uint8_t* ccnt;             // m x NW: survivors of each (query, window) this round
+  uint32_t* cand;            // m x NW x capw survivor rows (tensor-core layout rows)
+  int* ovflag;               // m: the query's survivors overflowed (rescan)
   int* ovf;                  // queries to rescan
   int* novf;
   int NW, capw;
@@ -86,12 +84,9 @@ struct SplitScanArgs {
   const int* num_tiles;
   int* tile_next;            // dynamic tile counter (zeroed by plan_split_kernel)
   const float* B;            // tensor-core layout (engine.cu build_tc_layout)
-  const uint32_t* ridx;
-  const float* rows;
   const long long* row_base;
-  int d;
   int W;                     // chunks per window
-  unsigned long long* stats; // diagnostics: tiles, chunks, candidates, writers, items (or null)
+  unsigned long long* stats; // diagnostics: tiles, chunks, survivors, writers, items, -, trips (or null)
   long long* dbg;            // BKT_SPLIT_DEBUG: per-event clock64 stamps of CTA 0 (or null)
   int dbg_cap;
 };
@@ -104,12 +99,8 @@ struct SplitWin {
 struct SplitSmem {
   static constexpr int KT = kSplitKT;
   static constexpr int kStageB = 128 * KT * 4;
-  static constexpr int kStageIdx = 128 * 4;
-  static constexpr int kStageRows = 128 * kSplitMaxD * 4;
   static constexpr int kA = 128 * KT * 4;
-  static constexpr int kOffIdx = kSplitStages * kStageB;
-  static constexpr int kOffRows = kOffIdx + kSplitStages * kStageIdx;
-  static constexpr int kOffA = kOffRows + kSplitStages * kStageRows;
+  static constexpr int kOffA = kSplitStages * kStageB;
   static constexpr int kOffQi = kOffA + kSplitNA * kA;
   static constexpr int kOffRec = kOffQi + kSplitNA * 128 * 4;
   static constexpr int kOffWin = kOffRec + kSplitNA * 16;
@@ -129,22 +120,19 @@ __host__ __device__ __forceinline__ int canon_off(int r, int k, int KT) {
   return (r >> 3) * (KT * 8) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
 }
 
-template <bool FMA>
 __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const SplitScanArgs A) {
   using S = SplitSmem;
   constexpr int KT = kSplitKT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   float* sB = reinterpret_cast<float*>(smem);
-  uint32_t* sIdx = reinterpret_cast<uint32_t*>(smem + S::kOffIdx);
-  float* sRows = reinterpret_cast<float*>(smem + S::kOffRows);
   float* sA = reinterpret_cast<float*>(smem + S::kOffA);
   int* sQi = reinterpret_cast<int*>(smem + S::kOffQi);
   int4* s_rec = reinterpret_cast<int4*>(smem + S::kOffRec);
   SplitWin* s_win = reinterpret_cast<SplitWin*>(smem + S::kOffWin);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
-  uint64_t* full = bars;                       // [stages] TMA -> MMA / survivors
-  uint64_t* empty = bars + kSplitStages;       // [stages] epilogue -> TMA
+  uint64_t* full = bars;                       // [stages] TMA -> MMA
+  uint64_t* empty = bars + kSplitStages;       // [stages] MMA completion (tcgen05.commit) -> TMA
   uint64_t* tfull = bars + 2 * kSplitStages;   // [2] MMA -> epilogue
   uint64_t* tempty = tfull + 2;                // [2] epilogue -> MMA
   uint64_t* afull = tempty + 2;                // [NA] producer (A rows, ids, tile record) -> MMA, epilogue
@@ -156,7 +144,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
   if (tid == 0) {
     for (int s = 0; s < kSplitStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kTcEpiWarps);
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -178,11 +166,10 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   const int tiles_end = *A.num_tiles;
-  const int d = A.d;
 
   if (warp == 4) {
     // ===== producer: tile records, A-row gather (all lanes, cp.async, kAhead
-    // tiles in flight), TMA of the window's chunks (lane 0).  The dependent
+    // tiles in flight), TMA of the window's B chunks (lane 0).  The dependent
     // loads of a tile (its index from the counter, its record, its query ids
     // and leaf rows) are spread over three consecutive issues, so each one's
     // latency overlaps a tile of work. =====
@@ -277,16 +264,16 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
           const long long row = win.r0 + (long long)c * 128;
           const int nr = (int)dmin_ll(128, win.r1 - row);
           if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * A.dbg_cap + 8 * g + 5] = clock64();
-          mbar_arrive_expect_tx(&full[s], nr * (KT * 4 + 4 + d * 4));
+          mbar_arrive_expect_tx(&full[s], nr * KT * 4);
           bulk_g2s(sB + s * (S::kStageB / 4), A.B + row * KT, nr * KT * 4, &full[s]);
-          bulk_g2s(sIdx + s * 128, A.ridx + row, nr * 4, &full[s]);
-          bulk_g2s(sRows + s * (S::kStageRows / 4), A.rows + row * d, nr * d * 4, &full[s]);
         }
       }
       __syncwarp();
     }
   } else if (warp == 5) {
-    // ===== MMA issuer =====
+    // ===== MMA issuer: per chunk two tf32 MMAs (K = 16) into one of two TMEM
+    // accumulators; the commit frees the smem stage (the epilogue reads only
+    // TMEM) and then signals the epilogue =====
     if (lane == 0) {
       uint32_t g = 0;
       const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
@@ -318,6 +305,9 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
                 "l"(da), "l"(db), "r"(idesc), "r"(acc));
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_addr(&empty[s]))
+                       : "memory");
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            smem_addr(&tfull[b]))
                        : "memory");
           if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * A.dbg_cap + 8 * g + 1] = clock64();
@@ -328,7 +318,10 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       }
     }
   } else {
-    // ===== epilogue: one thread per item (query) of the tile =====
+    // ===== epilogue: one thread per item (query) of the tile.  Per chunk the
+    // filter's minimum over 128 columns and one vote; the rows of the points
+    // that survive are appended to the item's slice (their exact evaluation
+    // runs in advance_kernel) =====
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
     const int capw = A.capw;
     uint32_t g = 0;
@@ -349,81 +342,16 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       __syncwarp();
       if (lane == 0) mbar_arrive(&aempty[ab]);
 
-      if (dbg_on && (int)j < A.dbg_cap) A.dbg[8 * j + 1] = clock64();
       const float qnc = (1.0f - kTcMargin) * qn;
       const bool force = valid && !(qn >= 1e-30f && qn <= 1e30f);
       // kth - (1 - C) qn, rounded up by a hair (leafscan_tc.cuh); forced rows pass everything
       float thr = -__int_as_float(0x7f800000);
       if (valid) thr = force ? __int_as_float(0x7f800000) : __fsub_ru(kth, qnc) + 1e-6f * (fabsf(kth) + qnc);
       int cn = 0;
-      bool have_q = false;
-      float qv[kSplitMaxD];
-#pragma unroll
-      for (int jj = 0; jj < kSplitMaxD; ++jj) qv[jj] = 0.0f;
-      // this (query, window)'s candidates go straight to its slice of the list
-      uint64_t* cdst = A.cand + ((long long)qi * A.NW + rec.w) * capw;
-#if BKT_SPLIT_QEAGER
-      // the query's coordinates for survivor re-evaluation, loaded at the
-      // tile's start so their latency overlaps the first chunks' MMA
-      // (config 2: 33.6 -> 36.1 M q/s; lazily at the first survivor the load
-      // was a long-scoreboard stall on nearly every tile's critical path)
-      if (valid) {
-        const float* qp = A.q + (long long)qi * A.qstride;
-#pragma unroll
-        for (int jj = 0; jj < kSplitMaxD; ++jj) qv[jj] = jj < d ? __ldg(qp + jj) : 0.0f;
-      }
-      have_q = true;
-#endif
-      if (dbg_on && (int)j < A.dbg_cap) A.dbg[8 * j + 2] = clock64();
-
-      auto process = [&](const uint32_t (&v)[32], int gcol, int s) {
-        uint32_t mask = 0;
-        if (valid) {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) mask |= (!(__uint_as_float(v[jj]) > thr) ? 1u : 0u) << jj;
-        }
-        if (A.stats) {
-          unsigned long long sv = __popc(mask);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-          if (lane == 0) atomicAdd(A.stats + 5, sv);
-        }
-        if (mask && !have_q) {
-          const float* qp = A.q + (long long)qi * A.qstride;
-#pragma unroll
-          for (int jj = 0; jj < kSplitMaxD; ++jj) qv[jj] = jj < d ? __ldg(qp + jj) : 0.0f;
-          have_q = true;
-        }
-        const uint32_t* ids = sIdx + s * 128 + gcol;
-        const float* prow = sRows + s * (S::kStageRows / 4) + gcol * d;
-        while (__any_sync(0xffffffffu, mask != 0)) {
-          if (A.stats && lane == 0) atomicAdd(A.stats + 6, 1ull);
-          if (mask) {
-            const int jj0 = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const float* pp = prow + jj0 * d;
-            float pv[kSplitMaxD];
-#pragma unroll
-            for (int jj = 0; jj < kSplitMaxD; ++jj) pv[jj] = jj < d ? pp[jj] : 0.0f;
-            float acc = 0.0f;
-#pragma unroll
-            for (int jj = 0; jj < kSplitMaxD; ++jj) {
-              if (jj < d) {
-                const float df = __fsub_rn(qv[jj], pv[jj]);
-                if constexpr (FMA) acc = __fmaf_rn(df, df, acc);
-                else acc = __fadd_rn(acc, __fmul_rn(df, df));
-              }
-            }
-            if (acc <= kth && ids[jj0] != kIndexSentinel) {
-              if (cn < capw) cdst[cn] = pack_key(acc, ids[jj0]);
-              ++cn;
-            }
-          }
-        }
-      };
+      // this (query, window)'s survivors go straight to its slice of the list
+      uint32_t* cdst = A.cand + ((long long)qi * A.NW + rec.w) * capw;
 
       for (int c = win.cb; c < win.ce; ++c, ++g) {
-        const int s = g % kSplitStages;
         const uint32_t b = g & 1u;
         const bool dbg_c = dbg_on && (int)g < A.dbg_cap;
         if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 2] = clock64();
@@ -458,24 +386,41 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
         }
         const float mchunk = fminf(fminf(gmn[0], gmn[1]), fminf(gmn[2], gmn[3]));
         if (__any_sync(0xffffffffu, valid && !(mchunk > thr))) {
-          mbar_wait(&full[s], (g / kSplitStages) & 1u);
+          // groups in the order 2, 3, 0, 1: groups 2 and 3 are still in va / vb
 #pragma unroll 1
-          for (int gi = 0; gi < ngrp; ++gi) {
+          for (int it = 0; it < 4; ++it) {
+            const int gi = it ^ 2;
+            if (gi >= ngrp) continue;
             float gv = gmn[0];
 #pragma unroll
             for (int jj = 1; jj < 4; ++jj) gv = gi == jj ? gmn[jj] : gv;
             if (!__any_sync(0xffffffffu, valid && !(gv > thr))) continue;
-            tmem_ld32_async(tbase + 32 * gi, va);
-            tmem_wait(va);
-            process(va, 32 * gi, s);
+            if (gi < 2) {
+              tmem_ld32_async(tbase + 32 * gi, va);
+              tmem_wait(va);
+            }
+            const uint32_t(&v)[32] = gi == 3 ? vb : va;
+            uint32_t mask = 0;
+            if (valid) {
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj) mask |= (!(__uint_as_float(v[jj]) > thr) ? 1u : 0u) << jj;
+            }
+            if (A.stats) {
+              unsigned long long sv = __popc(mask);
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+              if (lane == 0) atomicAdd(A.stats + 5, sv);
+            }
+            const uint32_t rbase = (uint32_t)(row0 + 32 * gi);
+            for (; mask; mask &= mask - 1) {
+              if (cn < capw) cdst[cn] = rbase + (uint32_t)(__ffs(mask) - 1);
+              ++cn;
+            }
           }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&tempty[b]);
-          mbar_arrive(&empty[s]);
-        }
+        if (lane == 0) mbar_arrive(&tempty[b]);
         if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 4] = clock64();
       }
       if (cn > 0) {
@@ -535,9 +480,12 @@ struct AdvanceArgs {
   TopTreeView top;
   uint64_t* keys;
   int4* qs;                  // per query {kth bits, traversal state, visits, next leaf} (split_state)
-  uint8_t* ccnt;             // m x NW candidates of the round per window (all zero after the home round)
-  const uint64_t* cand;      // m x NW x capw
+  uint8_t* ccnt;             // m x NW survivors of the round per window (all zero after the home round)
+  const uint32_t* cand;      // m x NW x capw survivor rows of the tensor-core layout
   int NW, capw;
+  const float* rows;         // tensor-core layout: row-major original coordinates (exact re-evaluation)
+  const uint32_t* ridx;      // tensor-core layout: original index per row (padding: kIndexSentinel)
+  int fma;                   // 1: FMA accumulation (exact = 0: the reference's two roundings)
   const float* centroid;     // nl x kSplitKT
   float* arow;               // m x kSplitKT
   int* seq_log;
@@ -547,6 +495,36 @@ struct AdvanceArgs {
 
 constexpr int kAdvThreads = 256;
 __host__ __device__ inline int advance_smem_bytes(int h, int d) { return (start_tree_smem(h) + d * kAdvThreads) * 4; }
+
+// The packed key of survivor `row` for query coordinates qv, in the
+// reference arithmetic (core.py:138-146): acc = sum over j of (q_j - p_j)^2,
+// left to right, two roundings per term (exact) or one (FMA).  ~0 for a
+// padding row.
+__device__ __forceinline__ uint64_t survivor_key(const float (&qv)[kSplitMaxD], int d, const float* __restrict__ rows,
+                                                 const uint32_t* __restrict__ ridx, uint32_t row, int fma) {
+  const uint32_t id = __ldg(ridx + row);
+  const float* pp = rows + (long long)row * d;
+  float pv[kSplitMaxD];
+#pragma unroll
+  for (int j = 0; j < kSplitMaxD; ++j) pv[j] = j < d ? __ldg(pp + j) : 0.0f;
+  float acc = 0.0f;
+  if (fma) {
+#pragma unroll
+    for (int j = 0; j < kSplitMaxD; ++j)
+      if (j < d) {
+        const float df = __fsub_rn(qv[j], pv[j]);
+        acc = __fmaf_rn(df, df, acc);
+      }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSplitMaxD; ++j)
+      if (j < d) {
+        const float df = __fsub_rn(qv[j], pv[j]);
+        acc = __fadd_rn(acc, __fmul_rn(df, df));
+      }
+  }
+  return id == kIndexSentinel ? ~0ull : pack_key(acc, id);
+}
 
 // A top-k row of k <= 64 keys across a warp (lane j: row[j] in r0, row[32 + j]
 // in r1, ascending, ~0 past k).  Inserts cv (below the k-th key) at its rank
@@ -570,7 +548,10 @@ __device__ __forceinline__ uint64_t warp_row_insert(uint64_t& r0, uint64_t& r1, 
 // update_rows (core.py:251-262) in any insertion order.  Returns the new
 // k-th key; the counts are zeroed.
 __device__ __forceinline__ uint64_t warp_merge_query(uint64_t* __restrict__ row, int k, uint8_t* cc, int NW,
-                                                     const uint64_t* __restrict__ cand, int capw, int lane) {
+                                                     const uint32_t* __restrict__ cand, int capw, int lane,
+                                                     const float (&qv)[kSplitMaxD], int d,
+                                                     const float* __restrict__ rows,
+                                                     const uint32_t* __restrict__ ridx, int fma) {
   const uint32_t full = 0xffffffffu;
   uint64_t r0 = lane < k ? row[lane] : ~0ull;
   uint64_t r1 = lane + 32 < k ? row[lane + 32] : ~0ull;
@@ -584,8 +565,9 @@ __device__ __forceinline__ uint64_t warp_merge_query(uint64_t* __restrict__ row,
       wm &= wm - 1;
       const int w = src + 32 * half;
       const int nc = min(__shfl_sync(full, half ? n1 : n0, src), capw);
-      for (int e0 = 0; e0 < nc; e0 += 32) {  // the slice in batches of 32, one key per lane
-        const uint64_t c = e0 + lane < nc ? cand[(long long)w * capw + e0 + lane] : ~0ull;
+      for (int e0 = 0; e0 < nc; e0 += 32) {  // the slice in batches of 32, one survivor per lane
+        const uint64_t c =
+            e0 + lane < nc ? survivor_key(qv, d, rows, ridx, cand[(long long)w * capw + e0 + lane], fma) : ~0ull;
         unsigned todo = __ballot_sync(full, c < kk);
         while (todo) {
           const int e = __ffs(todo) - 1;
@@ -655,8 +637,12 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
         const int src = __ffs(mq) - 1;
         mq &= mq - 1;
         const int q = __shfl_sync(0xffffffffu, qi, src);
+        float qq[kSplitMaxD];
+#pragma unroll
+        for (int j = 0; j < kSplitMaxD; ++j) qq[j] = __shfl_sync(0xffffffffu, qv[j], src);
         const uint64_t kk = warp_merge_query(a.keys + (long long)q * k, k, a.ccnt + (long long)q * NW, NW,
-                                             a.cand + (long long)q * NW * a.capw, a.capw, lane);
+                                             a.cand + (long long)q * NW * a.capw, a.capw, lane, qq, d, a.rows,
+                                             a.ridx, a.fma);
         if (lane == src) kth = key_dist(kk);
       }
     } else if (valid) {
@@ -680,22 +666,18 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
         for (int b = 0; b < 8; ++b) {
           const int nc = min((int)((word >> (8 * b)) & 0xFF), a.capw);
           if (nc == 0) continue;
-          // the window's list in batches of eight keys (16-byte loads), then the inserts
-          const ulonglong2* cp2 =
-              reinterpret_cast<const ulonglong2*>(a.cand + ((long long)qi * NW + w0 + b) * a.capw);
-          for (int e0 = 0; e0 < nc; e0 += 8) {
-            uint64_t cb[8];
+          // the window's survivors in batches of four rows (one 16-byte load):
+          // exact keys, then the inserts below the k-th key
+          const uint4* cp4 = reinterpret_cast<const uint4*>(a.cand + ((long long)qi * NW + w0 + b) * a.capw);
+          for (int e0 = 0; e0 < nc; e0 += 4) {
+            const uint4 r4 = cp4[e0 / 4];
+            const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+            uint64_t cb[4];
 #pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-              if (e0 + 2 * e2 < nc) {
-                const ulonglong2 v = cp2[e0 / 2 + e2];
-                cb[2 * e2] = v.x;
-                cb[2 * e2 + 1] = v.y;
-              }
-            }
+            for (int e = 0; e < 4; ++e) cb[e] = e0 + e < nc ? survivor_key(qv, d, a.rows, a.ridx, rr[e], a.fma) : ~0ull;
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (e0 + e < nc && cb[e] < arr[0]) topk_insert<KB>(arr, cb[e]);
+            for (int e = 0; e < 4; ++e)
+              if (cb[e] < arr[0]) topk_insert<KB>(arr, cb[e]);
           }
         }
       }

@@ -526,6 +526,15 @@ __device__ __forceinline__ uint64_t survivor_key(const float (&qv)[kSplitMaxD], 
   return id == kIndexSentinel ? ~0ull : pack_key(acc, id);
 }
 
+// survivor_key with the query's coordinates at qp[j * qs] (shared memory)
+__device__ __forceinline__ uint64_t survivor_key_s(const float* qp, int qs, int d, const float* __restrict__ rows,
+                                                   const uint32_t* __restrict__ ridx, uint32_t row, int fma) {
+  float qv[kSplitMaxD];
+#pragma unroll
+  for (int j = 0; j < kSplitMaxD; ++j) qv[j] = j < d ? qp[j * qs] : 0.0f;
+  return survivor_key(qv, d, rows, ridx, row, fma);
+}
+
 // A top-k row of k <= 64 keys across a warp (lane j: row[j] in r0, row[32 + j]
 // in r1, ascending, ~0 past k).  Inserts cv (below the k-th key) at its rank
 // by a one-lane shift; returns the new k-th key.
@@ -588,6 +597,7 @@ __device__ __forceinline__ uint64_t warp_merge_query(uint64_t* __restrict__ row,
 template <int KB>
 __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceArgs a) {
   extern __shared__ float s_adv[];
+  __shared__ uint64_t s_keys[kAdvThreads];  // survivor keys of each warp's evaluation pass
   const int ntree = start_tree_smem(a.top.h);
   float* s_split = s_adv;
   float* myq = s_adv + ntree + threadIdx.x;  // [j][thread]: the thread's query coordinates
@@ -627,6 +637,10 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
     const float* qp = a.q + (long long)qi * a.D;
 #pragma unroll
     for (int j = 0; j < kSplitMaxD; ++j) qv[j] = (valid && j < d) ? __ldg(qp + j) : 0.0f;
+#pragma unroll
+    for (int j = 0; j < kSplitMaxD; ++j)
+      if (j < d) myq[j * kAdvThreads] = qv[j];  // (FindLeaf and the survivor evaluation read it)
+    __syncwarp();
     // 1. merge this visit's candidates (one list per window) into the top-k row
     //    (a query the rescan handled has its counts zeroed: its row and kth are final)
     if constexpr (KB >= 16) {
@@ -645,54 +659,89 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
                                              a.ridx, a.fma);
         if (lane == src) kth = key_dist(kk);
       }
-    } else if (valid) {
-      // register top-k (descending, sentinel-padded: leafscan.cuh merge_queue)
-      uint64_t arr[KB];
-      bool loaded = false;
-      uint64_t* row = a.keys + (long long)qi * k;
-      for (int w0 = 0; w0 < NW; w0 += 8) {
+    } else {
+      // (k <= 10) The warp's survivors, 32 per pass, one per lane: each lane evaluates
+      // one (owner query, row) pair exactly (the owner's coordinates by
+      // shuffle), the keys go through shared memory, and every owner inserts
+      // its own keys into its register top-k (descending, sentinel-padded:
+      // leafscan.cuh merge_queue).
+      const uint32_t full = 0xffffffffu;
+      int S = 0;
+      bool any = false;
+      for (int w0 = 0; w0 < NW && valid; w0 += 8) {
         const uint64_t word = w0 == 0 ? word0 : counts8(w0);
-        if (word == 0) continue;
-        if ((NW & 7) == 0) {
-          *reinterpret_cast<uint64_t*>(cc + w0) = 0ull;
-        } else {
-          for (int w = w0; w < min(NW, w0 + 8); ++w) cc[w] = 0;
+        any |= word != 0ull;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) S += min((int)((word >> (8 * b)) & 0xFF), a.capw);
+      }
+      int incl = S;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int off = incl - S;
+      const int T = __shfl_sync(full, incl, 31);
+      if (T > 0) {
+        uint64_t arr[KB];
+        bool loaded = false;
+        uint64_t* row = a.keys + (long long)qi * k;
+        uint64_t* s_k = s_keys + (threadIdx.x & ~31);
+        for (int e0 = 0; e0 < T; e0 += 32) {
+          const int e = e0 + lane;
+          // owner: the last lane whose first entry is <= e (offsets are non-decreasing)
+          int own = 0;
+#pragma unroll
+          for (int stp = 16; stp > 0; stp >>= 1)
+            if (__shfl_sync(full, off, own + stp) <= e) own += stp;
+          int idx = e - __shfl_sync(full, off, own);
+          const int oq = __shfl_sync(full, qi, own);
+          // the owner's window holding its entry idx (walk its counts)
+          int wsel = 0;
+          if (e < T) {
+            const uint8_t* occ = a.ccnt + (long long)oq * NW;
+            for (;; ++wsel) {
+              const int c = min((int)occ[wsel], a.capw);
+              if (idx < c) break;
+              idx -= c;
+            }
+          }
+          // the owner's coordinates: its column of myq
+          s_k[lane] = e < T ? survivor_key_s(myq - lane + own, kAdvThreads, d, a.rows, a.ridx,
+                                             __ldg(a.cand + ((long long)oq * NW + wsel) * a.capw + idx), a.fma)
+                            : ~0ull;
+          __syncwarp();
+          const int b0 = max(off, e0) - e0, b1 = min(off + S, e0 + 32) - e0;
+          if (b0 < b1) {
+            if (!loaded) {
+#pragma unroll
+              for (int j = 0; j < KB; ++j) arr[j] = j < k ? row[k - 1 - j] : 0ull;
+              loaded = true;
+            }
+            for (int x = b0; x < b1; ++x) {
+              const uint64_t c = s_k[x];
+              if (c < arr[0]) topk_insert<KB>(arr, c);
+            }
+          }
+          __syncwarp();
         }
-        if (!loaded) {
+        if (loaded) {
 #pragma unroll
-          for (int j = 0; j < KB; ++j) arr[j] = j < k ? row[k - 1 - j] : 0ull;
-          loaded = true;
+          for (int j = 0; j < KB; ++j)
+            if (j < k) row[k - 1 - j] = arr[j];
+          kth = key_dist(arr[0]);
         }
-        for (int b = 0; b < 8; ++b) {
-          const int nc = min((int)((word >> (8 * b)) & 0xFF), a.capw);
-          if (nc == 0) continue;
-          // the window's survivors in batches of four rows (one 16-byte load):
-          // exact keys, then the inserts below the k-th key
-          const uint4* cp4 = reinterpret_cast<const uint4*>(a.cand + ((long long)qi * NW + w0 + b) * a.capw);
-          for (int e0 = 0; e0 < nc; e0 += 4) {
-            const uint4 r4 = cp4[e0 / 4];
-            const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
-            uint64_t cb[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) cb[e] = e0 + e < nc ? survivor_key(qv, d, a.rows, a.ridx, rr[e], a.fma) : ~0ull;
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (cb[e] < arr[0]) topk_insert<KB>(arr, cb[e]);
+        if (any) {  // the counts were read by the evaluating lanes: cleared last
+          if ((NW & 7) == 0) {
+            for (int w0 = 0; w0 < NW; w0 += 8) *reinterpret_cast<uint64_t*>(cc + w0) = 0ull;
+          } else {
+            for (int w = 0; w < NW; ++w) cc[w] = 0;
           }
         }
-      }
-      if (loaded) {
-#pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (j < k) row[k - 1 - j] = arr[j];
-        kth = key_dist(arr[0]);
       }
     }
     if (!valid) continue;
     // 2. FindLeaf with the new k-th distance
-#pragma unroll
-    for (int j = 0; j < kSplitMaxD; ++j)
-      if (j < d) myq[j * kAdvThreads] = qv[j];
     auto qget = [myq](int j) { return myq[j * kAdvThreads]; };
     uint32_t lf = st & 0xFFFFu, pend = st >> 16;
     int nxt;
@@ -725,7 +774,7 @@ __global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceAr
       for (int j = 0; j < kSplitKT; ++j) {
         float v = 0.0f;
         if (j < d) {
-          const float qc = __fsub_rn(qv[j], cen[j]);
+          const float qc = __fsub_rn(myq[j * kAdvThreads], cen[j]);
           qn = __fmaf_rn(qc, qc, qn);
           v = __uint_as_float(tf32_rna(qc));
         } else if (j == d) {

@@ -54,6 +54,10 @@
 namespace bkt {
 
 
+#ifndef BKT_SPLIT_ONEPASS
+#define BKT_SPLIT_ONEPASS 1
+#endif
+
 constexpr int kSplitKT = 16;     // A row: d coordinates, 1.0 at column d, zeros, kth at KT-2, |q'|^2 at KT-1 (d <= 13)
 constexpr int kSplitMaxD = kSplitKT - 3;
 constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhead = 2 tiles ahead
@@ -364,6 +368,56 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
         uint32_t va[32], vb[32];
         float gmn[4];
         const float kInf = __int_as_float(0x7f800000);
+#if BKT_SPLIT_ONEPASS
+        // One pass over the four 32-column groups, each load issued while the
+        // previous group's minimum is computed; a group whose minimum passes
+        // in some lane has its survivor bitmask built from the registers it
+        // is already in, so the accumulator is released before the survivor
+        // rows are written and nothing is read from TMEM twice.  Columns past
+        // a short chunk (groups >= ngrp) hold an earlier chunk's values and
+        // are never tested.
+        auto gmask = [&](const uint32_t(&v)[32]) {
+          uint32_t mk = 0;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) mk |= (!(__uint_as_float(v[jj]) > thr) ? 1u : 0u) << jj;
+          return valid ? mk : 0u;
+        };
+        auto passes = [&](float m) { return __any_sync(0xffffffffu, valid && !(m > thr)); };
+        uint32_t mk0 = 0, mk1 = 0, mk2 = 0, mk3 = 0;
+        tmem_ld32_async(tbase, va);
+        tmem_ld32_async(tbase + 32, vb);
+        tmem_wait(va);
+        tmem_touch(vb);
+        if (passes(min32(va))) mk0 = gmask(va);
+        tmem_ld32_async(tbase + 64, va);
+        if (ngrp > 1 && passes(min32(vb))) mk1 = gmask(vb);
+        tmem_ld32_async(tbase + 96, vb);
+        tmem_wait(va);
+        tmem_touch(vb);
+        if (ngrp > 2 && passes(min32(va))) mk2 = gmask(va);
+        if (ngrp > 3 && passes(min32(vb))) mk3 = gmask(vb);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+        if (A.stats) {
+          unsigned long long sv = __popc(mk0) + __popc(mk1) + __popc(mk2) + __popc(mk3);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+          if (lane == 0) atomicAdd(A.stats + 5, sv);
+        }
+        const uint32_t rbase = (uint32_t)row0;
+        auto emit = [&](uint32_t mk, uint32_t base) {
+          for (; mk; mk &= mk - 1) {
+            if (cn < capw) cdst[cn] = base + (uint32_t)(__ffs(mk) - 1);
+            ++cn;
+          }
+        };
+        emit(mk0, rbase);
+        emit(mk1, rbase + 32);
+        emit(mk2, rbase + 64);
+        emit(mk3, rbase + 96);
+        (void)gmn;
+#else
         // all four groups unconditionally (columns past a short chunk hold an
         // earlier chunk's values and are masked below), each load issued
         // while the previous group's minimum is computed
@@ -421,6 +475,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
+#endif
         if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 4] = clock64();
       }
       if (cn > 0) {

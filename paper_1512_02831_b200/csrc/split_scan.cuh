@@ -650,7 +650,7 @@ __device__ __forceinline__ uint64_t warp_merge_query(uint64_t* __restrict__ row,
 }
 
 template <int KB>
-__global__ void __launch_bounds__(kAdvThreads, 3) advance_kernel(const AdvanceArgs a) {
+__global__ void __launch_bounds__(kAdvThreads, 4) advance_kernel(const AdvanceArgs a) {
   extern __shared__ float s_adv[];
   __shared__ uint64_t s_keys[kAdvThreads];  // survivor keys of each warp's evaluation pass
   const int ntree = start_tree_smem(a.top.h);
@@ -880,7 +880,7 @@ struct RouteArgs {
 
 // pass 1: masks, per-key counts, each route tile's base slot per window; pairs
 __global__ void __launch_bounds__(kRouteThreads) route_kernel(const RouteArgs a) {
-  __shared__ uint64_t s_box[kMaxWin * kSplitMaxD];  // per window, per dimension f32x2 {lo, -hi}
+  __shared__ __align__(16) uint64_t s_box[kMaxWin * kSplitMaxD];  // per window, per dimension f32x2 {lo, -hi}
   __shared__ int s_cnt[kMaxWin];
   const int nt = a.ctl->num_tiles;
   const int d = a.d;
@@ -893,42 +893,75 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const RouteArgs a)
     for (int e = threadIdx.x; e < nw * d; e += blockDim.x) s_box[e] = __ldg(gbox + e);
     for (int e = threadIdx.x; e < kMaxWin; e += blockDim.x) s_cnt[e] = 0;
     __syncthreads();
-    for (int r = threadIdx.x; r < rt.z; r += blockDim.x) {
-      const int p = rt.y + r;
+    // per-window counts of this lane's windows (lane w: windows w and w + 32),
+    // summed over the warp's iterations, then one shared atomic per warp and window
+    int cnt0 = 0, cnt1 = 0;
+    const int lane = threadIdx.x & 31;
+    const bool pairs2 = (d & 1) == 0 && (a.D & 1) == 0;  // 16-byte box pairs, 8-byte query pairs
+    // whole warps per iteration (the per-window counts below are kept by lane w)
+    for (int r0 = threadIdx.x & ~31; r0 < rt.z; r0 += blockDim.x) {
+      const int r = r0 + lane;
+      const bool valid = r < rt.z;
+      const int p = rt.y + (valid ? r : 0);
       const int qi = __ldg(a.work + p);
-      const float kth = __int_as_float(__ldg(reinterpret_cast<const int*>(a.qs + qi)));
+      const float kth = valid ? __int_as_float(__ldg(reinterpret_cast<const int*>(a.qs + qi))) : -1.0f;
       // {q_j, -q_j}: one packed subtraction per dimension gives {lo - q, q - hi}
       uint64_t qq[kSplitMaxD];
       const float* qp = a.q + (long long)qi * a.D;
+      if (pairs2) {
 #pragma unroll
-      for (int j = 0; j < kSplitMaxD; ++j) {
-        const float v = j < d ? __ldg(qp + j) : 0.0f;
-        qq[j] = ((uint64_t)__float_as_uint(-v) << 32) | __float_as_uint(v);
+        for (int j = 0; j < kSplitMaxD / 2; ++j) {
+          const float2 v = 2 * j < d ? __ldg(reinterpret_cast<const float2*>(qp) + j) : make_float2(0.0f, 0.0f);
+          qq[2 * j] = ((uint64_t)__float_as_uint(-v.x) << 32) | __float_as_uint(v.x);
+          qq[2 * j + 1] = ((uint64_t)__float_as_uint(-v.y) << 32) | __float_as_uint(v.y);
+        }
+        qq[kSplitMaxD - 1] = 0;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kSplitMaxD; ++j) {
+          const float v = j < d ? __ldg(qp + j) : 0.0f;
+          qq[j] = ((uint64_t)__float_as_uint(-v) << 32) | __float_as_uint(v);
+        }
       }
       unsigned long long mask = 0;
       for (int w = 0; w < nw; ++w) {
         // box lower bound in f32, relaxed by 1e-5: never above the reference distance
         const uint64_t* bx = s_box + w * d;
         float lb = 0.0f;
+        if (pairs2) {
 #pragma unroll
-        for (int j = 0; j < kSplitMaxD; ++j) {
-          if (j < d) {
-            const uint64_t df = f2_sub(bx[j], qq[j]);
-            const float e = fmaxf(fmaxf(f2_lo(df), f2_hi(df)), 0.0f);
-            lb = __fmaf_rn(e, e, lb);
+          for (int j = 0; j < kSplitMaxD / 2; ++j) {
+            if (2 * j < d) {
+              const ulonglong2 b2 = reinterpret_cast<const ulonglong2*>(bx)[j];
+              const uint64_t df0 = f2_sub(b2.x, qq[2 * j]), df1 = f2_sub(b2.y, qq[2 * j + 1]);
+              const float e0 = fmaxf(fmaxf(f2_lo(df0), f2_hi(df0)), 0.0f);
+              const float e1 = fmaxf(fmaxf(f2_lo(df1), f2_hi(df1)), 0.0f);
+              lb = __fmaf_rn(e0, e0, lb);
+              lb = __fmaf_rn(e1, e1, lb);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < kSplitMaxD; ++j) {
+            if (j < d) {
+              const uint64_t df = f2_sub(bx[j], qq[j]);
+              const float e = fmaxf(fmaxf(f2_lo(df), f2_hi(df)), 0.0f);
+              lb = __fmaf_rn(e, e, lb);
+            }
           }
         }
         if (!(lb * 0.99999f > kth)) mask |= 1ull << w;
       }
-      a.qmask[p] = mask;
-      // per-window counts: one shared atomic per warp and window
-      const unsigned act = __activemask();
-      const int leader = __ffs(act) - 1;
+      if (valid) a.qmask[p] = mask;
       for (int w = 0; w < nw; ++w) {
-        const unsigned b = __ballot_sync(act, (mask >> w) & 1ull);
-        if ((int)(threadIdx.x & 31) == leader && b) atomicAdd(&s_cnt[w], __popc(b));
+        const int c = __popc(__ballot_sync(0xffffffffu, (mask >> w) & 1ull));
+        if (lane == (w & 31)) {
+          if (w < 32) cnt0 += c; else cnt1 += c;
+        }
       }
     }
+    if (lane < nw && cnt0) atomicAdd(&s_cnt[lane], cnt0);
+    if (lane + 32 < nw && cnt1) atomicAdd(&s_cnt[lane + 32], cnt1);
     __syncthreads();
     for (int w = threadIdx.x; w < nw; w += blockDim.x) {
       const int c = s_cnt[w];

@@ -327,6 +327,11 @@ def main() -> None:
     info = gpu.info()
 
     q_dev = torch.from_numpy(queries).to(dev_t)
+    # e2e inputs live in page-locked host memory (the contract's "pinned host
+    # memory"): filled once here, outside every timed region
+    from paper_1512_02831_b200 import _native
+    queries_h = _native.pinned_empty(queries.shape, np.float32)
+    queries_h[...] = queries
     keys_dev = torch.empty((max(m, 1), K), dtype=torch.int64, device=dev_t)
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev_t)
 
@@ -378,7 +383,7 @@ def main() -> None:
             torch.cuda.synchronize()
             barrier()
             w0 = time.perf_counter()
-            res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=K), device=gpu, exact=exact, kernel=a.kernel)
+            res = bkt.lazy_search(tree, queries_h, bkt.SearchParams(k=K), device=gpu, exact=exact, kernel=a.kernel)
             w1 = time.perf_counter()
             barrier()
             if i >= e2e_warm:
@@ -405,6 +410,7 @@ def main() -> None:
     value = job_value(w["total"], a.steps, [dev_ms_max / 1e3])
     if e2e is not None:
         e2e = {"value": job_value(w["total"], e2e["steps"], [red["e2e_s_max"]]), "unit": UNIT,
+               "inputs": "queries in page-locked host memory (bkt_host_alloc), keys returned into host arrays",
                "h2d_bytes_per_step": int(m * DIM * 4), "d2h_bytes_per_step": int(m * K * 8)}
     parity = None
     if ok is not None:

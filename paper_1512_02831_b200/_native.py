@@ -194,6 +194,20 @@ class _PinnedPool:
 _PINNED = _PinnedPool(max_bytes=0 if os.environ.get("BKT_NO_PINNED_POOL") else 4 << 30)
 
 
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A page-locked host array (bkt_host_alloc), freed when the array is
+    collected.  Query arrays in page-locked memory reach the device in one
+    direct DMA (bkt_search skips its staging copy)."""
+    dt = np.dtype(dtype)
+    nbytes = max(1, int(np.prod(shape)) * dt.itemsize)
+    addr = lib().bkt_host_alloc(nbytes)
+    if not addr:
+        raise MemoryError(f"bkt_host_alloc({nbytes}) failed")
+    buf = (ctypes.c_char * nbytes).from_address(addr)
+    weakref.finalize(buf, lib().bkt_host_free, addr)
+    return np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+
 def host_empty(shape, dtype) -> np.ndarray:
     """np.empty for large host result arrays.
 

@@ -476,6 +476,17 @@ void free_stageset(bkt_ctx::StageSet& S) {
 int h2d_staged(bkt_ctx* ctx, bkt_ctx::StageSet& S, void* dst, const void* src, size_t bytes) {
   int rc = ensure_stageset(ctx, S);
   if (rc != BKT_OK) return rc;
+  {
+    // page-locked source (e.g. bkt_host_alloc): one direct DMA, no staging copy
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // pageable memory reports an error on some drivers: clear it
+    if (pinned) {
+      CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S.stream));
+      CU(cudaStreamSynchronize(S.stream));
+      return BKT_OK;
+    }
+  }
   size_t off = 0;
   for (int i = 0; off < bytes; ++i) {
     const int s = i & 1;

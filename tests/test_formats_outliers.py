@@ -153,6 +153,32 @@ class TestSelfMatches:
                 bkt.self_excluded_knn(pts, k, oracle_engine)
 
 
+class TestExhaustiveStructure:
+    """brute_knn's two-leaf structure with a NaN root split, checked on the
+    CPU with the oracle's restatement of the reference traversal
+    (kdtree.py:157-204): every query descends right (q < NaN is false) and
+    visits the left leaf too ((q - NaN)^2 > kth is false), so the traversal
+    is a full scan and its keys are the brute-force keys."""
+
+    def test_traversal_is_brute_force(self, rng):
+        refs = rng.random((3001, 6), dtype=np.float32)
+        refs[100:140] = refs[:40]  # duplicates: ties broken by index
+        q = rng.random((400, 6), dtype=np.float32)
+        t = bkt.exhaustive_tree(refs)
+        assert t.top.height == 1 and np.isnan(t.top.split_values[0])
+        assert list(t.leaves.leaf_starts) == [0, 1500, 3001]
+        ot = O.OracleTree(1, 6, t.top.split_values, np.ascontiguousarray(t.leaves.points), t.leaves.original_index,
+                          t.leaves.leaf_starts)
+        for k in (1, 7, 40):
+            r = O.knn_tree(ot, q, k, threads=2)
+            assert np.array_equal(r["keys"], O.brute_keys(refs, q, k, threads=2))
+            assert np.all(r["visited"] == 2)
+
+    def test_needs_two_points(self):
+        with pytest.raises(ValueError):
+            bkt.exhaustive_tree(np.zeros((1, 3), np.float32))
+
+
 @pytest.mark.gpu
 class TestGpuBrute:
     def test_brute_matches_oracle(self, rng, gpu_device):

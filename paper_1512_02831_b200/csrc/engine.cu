@@ -1434,7 +1434,7 @@ int enqueue_split_round(bkt_ctx* ctx, SearchRun& R, int cur, int slot, cudaEvent
       sa.dbg = sdbg;
       sa.dbg_cap = kDbgCap;
     }
-    CU(launch_splitscan(R.fma, R.grid_scan, ctx->stream, sa));
+    CU(launch_splitscan(R.fma, kSplitCtas * ctx->sm_count, ctx->stream, sa));
     if (sdbg_now) {
       // per tile: published (producer), afull wait start/ready (epilogue), afull ready (MMA);
       // per chunk: MMA issued, epilogue tfull wait start/ready, released, TMA issued, full ready (MMA)

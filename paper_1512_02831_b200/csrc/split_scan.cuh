@@ -61,7 +61,15 @@ namespace bkt {
 constexpr int kSplitKT = 16;     // A row: d coordinates, 1.0 at column d, zeros, kth at KT-2, |q'|^2 at KT-1 (d <= 13)
 constexpr int kSplitMaxD = kSplitKT - 3;
 constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhead = 2 tiles ahead
-constexpr int kSplitStages = 8;  // TMA ring stages (128-row chunks of the B operand)
+// CTAs per SM: 2 (two 128-column TMEM accumulators each, 8 TMA stages) or
+// 3 (one accumulator each, 4 stages): with one accumulator a CTA's MMA and
+// epilogue alternate, and three CTAs interleave on the SM's tensor core
+#ifndef BKT_SPLIT_CTAS
+#define BKT_SPLIT_CTAS 2
+#endif
+constexpr int kSplitCtas = BKT_SPLIT_CTAS;
+constexpr int kSplitAcc = kSplitCtas >= 3 ? 1 : 2;  // TMEM accumulators per CTA
+constexpr int kSplitStages = kSplitCtas >= 3 ? 4 : 8;  // TMA ring stages (128-row chunks of the B operand)
 constexpr int kSplitThreads = 192;
 // Survivor entries (u32 rows of the tensor-core layout) per (query, window)
 // slice: 32 for leaves of <= 8 windows, at least 16 for leaves of more (the
@@ -112,7 +120,7 @@ struct SplitSmem {
   static constexpr int kNumBars = 2 * kSplitStages + 4 + 2 * kSplitNA;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
   static_assert(sizeof(SplitWin) <= 32, "window record");
-  static_assert(kBytes <= tc_smem_per_cta(2), "split scan shared memory exceeds half an SM");
+  static_assert(kBytes <= tc_smem_per_cta(kSplitCtas), "split scan shared memory exceeds the SM's share");
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -124,7 +132,7 @@ __host__ __device__ __forceinline__ int canon_off(int r, int k, int KT) {
   return (r >> 3) * (KT * 8) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
 }
 
-__global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const SplitScanArgs A) {
+__global__ void __launch_bounds__(kSplitThreads, kSplitCtas) splitscan_tc_kernel(const SplitScanArgs A) {
   using S = SplitSmem;
   constexpr int KT = kSplitKT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
   uint64_t* full = bars;                       // [stages] TMA -> MMA
   uint64_t* empty = bars + kSplitStages;       // [stages] MMA completion (tcgen05.commit) -> TMA
   uint64_t* tfull = bars + 2 * kSplitStages;   // [2] MMA -> epilogue
-  uint64_t* tempty = tfull + 2;                // [2] epilogue -> MMA
+  uint64_t* tempty = tfull + 2;                // [kSplitAcc] epilogue -> MMA
   uint64_t* afull = tempty + 2;                // [NA] producer (A rows, ids, tile record) -> MMA, epilogue
   uint64_t* aempty = afull + kSplitNA;         // [NA] MMA (tile issued) + 4 epilogue warps -> producer
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + S::kNumBars);
@@ -150,7 +158,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kSplitAcc; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kTcEpiWarps);
     }
@@ -162,7 +170,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
   }
   if (warp == 5) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(s_tmem)),
-                 "r"(256));
+                 "r"(128 * kSplitAcc));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
         tc_fence_after();
         for (int c = win.cb; c < win.ce; ++c, ++g) {
           const int s = g % kSplitStages;
-          const uint32_t b = g & 1u, use = g >> 1;
+          const uint32_t b = g % kSplitAcc, use = g / kSplitAcc;
           mbar_wait(&full[s], (g / kSplitStages) & 1u);
           if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * A.dbg_cap + 8 * g + 6] = clock64();
           if (use > 0) mbar_wait(&tempty[b], (use - 1) & 1u);
@@ -356,10 +364,10 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
       uint32_t* cdst = A.cand + ((long long)qi * A.NW + rec.w) * capw;
 
       for (int c = win.cb; c < win.ce; ++c, ++g) {
-        const uint32_t b = g & 1u;
+        const uint32_t b = g % kSplitAcc;
         const bool dbg_c = dbg_on && (int)g < A.dbg_cap;
         if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 2] = clock64();
-        mbar_wait(&tfull[b], (g >> 1) & 1u);
+        mbar_wait(&tfull[b], (g / kSplitAcc) & 1u);
         if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 3] = clock64();
         tc_fence_after();
         const long long row0 = win.r0 + (long long)c * 128;
@@ -492,7 +500,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) splitscan_tc_kernel(const Sp
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128 * kSplitAcc));
   }
 }
 

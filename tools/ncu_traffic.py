@@ -25,7 +25,7 @@ def main(rep, trace, rnd, n, nl):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd = float(d["dram__bytes_read.sum"]) * scale[u["dram__bytes_read.sum"]]
     wr = float(d["dram__bytes_write.sum"]) * scale[u["dram__bytes_write.sum"]]
-    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}
+    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
     ms = float(d["gpu__time_duration.sum"]) * tscale[u["gpu__time_duration.sum"]]
     active = None
     for line in open(trace):

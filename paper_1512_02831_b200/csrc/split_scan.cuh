@@ -60,16 +60,18 @@ namespace bkt {
 
 constexpr int kSplitKT = 16;     // A row: d coordinates, 1.0 at column d, zeros, kth at KT-2, |q'|^2 at KT-1 (d <= 13)
 constexpr int kSplitMaxD = kSplitKT - 3;
-constexpr int kSplitNA = 4;      // A operand buffers: the producer gathers kAhead = 2 tiles ahead
-// CTAs per SM: 2 (two 128-column TMEM accumulators each, 8 TMA stages) or
-// 3 (one accumulator each, 4 stages): with one accumulator a CTA's MMA and
-// epilogue alternate, and three CTAs interleave on the SM's tensor core
 #ifndef BKT_SPLIT_CTAS
-#define BKT_SPLIT_CTAS 2
+#define BKT_SPLIT_CTAS 3
 #endif
+constexpr int kSplitNA = BKT_SPLIT_CTAS >= 4 ? 3 : 4;  // A operand buffers: the producer gathers kAhead = 2 tiles ahead
+// CTAs per SM: 2 (two 128-column TMEM accumulators each, 8 TMA stages), 3
+// (one accumulator each, 4 stages) or 4 (one accumulator, 3 stages, 3 A
+// buffers): with one accumulator a CTA's MMA and epilogue alternate and the
+// CTAs interleave on the SM's tensor core (config 2: 2 -> 3 CTAs 48.7 ->
+// 52.5 M q/s)
 constexpr int kSplitCtas = BKT_SPLIT_CTAS;
 constexpr int kSplitAcc = kSplitCtas >= 3 ? 1 : 2;  // TMEM accumulators per CTA
-constexpr int kSplitStages = kSplitCtas >= 3 ? 4 : 8;  // TMA ring stages (128-row chunks of the B operand)
+constexpr int kSplitStages = kSplitCtas >= 4 ? 3 : (kSplitCtas == 3 ? 4 : 8);  // TMA ring stages (128-row chunks)
 constexpr int kSplitThreads = 192;
 // Survivor entries (u32 rows of the tensor-core layout) per (query, window)
 // slice: 32 for leaves of <= 8 windows, at least 16 for leaves of more (the

@@ -151,7 +151,8 @@ class _PinnedPool:
 
     def _fill(self, nbytes: int) -> None:
         # page-lock buffers of this size one after another up to `per_size`
-        # (a caller that keeps its previous result alive needs two)
+        # (a caller that keeps its previous result alive needs two; a third
+        # covers one more live reference, e.g. a checker's copy)
         while True:
             with self._lock:
                 if self._held + nbytes > self._max or self._count.get(nbytes, 0) >= self._per_size:
@@ -191,7 +192,7 @@ class _PinnedPool:
             self._free.setdefault(nbytes, []).append(addr)
 
 
-_PINNED = _PinnedPool(max_bytes=0 if os.environ.get("BKT_NO_PINNED_POOL") else 4 << 30)
+_PINNED = _PinnedPool(max_bytes=0 if os.environ.get("BKT_NO_PINNED_POOL") else 6 << 30, per_size=3)
 
 
 def pinned_empty(shape, dtype) -> np.ndarray:

@@ -1139,8 +1139,9 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.tile_next = &ctx->ctl->tile_next;
     if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e);
     const char* dbg_env = std::getenv("BKT_TC_DEBUG");
-    if (dbg_env && R.leafscan_launches == (std::atoi(dbg_env) > 1 ? std::atoi(dbg_env) : 5)) {
-      // per-chunk timestamps of CTA 0 in one leafscan launch (BKT_TC_DEBUG=<launch>, default the 6th)
+    if (dbg_env && R.leafscan_launches == (*dbg_env ? std::atoi(dbg_env) : 5)) {
+      // per-chunk timestamps of CTA 0 in one leafscan launch (BKT_TC_DEBUG=<launch>: 0 is the home
+      // round; empty: the 6th)
       static long long* dbg = nullptr;
       const int cap = 4096;
       const int extra = 2048;  // per-CTA start / end stamps

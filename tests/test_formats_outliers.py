@@ -228,3 +228,34 @@ class TestGpuBrute:
         _, sq = bkt.self_excluded_knn(pts, 10)
         order = bkt.rank_outliers(bkt.outlier_scores(sq))
         assert set(order[:6].tolist()) == set(planted.tolist())
+
+
+class TestCli:
+    """The command-line front end (reference cli.py:105-177)."""
+
+    def test_parser(self):
+        from paper_1512_02831_b200 import cli
+        a = cli.build_parser().parse_args(["query", "--refs", "r.bknn", "--queries", "q.bknn", "--k", "7",
+                                           "--engine", "brute", "--num-chunks", "3"])
+        assert (a.cmd, a.k, a.engine, a.num_chunks) == ("query", 7, "brute", 3)
+        with pytest.raises(SystemExit):
+            cli.build_parser().parse_args(["query", "--refs", "r.bknn", "--queries", "q", "--engine", "kdtree-cpu"])
+
+    @pytest.mark.gpu
+    def test_query_and_build_on_files(self, rng, tmp_path):
+        import json
+        from paper_1512_02831_b200 import cli
+        refs = rng.random((5000, 6), dtype=np.float32)
+        q = rng.random((700, 6), dtype=np.float32)
+        bkt.write_dataset(tmp_path / "r.bknn", bkt.PointMatrix(refs))
+        bkt.write_dataset(tmp_path / "q.csv", bkt.PointMatrix(q), fmt="csv")
+        rep = tmp_path / "rep.json"
+        assert cli.main(["query", "--refs", str(tmp_path / "r.bknn"), "--queries", str(tmp_path / "q.csv"),
+                         "--k", "5", "--height", "5", "--out", str(tmp_path / "nn.npz"),
+                         "--report-out", str(rep)]) == 0
+        got = np.load(tmp_path / "nn.npz")
+        want = O.brute_keys(refs, bkt.load_dataset(tmp_path / "q.csv").data, 5)
+        wd, wi = bkt.unpack_keys(want)
+        assert np.array_equal(got["indices"], wi) and np.array_equal(got["sq_dists"], wd)
+        assert json.load(open(rep))["digest"] == bkt.result_digest(bkt.NeighborBatch.from_keys(want, 5))
+        assert cli.main(["build", "--refs", str(tmp_path / "r.bknn"), "--height", "6", "--on-gpu"]) == 0

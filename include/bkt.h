@@ -122,6 +122,22 @@ int bkt_scan_groups(bkt_ctx* ctx, const float* points, const int64_t* ids, int64
                     const int64_t* group_ptr, const int64_t* group_rows, const int64_t* group_lo,
                     const int64_t* group_hi, int32_t exact);
 
+/* The same seam with device-resident chunk slots (SimulatedDevice
+ * enqueue_copy / enqueue_brute_kernel, device.py:256-337, as driven by
+ * ChunkPipeline, device.py:367-457).  bkt_seam_copy uploads a chunk (L
+ * points of d coordinates + ids) into slot 0 or 1 on the context's copy
+ * stream and returns at once when `points` is page-locked (an event marks
+ * the copy's completion; bkt_seam_sync waits for it).  bkt_seam_scan runs the
+ * group scan against a resident slot on the compute stream after that copy,
+ * moving only the query rows and top-k rows the groups name, one warp per
+ * distinct row (all of a row's ranges merged in one pass); keys (m, k) host
+ * array is merged in place.  Same arguments and errors as bkt_scan_groups. */
+int bkt_seam_copy(bkt_ctx* ctx, int32_t slot, const float* points, const int64_t* ids, int64_t L, int32_t d);
+int bkt_seam_sync(bkt_ctx* ctx, int32_t slot);
+int bkt_seam_scan(bkt_ctx* ctx, int32_t slot, const float* queries, int64_t m, int32_t k, uint64_t* keys,
+                  int32_t ngroups, const int64_t* group_ptr, const int64_t* group_rows, const int64_t* group_lo,
+                  const int64_t* group_hi, int32_t exact);
+
 /* FP32 pipe probe: FFMA throughput of this device (TFLOP/s) measured with
  * CUDA events; used as the measured roofline denominator. */
 int bkt_fp32_peak(bkt_ctx* ctx, double* tflops);

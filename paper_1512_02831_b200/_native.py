@@ -27,7 +27,8 @@ BKT_ESTATE = -5
 # every symbol include/bkt.h declares
 EXPORTS = ("bkt_open", "bkt_close", "bkt_last_error", "bkt_device_info", "bkt_build_tree",
            "bkt_build_tree_device", "bkt_build_tree_device_error", "bkt_load_tree", "bkt_search",
-           "bkt_scan_groups", "bkt_fp32_peak", "bkt_host_alloc", "bkt_host_free")
+           "bkt_scan_groups", "bkt_seam_copy", "bkt_seam_sync", "bkt_seam_scan", "bkt_fp32_peak",
+           "bkt_host_alloc", "bkt_host_free")
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -101,6 +102,9 @@ def lib() -> ctypes.CDLL:
         L.bkt_load_tree.argtypes = [P, i32, i32, i64, P, P, P, P, i32, i32, P]
         L.bkt_search.argtypes = [P, P, i64, i32, ctypes.POINTER(SearchOpts), P, ctypes.POINTER(Stats)]
         L.bkt_scan_groups.argtypes = [P, P, P, i64, i32, P, i64, i32, P, i32, P, P, P, P, i32]
+        L.bkt_seam_copy.argtypes = [P, i32, P, P, i64, i32]
+        L.bkt_seam_sync.argtypes = [P, i32]
+        L.bkt_seam_scan.argtypes = [P, i32, P, i64, i32, P, i32, P, P, P, P, i32]
         L.bkt_fp32_peak.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
         L.bkt_host_alloc.argtypes = [i64]
         L.bkt_host_alloc.restype = P

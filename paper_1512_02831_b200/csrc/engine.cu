@@ -34,6 +34,7 @@
 #include "round_kernels.cuh"
 #include "split_launch.cuh"
 #include "wide_search.cuh"
+#include "seam.h"
 
 using namespace bkt;
 
@@ -196,6 +197,7 @@ struct bkt_ctx {
   int4* stiles = nullptr;
   long long stiles_cap = 0;
 
+  bkt_internal::SeamSlot seam[bkt_internal::kSeamSlots];  // fine seam chunk slots (misc.cu)
   std::vector<cudaEvent_t> ev_pool;   // leafscan timing events
   cudaEvent_t ring_ev[4] = {};        // round-check ring (kRing)
   cudaEvent_t group_ev[2] = {};       // graph mode: end of the last two round groups
@@ -754,6 +756,10 @@ void bkt_close(bkt_ctx* ctx) {
   for (int i = 0; i < 2; ++i) free_stageset(ctx->io[i]);
   dfree(ctx->q_alt); dfree(ctx->q_raw_alt); dfree(ctx->keys_alt);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& sl : ctx->seam) {
+    dfree(sl.pts); dfree(sl.ids);
+    if (sl.ready) cudaEventDestroy(sl.ready);
+  }
   for (int i = 0; i < kRing; ++i)
     if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
   for (int i = 0; i < 2; ++i)
@@ -2220,4 +2226,6 @@ namespace bkt_internal {
 int ctx_device(bkt_ctx* c) { return c->device; }
 cudaStream_t ctx_stream(bkt_ctx* c) { return c->stream; }
 int ctx_fail(bkt_ctx* c, int code, const std::string& msg) { return set_err(c, code, msg); }
+SeamSlot* ctx_seam_slot(bkt_ctx* c, int slot) { return slot >= 0 && slot < kSeamSlots ? &c->seam[slot] : nullptr; }
+cudaStream_t ctx_copy_stream(bkt_ctx* c) { return c->copy_stream; }
 }  // namespace bkt_internal

@@ -66,21 +66,28 @@ def chunk_required(n_points: int, d: int) -> int:
 
 
 class Event:
-    """Completion handle (device.py:64-88).  Commands run synchronously, so
-    an event is complete when returned; a failed command re-raises on wait."""
+    """Completion handle (device.py:64-88).  A chunk copy's event waits for
+    the CUDA event its slot recorded on the copy stream (bkt_seam_sync);
+    other commands complete before they return.  A failed command re-raises
+    on wait."""
 
-    __slots__ = ("_exc",)
+    __slots__ = ("_exc", "_sync", "_done")
 
-    def __init__(self, exc: BaseException | None = None) -> None:
+    def __init__(self, exc: BaseException | None = None, sync=None) -> None:
         self._exc = exc
+        self._sync = sync
+        self._done = sync is None
 
     @property
     def done(self) -> bool:
-        return True
+        return self._done
 
     def wait(self, timeout: float | None = None) -> None:
         if self._exc is not None:
             raise self._exc
+        if not self._done:
+            self._sync()
+            self._done = True
 
 
 @dataclass(frozen=True)
@@ -118,8 +125,11 @@ class GpuDevice:
         self.query_block_bytes = query_block_bytes
         self.hazard_violations: list[str] = []
         self.trace: list[tuple[str, str, int, int, int]] = []
+        # staged chunks live in page-locked buffers (so the slot copy is an
+        # asynchronous DMA); the device slots hold (L, d, chunk id) of their chunk
         self._staging: list[tuple[np.ndarray, np.ndarray] | None] = [None, None]
-        self._resident: list[tuple[np.ndarray, np.ndarray] | None] = [None, None]
+        self._resident: list[tuple[int, int, int] | None] = [None, None]
+        self._staged_len = [0, 0]
         self._tree_key = None
         self._tree_ref = None
         self._closed = False
@@ -257,8 +267,17 @@ class GpuDevice:
         for dep in deps:
             dep.wait()
         t0 = time.monotonic_ns()
-        self._staging[slot] = (np.ascontiguousarray(points_src, np.float32).copy(),
-                               np.ascontiguousarray(ids_src, np.int64).copy())
+        # the slot's previous copy must have left its staging buffer
+        _native.check(_native.lib().bkt_seam_sync(self.ctx, int(slot)), self.ctx)
+        cur = self._staging[slot]
+        if cur is None or cur[0].shape[0] < L or cur[0].shape[1] != d:
+            pts = _native.pinned_empty((max(L, 1), d), np.float32)
+            ids = np.empty(max(L, 1), np.int64)
+            cur = (pts, ids)
+        cur[0][:L] = points_src
+        cur[1][:L] = ids_src
+        self._staging[slot] = cur
+        self._staged_len[slot] = L
         self._record("stage", queue_id, chunk_id, t0, time.monotonic_ns())
         return Event()
 
@@ -269,9 +288,14 @@ class GpuDevice:
         for dep in deps:
             dep.wait()
         t0 = time.monotonic_ns()
-        self._resident[slot] = self._staging[slot]
+        pts, ids = self._staging[slot]
+        L = self._staged_len[slot]
+        _native.check(_native.lib().bkt_seam_copy(self.ctx, int(slot), _native.ptr(pts), _native.ptr(ids), L,
+                                                  int(pts.shape[1])), self.ctx)
+        self._resident[slot] = (L, int(pts.shape[1]), chunk_id)
         self._record("copy", queue_id, chunk_id, t0, time.monotonic_ns())
-        return Event()
+        ctx = self.ctx
+        return Event(sync=lambda: _native.check(_native.lib().bkt_seam_sync(ctx, int(slot)), ctx))
 
     def enqueue_brute_kernel(self, queue_id: str, slot: int, chunk_lo: int, chunk_hi: int, d: int,
                              groups: list, queries: np.ndarray, neighbors: NeighborBatch, chunk_id: int,
@@ -286,8 +310,8 @@ class GpuDevice:
         for dep in deps:
             dep.wait()
         t0 = time.monotonic_ns()
-        pts, ids = self._resident[slot]
-        if pts.shape[0] != chunk_hi - chunk_lo:
+        res = self._resident[slot]
+        if res is None or res[0] != chunk_hi - chunk_lo:
             raise ValueError("resident chunk does not match [chunk_lo, chunk_hi)")
         if groups:
             rows_all = np.concatenate([np.asarray(r, np.int64) for r, _, _ in groups])
@@ -299,10 +323,10 @@ class GpuDevice:
             keys = neighbors.keys
             if not keys.flags.c_contiguous:
                 raise ValueError("neighbors.keys must be C-contiguous")
-            _native.check(_native.lib().bkt_scan_groups(
-                self.ctx, _native.ptr(pts), _native.ptr(ids), pts.shape[0], int(d), _native.ptr(q),
-                q.shape[0], int(neighbors.k), _native.ptr(keys), len(groups), _native.ptr(ptr),
-                _native.ptr(rows_all), _native.ptr(glo), _native.ptr(ghi), 1), self.ctx)
+            # the scan waits for the slot's copy on the device (stream order), not on the host
+            _native.check(_native.lib().bkt_seam_scan(
+                self.ctx, int(slot), _native.ptr(q), q.shape[0], int(neighbors.k), _native.ptr(keys), len(groups),
+                _native.ptr(ptr), _native.ptr(rows_all), _native.ptr(glo), _native.ptr(ghi), 1), self.ctx)
             for rows, lo, hi in groups:
                 neighbors.counts[rows] = np.minimum(neighbors.counts[rows] + (hi - lo), neighbors.k)
         self._record("compute", queue_id, chunk_id, t0, time.monotonic_ns())
@@ -398,13 +422,16 @@ class ChunkPipeline:
             kq = "A" if j % 2 == 0 else "B"
             slot = self._slot_chunk.index(j)
             lo, hi = plan.range(j)
+            # the next chunk is staged and its copy issued into the other slot
+            # first, so the DMA (queue B) runs while this chunk's kernel (queue
+            # A) scans (device.py:432-446)
+            if N > 1:
+                nxt = j + 1 if j + 1 < N else 0
+                self._load(nxt, "B" if kq == "A" else "A")
             if groups_per_chunk[j]:
                 ev = self.device.enqueue_brute_kernel(kq, slot, lo, hi, d, groups_per_chunk[j], queries,
                                                       neighbors, chunk_id=j)
                 self.device.wait(ev)
-            nxt = j + 1 if j + 1 < N else 0
-            if N > 1 or self._slot_chunk[0] is None:
-                self._load(nxt, "B" if kq == "A" else "A")
 
     def close(self) -> None:
         pass

@@ -37,6 +37,13 @@ def oracle_check(tree, queries, keys, k, rows=512):
     return bool(np.array_equal(r["keys"], keys[:rows]))
 
 
+def _tf32_peak():
+    """Dense TF32 TFLOP/s: half the measured bf16 GEMM figure (MEASURED_PEAKS.json), else the guide's fallback."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    bf16 = json.load(open(p)).get("bf16_tflops", 1590.0) if p.exists() else 1590.0
+    return bf16 / 2
+
+
 def emit(d):
     print(json.dumps(d), flush=True)
 
@@ -142,9 +149,22 @@ def cfg4(a):
             dev.search(queries, 10, kernel=kern)  # warm-up at full size (work buffers, result pool)
             keys, st, _ = dev.search(queries, 10, kernel=kern, timing=True)
             ok = oracle_check(tree, queries, keys, 10, rows=256)
-            emit({"config": f"cfg4 mixture n=2M m={m} d={d} k=10 h=9", "kernel": kern, "qps_device": m / (st["search_ms"] / 1e3),
-                  "pairs_per_query": st["pairs"] / m, "leafscan_tflops_fp32_equiv": 3 * d * st["pairs"] / (st["leafscan_ms"] / 1e3) / 1e12,
-                  "rounds": st["rounds"], "sample_rows_match_oracle": ok})
+            scan_s = st["leafscan_ms"] / 1e3
+            line = {"config": f"cfg4 mixture n=2M m={m} d={d} k=10 h=9", "kernel": kern,
+                    "qps_device": m / (st["search_ms"] / 1e3), "pairs_per_query": st["pairs"] / m,
+                    "leafscan_tflops_fp32_equiv": 3 * d * st["pairs"] / scan_s / 1e12,
+                    "leafscan_share": st["leafscan_ms"] / st["search_ms"], "rounds": st["rounds"],
+                    "sample_rows_match_oracle": ok}
+            if kern == "auto" and d >= 8:
+                # tensor-core roofline: 2 * KT FLOPs per algorithmic pair (K = d + 1 padded to 16 / 32)
+                kt = 16 if d + 1 <= 16 else 32
+                ach = 2 * kt * st["pairs"] / scan_s / 1e12
+                line.update(roofline_tensor={"achieved": ach, "peak": _tf32_peak(), "frac": ach / _tf32_peak(),
+                                             "flops_per_pair": 2 * kt})
+            else:
+                line.update(roofline_fp32={"achieved": line["leafscan_tflops_fp32_equiv"], "peak": dev.fp32_peak_tflops(),
+                                           "frac": line["leafscan_tflops_fp32_equiv"] / dev.fp32_peak_tflops()})
+            emit(line)
         dev.close()
 
 

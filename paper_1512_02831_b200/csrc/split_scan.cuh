@@ -71,7 +71,10 @@ constexpr int kSplitNA = BKT_SPLIT_CTAS >= 4 ? 3 : 4;  // A operand buffers: the
 // 52.5 M q/s)
 constexpr int kSplitCtas = BKT_SPLIT_CTAS;
 constexpr int kSplitAcc = kSplitCtas >= 3 ? 1 : 2;  // TMEM accumulators per CTA
-constexpr int kSplitStages = kSplitCtas >= 4 ? 3 : (kSplitCtas == 3 ? 4 : 8);  // TMA ring stages (128-row chunks)
+#ifndef BKT_SPLIT_STAGES
+#define BKT_SPLIT_STAGES (BKT_SPLIT_CTAS >= 4 ? 3 : (BKT_SPLIT_CTAS == 3 ? 4 : 8))
+#endif
+constexpr int kSplitStages = BKT_SPLIT_STAGES;  // TMA ring stages (128-row chunks)
 constexpr int kSplitThreads = 192;
 // Survivor entries (u32 rows of the tensor-core layout) per (query, window)
 // slice: 32 for leaves of <= 8 windows, at least 16 for leaves of more (the

@@ -18,6 +18,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:spli
   python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --check-rows 0 > /dev/null 2>&1
 python tools/ncu_summary.py $out/splitscan_full.ncu-rep > $out/ncu_splitscan_full.txt 2>&1
 python tools/ncu_traffic.py $out/splitscan_full.ncu-rep $out/trace_rounds.err 20 2000000 512 > $out/ncu_traffic.json 2> $out/ncu_traffic.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_cfg4.csv python tools/configs.py cfg4 --m 2e6 > /dev/null 2>&1
+python tools/launch_summary.py $out/launches_cfg4.csv > $out/launches_cfg4_summary.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:leafscan_tc -s 0 -c 1 -o $out/leafscan_home_full \
   python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --check-rows 0 > /dev/null 2>&1
 python tools/ncu_summary.py $out/leafscan_home_full.ncu-rep > $out/ncu_leafscan_home_full.txt 2>&1

@@ -1076,7 +1076,6 @@ struct SearchRun {
   bool renumber = false;     // search in home-bucket order (gather_rows_kernel)
   bool verbose = false;      // BKT_VERBOSE: split-round totals on stderr
   int split_from = 1;        // first split round (earlier rounds: leaf-level tiles)
-  bool seed = false;         // home round on the split path too (seed_kernel bound)
   bool drain_fired = false;
   std::function<void()> drain_start;
 };
@@ -1570,44 +1569,6 @@ int split_rounds(bkt_ctx* ctx, SearchRun& R, int cur, long long round) {
   return fin ? launch_finisher(ctx, R, fin) : BKT_OK;
 }
 
-// Every round on the split path, the home round included: the home visit's
-// filter bound from the query's home block (seed_kernel), then split rounds
-// from round 0.  On entry start_kernel has set the per-query arrays.
-int split_rounds_seeded(bkt_ctx* ctx, SearchRun& R) {
-  split_state_pack<<<R.grid_small, 256, 0, ctx->stream>>>(R.m, ctx->kthv, ctx->state, ctx->visits, ctx->next, ctx->qs);
-  CU(cudaGetLastError());
-  R.launches++;
-  CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
-  SeedArgs s{};
-  s.m = R.m;
-  s.q = ctx->q;
-  s.D = ctx->D;
-  s.d = ctx->d;
-  s.k = R.k;
-  s.fma = R.fma ? 1 : 0;
-  s.blk_base = ctx->blk_base;
-  s.nodes = ctx->nodes;
-  s.row_base = ctx->tc_row_base;
-  s.leaf_size = ctx->leaf_size;
-  s.rows = ctx->tc_rowsxyz;
-  s.centroid = ctx->tc_centroid;
-  s.arow = ctx->arow;
-  s.qs = ctx->qs;
-  s.counts = ctx->counts;
-  s.pos = ctx->pos;
-  s.list = ctx->work[1];
-  CU(launch_seed(R.kb, R.grid_small, ctx->stream, s));
-  R.launches++;
-  const int* fin = nullptr;
-  int rc = split_rounds_loop(ctx, R, 0, 0, &fin);
-  if (rc != BKT_OK) return rc;
-  split_state_unpack<<<R.grid_small, 256, 0, ctx->stream>>>(R.m, ctx->qs, ctx->kthv, ctx->state, ctx->visits,
-                                                            ctx->next);
-  CU(cudaGetLastError());
-  R.launches++;
-  return fin ? launch_finisher(ctx, R, fin) : BKT_OK;
-}
-
 int search_batch_impl(bkt_ctx* ctx, SearchRun& R);
 
 // The batch in home-bucket order: a first start/plan/scatter pass orders the
@@ -1727,11 +1688,7 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
   // is read back asynchronously and checked kRing-1 rounds later
   cudaEvent_t* ring = ctx->ring_ev;
   const bool ooc = ctx->residency == 1;
-  if (R.seed) {
-    int rc = split_rounds_seeded(ctx, R);
-    if (rc != BKT_OK) return rc;
-  }
-  while (!R.seed) {
+  for (;;) {
     // queries with a next leaf -> bucket keys (leaf, block) + counts
     // home visits (round 0) are sub-bucketed per block; later rounds key by leaf only
     const int sw = round == 0 ? ctx->sub_w : 1;
@@ -1869,7 +1826,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // auto: the tensor-core filter from d >= 8 (below that the CUDA-core scan is
   // as fast: few pairs per query and a mostly empty K=16 MMA; tools/configs.py cfg4)
   // k > 64 or a general-domain tree: the wide path (one CTA per query, wide_search.cuh)
-  R.wide = ctx->wide_only || k > kMaxK || std::getenv("BKT_FORCE_WIDE");
+  R.wide = ctx->wide_only || k > kMaxK;
   R.tc = !R.wide && ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
   R.unfused = false;
   if (const char* e = std::getenv("BKT_TC_N")) R.tc_rows = std::atoi(e) == 64 ? 64 : (std::atoi(e) == 256 ? 256 : 128);
@@ -1892,7 +1849,6 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   R.split = R.tc && !R.unfused && nw_ok && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 && R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
-  R.seed = R.split && R.split_from == 1 && std::getenv("BKT_SEED_HOME") && std::atoi(std::getenv("BKT_SEED_HOME")) != 0;
   // graph mode (opt-in, BKT_GRAPH=1): measured slower than eager launches on
   // config 1 (3.9 vs 5.0 M q/s: its rounds are bound by the kernels' own
   // fixed costs, not by host launch overhead); per-launch leaf-scan timing is

@@ -73,19 +73,6 @@ inline cudaError_t launch_advance(int kb, int grid, cudaStream_t s, const Advanc
   }
 }
 
-inline cudaError_t launch_seed(int kb, int grid, cudaStream_t s, const SeedArgs& a) {
-  switch (kb) {
-#define BKT_CASE(KB)                                  \
-  case KB:                                            \
-    seed_kernel<KB><<<grid, 256, 0, s>>>(a);          \
-    return cudaGetLastError();
-    BKT_KB_LIST(BKT_CASE)
-#undef BKT_CASE
-    default:
-      return cudaErrorInvalidValue;
-  }
-}
-
 inline cudaError_t launch_plan_split(cudaStream_t s, int* counts, int* key_off, int nkeys, int* toff, RoundCtl* ctl) {
   plan_split_kernel<<<1, kPlanThreads, 0, s>>>(counts, key_off, nkeys, toff, ctl, kNT);
   return cudaGetLastError();

@@ -861,127 +861,6 @@ __global__ void __launch_bounds__(kAdvThreads, 4) advance_kernel(const AdvanceAr
 }
 
 // ---------------------------------------------------------------------------
-// seed: the home visit on the split path.  A query's home leaf is scanned
-// like any later visit -- (leaf, window) items routed by box bounds, the
-// TF32 filter against the A row's kth, exact evaluation in advance_kernel --
-// once the query has a finite bound: the k-th smallest distance, in the
-// reference arithmetic (core.py:138-146), over the kBlockRows points of its
-// home block (the leaf-internal k-d cell it falls in, engine.cu
-// build_leaf_blocks).  Those points belong to the leaf, so the leaf's k-th
-// distance is at most the bound and every point of the leaf's top-k passes
-// the filter; the row stays EMPTY and advance_kernel merges the survivors
-// into it (a window overflow rescans the whole leaf, rescan_kernel).  The
-// result is the best k of the leaf, as the reference's first visit
-// (buffer_tree.py:451-485); the home visit itself is counted by start_kernel.
-// ---------------------------------------------------------------------------
-struct SeedArgs {
-  long long m;
-  const float* q;
-  int D;
-  int d;
-  int k;
-  int fma;
-  const int* blk_base;       // leaf-internal block trees (engine.cu LeafBlocks)
-  const int4* nodes;
-  const long long* row_base; // first row of each leaf in the split layout
-  const int* leaf_size;
-  const float* rows;         // row-major coordinates of the split layout
-  const float* centroid;
-  float* arow;
-  int4* qs;                  // packed records (split_state_pack): next = home leaf
-  int* counts;               // per leaf: the home round's bucket sizes
-  int2* pos;                 // per query: {home leaf, slot}
-  int* list;                 // identity work list of the home round
-};
-
-template <int KB>
-__global__ void __launch_bounds__(256) seed_kernel(const SeedArgs a) {
-  const int d = a.d, k = a.k;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.m;
-       i += (long long)gridDim.x * blockDim.x) {
-    int4 rec = a.qs[i];
-    const int leaf = rec.w;
-    float qv[kSplitMaxD];
-    const float* qp = a.q + i * a.D;
-#pragma unroll
-    for (int j = 0; j < kSplitMaxD; ++j) qv[j] = j < d ? __ldg(qp + j) : 0.0f;
-    // the home block (start_kernel's walk, at block resolution)
-    const int L = __ldg(a.leaf_size + leaf);
-    int b = 0;
-    const int b0 = __ldg(a.blk_base + leaf), nb = __ldg(a.blk_base + leaf + 1) - b0;
-    if (nb > 1) {
-      const int4* nd = a.nodes + (b0 - leaf);
-      int c = 0;
-      for (;;) {
-        const int4 v = __ldg(nd + c);
-        float qj = 0.0f;
-#pragma unroll
-        for (int j = 0; j < kSplitMaxD; ++j) qj = j == v.y ? qv[j] : qj;
-        c = (qj >= __int_as_float(v.x)) ? v.w : v.z;
-        if (c < 0) break;
-      }
-      b = ~c;
-    }
-    int r0 = b * kBlockRows, cnt = min(kBlockRows, L - r0);
-    if (cnt < k) {  // a short last block: the leaf's last kBlockRows rows instead
-      r0 = max(0, L - kBlockRows);
-      cnt = L - r0;
-    }
-    // the k smallest distances of the block (descending, +inf padded)
-    float arr[KB];
-#pragma unroll
-    for (int j = 0; j < KB; ++j) arr[j] = j < k ? __int_as_float(0x7f800000) : -1.0f;
-    const float* pr = a.rows + (__ldg(a.row_base + leaf) + r0) * d;
-    for (int r = 0; r < cnt; ++r, pr += d) {
-      float acc = 0.0f;
-#pragma unroll
-      for (int j = 0; j < kSplitMaxD; ++j)
-        if (j < d) {
-          const float df = __fsub_rn(qv[j], __ldg(pr + j));
-          acc = a.fma ? __fmaf_rn(df, df, acc) : __fadd_rn(acc, __fmul_rn(df, df));
-        }
-      if (acc < arr[0]) {
-#pragma unroll
-        for (int j = 0; j < KB - 1; ++j) arr[j] = arr[j + 1] > acc ? arr[j + 1] : (arr[j] > acc ? acc : arr[j]);
-        arr[KB - 1] = arr[KB - 1] > acc ? acc : arr[KB - 1];
-      }
-    }
-    const float kth = cnt >= k ? arr[0] : __int_as_float(0x7f800000);
-    // A row of the home visit: tf32(q - c) | 1 | 0.. | kth | |q - c|^2 (as advance_kernel)
-    const float4* cen4 = reinterpret_cast<const float4*>(a.centroid + (long long)leaf * kSplitKT);
-    float cen[kSplitKT];
-#pragma unroll
-    for (int j = 0; j < kSplitKT / 4; ++j) {
-      const float4 c4 = __ldg(cen4 + j);
-      cen[4 * j] = c4.x; cen[4 * j + 1] = c4.y; cen[4 * j + 2] = c4.z; cen[4 * j + 3] = c4.w;
-    }
-    float r[kSplitKT];
-    float qn = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kSplitKT; ++j) {
-      float v = 0.0f;
-      if (j < d) {
-        const float qc = __fsub_rn(qv[j], cen[j]);
-        qn = __fmaf_rn(qc, qc, qn);
-        v = __uint_as_float(tf32_rna(qc));
-      } else if (j == d) {
-        v = 1.0f;
-      }
-      r[j] = v;
-    }
-    r[kSplitKT - 2] = kth;
-    r[kSplitKT - 1] = qn;
-    float4* dst = reinterpret_cast<float4*>(a.arow + i * kSplitKT);
-#pragma unroll
-    for (int j = 0; j < kSplitKT / 4; ++j) dst[j] = make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-    rec.x = __float_as_int(kth);
-    a.qs[i] = rec;
-    a.list[i] = (int)i;
-    a.pos[i] = make_int2(leaf, warp_reserve(a.counts, leaf));
-  }
-}
-
-// ---------------------------------------------------------------------------
 // route: windows per query, one route tile = (leaf, <= kRouteQ queries of its bucket)
 // ---------------------------------------------------------------------------
 constexpr int kRouteQ = 1024;

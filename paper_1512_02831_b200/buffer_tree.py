@@ -210,7 +210,7 @@ class SearchStats:
     leaf) scans; find_leaf_seconds is fused into the scan and reported as 0;
     buffer_seconds = host wall time outside the device search.  Extra
     B200 fields: pairs (algorithmic distance pairs), leafscan_ms, search_ms,
-    kernel_launches."""
+    kernel_launches, stream_bytes."""
 
     record_sequences: bool = False
     iterations: int = 0
@@ -226,6 +226,7 @@ class SearchStats:
     search_ms: float = 0.0
     kernel_launches: int = 0
     leafscan_launches: int = 0
+    stream_bytes: int = 0  # host-resident structure: bytes streamed into the device chunk slots
 
 
 def _sequences(seq: np.ndarray, m: int) -> list[list[int]]:
@@ -320,6 +321,7 @@ def lazy_search(tree: BufferKdTree, queries, params: SearchParams, config: Buffe
         stats.search_ms += float(st["search_ms"])
         stats.kernel_launches += int(st["kernel_launches"])
         stats.leafscan_launches += int(st["leafscan_launches"])
+        stats.stream_bytes += int(st.get("stream_bytes", 0))
         if record:
             stats.leaf_sequences = _sequences(seq, m)
     return result

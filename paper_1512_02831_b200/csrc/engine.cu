@@ -94,6 +94,22 @@ struct bkt_ctx {
   cudaEvent_t slot_free[2] = {nullptr, nullptr};
   cudaEvent_t slot_ready[2] = {nullptr, nullptr};
   long long slot_quads = 0;
+  // out-of-core drain: leaf-aligned streaming units (each leaf goes to the
+  // chunk holding its first row), unit u = leaves [unit_leaf_lo[u], unit_leaf_hi[u]]
+  // = quads [unit_q[u], unit_q[u + 1]); slot_unit[s] = unit resident in slot s
+  std::vector<int> unit_leaf_lo, unit_leaf_hi;
+  std::vector<long long> unit_q;
+  int slot_unit[2] = {-1, -1};
+  int* park[2] = {nullptr, nullptr};  // park lists (queries waiting for a later unit)
+  long long park_cap = 0;
+  // host-resident tensor-core layout (rows [unit_r[u], unit_r[u + 1]) per unit) and its slots
+  float* h_tcB = nullptr;
+  uint32_t* h_tcidx = nullptr;
+  float* h_tcrows = nullptr;
+  std::vector<long long> h_row_base, unit_r;
+  float* slot_tcB[2] = {nullptr, nullptr};
+  uint32_t* slot_tcidx[2] = {nullptr, nullptr};
+  float* slot_tcrows[2] = {nullptr, nullptr};
   // tensor-core filter layout (resident trees with d <= 31)
   bool has_tc = false;
   int KT = 0;
@@ -291,7 +307,11 @@ void free_tree(bkt_ctx* c) {
   for (int s = 0; s < 2; ++s) {
     dfree(c->slot_pts[s]); dfree(c->slot_idx[s]);
     c->slot_chunk[s] = -1;
+    c->slot_unit[s] = -1;
+    dfree(c->slot_tcB[s]); dfree(c->slot_tcidx[s]); dfree(c->slot_tcrows[s]);
   }
+  c->unit_leaf_lo.clear(); c->unit_leaf_hi.clear(); c->unit_q.clear(); c->unit_r.clear(); c->h_row_base.clear();
+  hfree(c->h_tcB); hfree(c->h_tcidx); hfree(c->h_tcrows);
   c->has_tree = false;
   c->wide_only = false;
   c->wide_pts = nullptr;
@@ -306,6 +326,8 @@ void free_work(bkt_ctx* c) {
   dfree(c->pos);
   dfree(c->q); dfree(c->q_raw); dfree(c->keys); dfree(c->state); dfree(c->next); dfree(c->visits);
   dfree(c->work[0]); dfree(c->work[1]);
+  dfree(c->park[0]); dfree(c->park[1]);
+  c->park_cap = 0;
   c->cap_m = 0; c->cap_k = 0;
   dfree(c->q_alt); dfree(c->q_raw_alt); dfree(c->keys_alt);
   c->cap_alt = 0; c->cap_alt_k = 0;
@@ -841,17 +863,9 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
   CU(cudaHostAlloc(&ctx->h_pidx, idx_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
   build_quad_layout(leaf_points, original_index, leaf_starts, nl, d, D, ctx->h_quad_base, ctx->h_pts, ctx->h_pidx);
 
-  ctx->residency = residency;
-  if (residency == 0) {
-    CU(cudaMalloc(&ctx->pts, pts_bytes));
-    CU(cudaMalloc(&ctx->pidx, idx_bytes));
-    CU(cudaMemcpy(ctx->pts, ctx->h_pts, pts_bytes, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(ctx->pidx, ctx->h_pidx, idx_bytes, cudaMemcpyHostToDevice));
-    hfree(ctx->h_pts);
-    hfree(ctx->h_pidx);
-    ctx->num_chunks = 1;
-    ctx->wide_pts = ctx->pts;
-    ctx->wide_pidx = ctx->pidx;
+  // tensor-core filter layout (d + 1 <= 32); host_big: its row arrays stay in
+  // page-locked host memory (host-resident structure)
+  auto build_tc = [&](bool host_big) -> int {
     if (d + 1 <= 32 && !wide_only) {
       const int KT = (d + 1 <= 16) ? 16 : 32;
       std::vector<long long> rb(nl + 1, 0);
@@ -875,14 +889,26 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       }
       CU(cudaMalloc(&ctx->tc_pnmax, sizeof(float) * nl));
       CU(cudaMemcpy(ctx->tc_pnmax, hpn.data(), sizeof(float) * nl, cudaMemcpyHostToDevice));
-      CU(cudaMalloc(&ctx->tc_B, sizeof(float) * R * KT));
-      CU(cudaMalloc(&ctx->tc_idx, sizeof(uint32_t) * R));
-      CU(cudaMalloc(&ctx->tc_rowsxyz, sizeof(float) * R * d));
       CU(cudaMalloc(&ctx->tc_row_base, sizeof(long long) * (nl + 1)));
       CU(cudaMalloc(&ctx->tc_centroid, sizeof(float) * nl * KT));
-      CU(cudaMemcpy(ctx->tc_B, hB.data(), sizeof(float) * R * KT, cudaMemcpyHostToDevice));
-      CU(cudaMemcpy(ctx->tc_idx, hidx.data(), sizeof(uint32_t) * R, cudaMemcpyHostToDevice));
-      CU(cudaMemcpy(ctx->tc_rowsxyz, hrows.data(), sizeof(float) * R * d, cudaMemcpyHostToDevice));
+      if (host_big) {
+        // host-resident structure: the filter operands stay in page-locked
+        // memory and stream into the drain's slots per unit (ooc_drain)
+        CU(cudaHostAlloc(&ctx->h_tcB, sizeof(float) * R * KT, cudaHostAllocPortable));
+        CU(cudaHostAlloc(&ctx->h_tcidx, sizeof(uint32_t) * R, cudaHostAllocPortable));
+        CU(cudaHostAlloc(&ctx->h_tcrows, sizeof(float) * R * d, cudaHostAllocPortable));
+        std::memcpy(ctx->h_tcB, hB.data(), sizeof(float) * R * KT);
+        std::memcpy(ctx->h_tcidx, hidx.data(), sizeof(uint32_t) * R);
+        std::memcpy(ctx->h_tcrows, hrows.data(), sizeof(float) * R * d);
+      } else {
+        CU(cudaMalloc(&ctx->tc_B, sizeof(float) * R * KT));
+        CU(cudaMalloc(&ctx->tc_idx, sizeof(uint32_t) * R));
+        CU(cudaMalloc(&ctx->tc_rowsxyz, sizeof(float) * R * d));
+        CU(cudaMemcpy(ctx->tc_B, hB.data(), sizeof(float) * R * KT, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->tc_idx, hidx.data(), sizeof(uint32_t) * R, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->tc_rowsxyz, hrows.data(), sizeof(float) * R * d, cudaMemcpyHostToDevice));
+      }
+      ctx->h_row_base = rb;
       CU(cudaMemcpy(ctx->tc_row_base, rb.data(), sizeof(long long) * (nl + 1), cudaMemcpyHostToDevice));
       CU(cudaMemcpy(ctx->tc_centroid, hcen.data(), sizeof(float) * nl * KT, cudaMemcpyHostToDevice));
       {
@@ -954,6 +980,20 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       }
       ctx->has_tc = tc_safe;
     }
+    return BKT_OK;
+  };
+  ctx->residency = residency;
+  if (residency == 0) {
+    CU(cudaMalloc(&ctx->pts, pts_bytes));
+    CU(cudaMalloc(&ctx->pidx, idx_bytes));
+    CU(cudaMemcpy(ctx->pts, ctx->h_pts, pts_bytes, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->pidx, ctx->h_pidx, idx_bytes, cudaMemcpyHostToDevice));
+    hfree(ctx->h_pts);
+    hfree(ctx->h_pidx);
+    ctx->num_chunks = 1;
+    ctx->wide_pts = ctx->pts;
+    ctx->wide_pidx = ctx->pidx;
+    if (int rc = build_tc(false)) return rc;
   } else {
     // chunk bounds: the reference row bounds (ChunkPlan.bounds) mapped to the
     // containing quad of the padded layout; results do not depend on where a
@@ -990,11 +1030,47 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       ctx->chunk_leaf_lo[j] = lo;
       ctx->chunk_leaf_hi[j] = hi;
     }
+    // leaf-aligned streaming units of the drain schedule (ooc_drain)
+    ctx->unit_leaf_lo.clear();
+    ctx->unit_leaf_hi.clear();
+    ctx->unit_q.assign(1, 0);
+    for (int l = 0, u = -1; l < nl; ++l) {
+      const long long q0 = ctx->h_quad_base[l];
+      int j = (int)(std::upper_bound(ctx->chunk_q.begin(), ctx->chunk_q.end(), q0) - ctx->chunk_q.begin()) - 1;
+      j = std::max(0, std::min(j, num_chunks - 1));
+      if (j != u) {
+        if (!ctx->unit_leaf_lo.empty()) ctx->unit_q.push_back(q0);
+        ctx->unit_leaf_lo.push_back(l);
+        ctx->unit_leaf_hi.push_back(l);
+        u = j;
+      } else {
+        ctx->unit_leaf_hi.back() = l;
+      }
+    }
+    ctx->unit_q.push_back(ctx->h_quad_base[nl]);
+    for (size_t u = 0; u + 1 < ctx->unit_q.size(); ++u) maxq = std::max(maxq, ctx->unit_q[u + 1] - ctx->unit_q[u]);
     ctx->slot_quads = std::max<long long>(maxq, 1);
+    // tensor-core drain: the filter layout stays on the host, streamed per unit
+    if (int rc = build_tc(true)) return rc;
+    if (ctx->has_tc) {
+      long long maxr = 1;
+      ctx->unit_r.clear();
+      for (size_t u = 0; u < ctx->unit_leaf_lo.size(); ++u) {
+        ctx->unit_r.push_back(ctx->h_row_base[ctx->unit_leaf_lo[u]]);
+        maxr = std::max(maxr, ctx->h_row_base[ctx->unit_leaf_hi[u] + 1] - ctx->h_row_base[ctx->unit_leaf_lo[u]]);
+      }
+      ctx->unit_r.push_back(ctx->h_row_base[nl]);
+      for (int s = 0; s < 2; ++s) {
+        CU(cudaMalloc(&ctx->slot_tcB[s], sizeof(float) * maxr * ctx->KT));
+        CU(cudaMalloc(&ctx->slot_tcidx[s], sizeof(uint32_t) * maxr));
+        CU(cudaMalloc(&ctx->slot_tcrows[s], sizeof(float) * maxr * d));
+      }
+    }
     for (int s = 0; s < 2; ++s) {
       CU(cudaMalloc(&ctx->slot_pts[s], sizeof(float) * ctx->slot_quads * 4 * D));
       CU(cudaMalloc(&ctx->slot_idx[s], sizeof(uint32_t) * ctx->slot_quads * 4));
       ctx->slot_chunk[s] = -1;
+      ctx->slot_unit[s] = -1;
     }
   }
   if (wide_only) {
@@ -1067,6 +1143,10 @@ struct SearchRun {
   long long finish_at = -1;  // tail finisher: one launch once at most this many queries remain (-1: off)
   bool finish_cta = false;   // finisher with one CTA per query (else one warp per query)
   bool split = false;        // later rounds as (leaf, window) items (split_scan.cuh)
+  const float* unit_B = nullptr;       // drain: the resident unit's filter rows (row-indexed, origin applied)
+  const uint32_t* unit_idx = nullptr;
+  const float* unit_rows = nullptr;
+  bool drain = true;         // out-of-core: drain schedule (ooc_drain); BKT_OOC_ROUNDS=1: one round per leaf visit
   bool graph = false;        // split rounds replayed from a captured CUDA graph (launch-bound searches)
   long long stream_bytes = 0;   // out-of-core chunk streaming (bkt_stats.stream_bytes)
   long long stream_copies = 0;
@@ -1128,9 +1208,9 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
   if (R.tc) {
     TcArgs t{};
     t.s = a;
-    t.B = ctx->tc_B;
-    t.ridx = ctx->tc_idx;
-    t.rows = ctx->tc_rowsxyz;
+    t.B = R.unit_B ? R.unit_B : ctx->tc_B;
+    t.ridx = R.unit_idx ? R.unit_idx : ctx->tc_idx;
+    t.rows = R.unit_rows ? R.unit_rows : ctx->tc_rowsxyz;
     t.row_base = ctx->tc_row_base;
     t.centroid = ctx->tc_centroid;
     t.pnmax = ctx->tc_pnmax;
@@ -1266,6 +1346,7 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
                     ctx->copy_stream);
     cudaEventRecord(ctx->slot_ready[s], ctx->copy_stream);
     ctx->slot_chunk[s] = j;
+    ctx->slot_unit[s] = -1;
     R.stream_bytes += (sizeof(float) * 4 * D + sizeof(uint32_t) * 4) * (b - a);
     R.stream_copies += 1;
     return s;
@@ -1302,7 +1383,10 @@ int ooc_round(bkt_ctx* ctx, SearchRun& R, int cur) {
 
 // One batch: queries already in ctx->q (m x D).  Runs rounds until no query is active.
 // one launch of the tail finisher over `list` (ctl->active entries)
-int launch_finisher(bkt_ctx* ctx, SearchRun& R, const int* list) {
+int launch_finisher(bkt_ctx* ctx, SearchRun& R, const int* list, const FinishUnit& fu = FinishUnit{},
+                    const float* unit_pts = nullptr, const uint32_t* unit_pidx = nullptr) {
+  const float* pts = unit_pts ? unit_pts : ctx->pts;
+  const uint32_t* pidx = unit_pidx ? unit_pidx : ctx->pidx;
   const int blocks = (int)std::max<long long>(1, (R.finish_at + kFinishWarps - 1) / kFinishWarps);
   const TopTreeView top{ctx->split, ctx->h, ctx->d};
   int* seq = R.seq ? ctx->seq_dev : nullptr;
@@ -1310,19 +1394,19 @@ int launch_finisher(bkt_ctx* ctx, SearchRun& R, const int* list) {
   if (R.finish_cta && R.fma)
     finish_cta_kernel<true><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
         list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        pts, pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap, fu);
   else if (R.finish_cta)
     finish_cta_kernel<false><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
         list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        pts, pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap, fu);
   else if (R.fma)
     finish_kernel<true><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
         list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        pts, pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap, fu);
   else
     finish_kernel<false><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
         list, ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-        ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
+        pts, pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap, fu);
   CU(cudaGetLastError());
   R.launches++;
   return BKT_OK;
@@ -1355,6 +1439,200 @@ int launch_advance_round(bkt_ctx* ctx, SearchRun& R, const int* list) {
   a.seq_cap = R.seq_cap;
   CU(launch_advance(R.kb, R.grid_small, ctx->stream, a));
   R.launches++;
+  return BKT_OK;
+}
+
+// Out-of-core drain (residency 1, the default schedule): the streaming units
+// are taken in order and each resident unit is drained -- its queries are
+// scanned, advanced and re-bucketed round after round until none of them has
+// a next leaf inside the unit -- before the next unit is used.  A query whose
+// next leaf lies in another unit is parked; a pass over the units classifies
+// the park list.  Every query's visits happen in its own traversal order with
+// the same per-visit merge, so keys, visited counts and leaf sequences equal
+// the round-synchronous schedule's (reference buffer_tree.py:523-646; results
+// do not depend on the processing schedule, reference tests 263-284); what
+// changes is the number of times a unit crosses PCIe: a depth-first traversal
+// leaves a leaf-aligned unit (a subtree when chunks are equal) once, so a
+// query needs about one pass per unit it touches instead of one round per
+// leaf (sec. 3.2 processes a chunk's buffers the same way: all
+// queries buffered for its leaves, repeatedly, while it is resident).
+// Sub-rounds are launched kRing - 1 ahead of the host's check of their
+// active count; rounds after the unit empties have no work.
+int ooc_drain(bkt_ctx* ctx, SearchRun& R) {
+  const long long m = R.m;
+  if (ctx->park_cap < m) {
+    dfree(ctx->park[0]); dfree(ctx->park[1]);
+    ctx->park_cap = 0;
+    CU(cudaMalloc(&ctx->park[0], sizeof(int) * std::max<long long>(m, 1)));
+    CU(cudaMalloc(&ctx->park[1], sizeof(int) * std::max<long long>(m, 1)));
+    ctx->park_cap = m;
+  }
+  // the start kernel's home-round buckets are not used: the drain buckets by leaf
+  CU(cudaMemsetAsync(ctx->counts, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
+  ooc_init_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->park[0], m, ctx->ctl);
+  CU(cudaGetLastError());
+  R.launches++;
+  for (int s = 0; s < 2; ++s) ctx->slot_chunk[s] = -1;  // the round schedule's slot tags
+  const int U = (int)ctx->unit_leaf_lo.size();
+  const int D = ctx->D;
+  cudaEvent_t* ring = ctx->ring_ev;
+  int plans = 0;
+  // control block of the plan launched as number `seq` in mirror slot `slot`
+  auto mirror = [&](int slot, int seq, RoundCtl& c) -> int {
+    CU(cudaEventSynchronize(ring[slot]));
+    volatile RoundCtl* v = ctx->h_ctl + slot;
+    // the event orders the plan before this read; the mapped write can trail it briefly
+    for (long long spin = 0; v->plan_seq != seq; ++spin)
+      if (spin > (1ll << 32)) return set_err(ctx, BKT_ECUDA, "out-of-core drain: control block never arrived");
+    std::memcpy(&c, const_cast<RoundCtl*>(v), sizeof(RoundCtl));
+    return BKT_OK;
+  };
+  auto plan = [&](long long slot) -> int {
+    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, 1, ctx->nl, ctx->leaf_off,
+                                                     ctx->tile_off, ctx->ctl, ctx->nl, kNT, ctx->hist, kHistCap,
+                                                     ctx->d_ctl_mirror + slot);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(ring[slot], ctx->stream));
+    R.launches++;
+    return ++plans;
+  };
+  auto scatter = [&](const int* prev, int* out) -> int {
+    scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(prev, 0, ctx->pos, ctx->qkey, ctx->key_off, out, ctx->ctl,
+                                                           ctx->leaf_off, ctx->tile_off, ctx->nl, 1, kNT, ctx->tiles,
+                                                           (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
+    CU(cudaGetLastError());
+    R.launches++;
+    return BKT_OK;
+  };
+  auto ensure_resident = [&](int u, int avoid_slot) -> int {
+    for (int s = 0; s < 2; ++s)
+      if (ctx->slot_unit[s] == u) return s;
+    int s = avoid_slot >= 0 ? (avoid_slot ^ 1) : (ctx->slot_unit[0] < 0 ? 0 : (ctx->slot_unit[1] < 0 ? 1 : 0));
+    const long long a = ctx->unit_q[u], b = ctx->unit_q[u + 1];
+    cudaStreamWaitEvent(ctx->copy_stream, ctx->slot_free[s], 0);
+    cudaMemcpyAsync(ctx->slot_pts[s], ctx->h_pts + a * 4 * D, sizeof(float) * (b - a) * 4 * D,
+                    cudaMemcpyHostToDevice, ctx->copy_stream);
+    cudaMemcpyAsync(ctx->slot_idx[s], ctx->h_pidx + a * 4, sizeof(uint32_t) * (b - a) * 4, cudaMemcpyHostToDevice,
+                    ctx->copy_stream);
+    R.stream_bytes += (sizeof(float) * 4 * D + sizeof(uint32_t) * 4) * (b - a);
+    if (R.tc) {
+      const long long r0 = ctx->unit_r[u], r1 = ctx->unit_r[u + 1], KT = ctx->KT, dd = ctx->d;
+      cudaMemcpyAsync(ctx->slot_tcB[s], ctx->h_tcB + r0 * KT, sizeof(float) * (r1 - r0) * KT, cudaMemcpyHostToDevice,
+                      ctx->copy_stream);
+      cudaMemcpyAsync(ctx->slot_tcidx[s], ctx->h_tcidx + r0, sizeof(uint32_t) * (r1 - r0), cudaMemcpyHostToDevice,
+                      ctx->copy_stream);
+      cudaMemcpyAsync(ctx->slot_tcrows[s], ctx->h_tcrows + r0 * dd, sizeof(float) * (r1 - r0) * dd,
+                      cudaMemcpyHostToDevice, ctx->copy_stream);
+      R.stream_bytes += (sizeof(float) * (KT + dd) + sizeof(uint32_t)) * (r1 - r0);
+    }
+    cudaEventRecord(ctx->slot_ready[s], ctx->copy_stream);
+    ctx->slot_unit[s] = u;
+    R.stream_copies += 1;
+    return s;
+  };
+  int a = 0;  // park[a]: the list the next classify reads
+  int cur = 0;
+  long long slot_ctr = 0;
+  // start with a unit already resident (a previous batch's last)
+  int u0 = 0;
+  for (int s = 0; s < 2; ++s)
+    if (ctx->slot_unit[s] >= 0) u0 = ctx->slot_unit[s];
+  bool done = false;
+  int idle = 0;  // consecutive units without work (a full pass of them: nothing left)
+  for (int step = 0; !done; ++step) {
+    const int u = (u0 + step) % U;
+    const int lo = ctx->unit_leaf_lo[u], hi = ctx->unit_leaf_hi[u];
+    ooc_switch_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl);
+    ooc_classify_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->park[a], ctx->ctl, ctx->next, lo, hi, ctx->counts,
+                                                               ctx->pos, ctx->park[a ^ 1]);
+    CU(cudaGetLastError());
+    R.launches += 2;
+    const int slot0 = (int)(slot_ctr++ % kRing);
+    const int seq0 = plan(slot0);
+    if (seq0 < 0) return seq0;
+    RoundCtl c0;
+    if (int rc = mirror(slot0, seq0, c0)) return rc;
+    const int list = a;
+    a ^= 1;
+    if (c0.active == 0) {
+      if (c0.park_n == 0) done = true;
+      else if (++idle > U) return set_err(ctx, BKT_ECUDA, "out-of-core drain: parked queries match no unit");
+      continue;
+    }
+    idle = 0;
+    const int s = ensure_resident(u, -1);
+    // the next unit streams into the other slot while this one drains
+    if (U > 1) ensure_resident((u + 1) % U, s);
+    scatter(ctx->park[list], ctx->work[cur]);
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->slot_ready[s], 0));
+    std::vector<int> seqs(kRing, 0);
+    long long sub = 0;
+    int parked = 0;
+    for (;;) {
+      ScanArgs sa = make_scan_args(ctx, R, cur);
+      if (R.tc) {
+        // row-indexed views of the slot (the kernel adds the leaf's global row)
+        const long long r0 = ctx->unit_r[u];
+        R.unit_B = ctx->slot_tcB[s] - r0 * ctx->KT;
+        R.unit_idx = ctx->slot_tcidx[s] - r0;
+        R.unit_rows = ctx->slot_tcrows[s] - r0 * ctx->d;
+      }
+      sa.fused = 0;
+      sa.pts = ctx->slot_pts[s];
+      sa.pidx = ctx->slot_idx[s];
+      sa.quad_origin = ctx->unit_q[u];
+      sa.clip_lo = ctx->unit_q[u];
+      sa.clip_hi = ctx->unit_q[u + 1];
+      int rc = launch_scan(ctx, R, sa);
+      if (rc != BKT_OK) return rc;
+      findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
+          ctx->work[cur], ctx->ctl, ctx->q, D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys, ctx->state,
+          ctx->next, ctx->visits, ctx->counts, ctx->pos, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos, R.seq_cap, lo,
+          hi, ctx->park[a], &ctx->ctl->park_n);
+      CU(cudaGetLastError());
+      R.launches++;
+      const int sl = (int)(slot_ctr++ % kRing);
+      seqs[sl] = plan(sl);
+      if (seqs[sl] < 0) return seqs[sl];
+      scatter(ctx->work[cur], ctx->work[cur ^ 1]);
+      cur ^= 1;
+      ++sub;
+      if (sub >= kRing - 1) {
+        const int chk = (int)((slot_ctr - (kRing - 1)) % kRing);
+        RoundCtl c;
+        if (int rc = mirror(chk, seqs[chk], c)) return rc;
+        if (c.active == 0) {
+          parked = c.park_n;
+          break;
+        }
+        if (R.finish_at >= 0 && c.active <= R.finish_at) {
+          // the unit's last queries walk the rest of their stretch inside it
+          // in one launch (work[cur]: the list the last launched round built)
+          FinishUnit fu;
+          fu.origin = ctx->unit_q[u];
+          fu.leaf_lo = lo;
+          fu.leaf_hi = hi;
+          fu.park = ctx->park[a];
+          fu.park_n = &ctx->ctl->park_n;
+          fu.kth = ctx->kthv;
+          rc = launch_finisher(ctx, R, ctx->work[cur], fu, ctx->slot_pts[s], ctx->slot_idx[s]);
+          if (rc != BKT_OK) return rc;
+          const int sf = (int)(slot_ctr++ % kRing);
+          const int seqf = plan(sf);  // no counts left: active 0, the park count mirrored
+          if (seqf < 0) return seqf;
+          RoundCtl cf;
+          if (int rf = mirror(sf, seqf, cf)) return rf;
+          parked = cf.park_n;
+          break;
+        }
+      }
+    }
+    CU(cudaEventRecord(ctx->slot_free[s], ctx->stream));
+    if (parked == 0) done = true;
+  }
+  R.unit_B = nullptr;
+  R.unit_idx = nullptr;
+  R.unit_rows = nullptr;
   return BKT_OK;
 }
 
@@ -1688,7 +1966,11 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
   // is read back asynchronously and checked kRing-1 rounds later
   cudaEvent_t* ring = ctx->ring_ev;
   const bool ooc = ctx->residency == 1;
-  for (;;) {
+  if (ooc && R.drain) {
+    int rc = ooc_drain(ctx, R);
+    if (rc != BKT_OK) return rc;
+  }
+  for (; !(ooc && R.drain);) {
     // queries with a next leaf -> bucket keys (leaf, block) + counts
     // home visits (round 0) are sub-bucketed per block; later rounds key by leaf only
     const int sw = round == 0 ? ctx->sub_w : 1;
@@ -1749,28 +2031,8 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
       if (R.finish_at >= 0 && ctx->h_ctl[chk].active <= R.finish_at) {
         // the list just scanned (work[cur ^ 1], ctl->active entries) holds
         // every query that is still active; finish them in one launch
-        const int blocks = (int)std::max<long long>(1, (R.finish_at + kFinishWarps - 1) / kFinishWarps);
-        const TopTreeView top{ctx->split, ctx->h, ctx->d};
-        int* seq = R.seq ? ctx->seq_dev : nullptr;
-        const int cta_blocks = (int)std::max<long long>(1, std::min<long long>(R.finish_at, ctx->sm_count * 8ll));
-        if (R.finish_cta && R.fma)
-          finish_cta_kernel<true><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
-              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
-        else if (R.finish_cta)
-          finish_cta_kernel<false><<<cta_blocks, kFinishT, 0, ctx->stream>>>(
-              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
-        else if (R.fma)
-          finish_kernel<true><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
-              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
-        else
-          finish_kernel<false><<<blocks, kFinishWarps * 32, 0, ctx->stream>>>(
-              ctx->work[cur ^ 1], ctx->ctl, ctx->q, ctx->D, R.k, top, ctx->keys, ctx->state, ctx->next, ctx->visits,
-              ctx->pts, ctx->pidx, ctx->quad_base, ctx->leaf_size, ctx->pairs, seq, ctx->seq_pos, R.seq_cap);
-        CU(cudaGetLastError());
-        R.launches++;
+        int rc = launch_finisher(ctx, R, ctx->work[cur ^ 1]);
+        if (rc != BKT_OK) return rc;
         break;
       }
       if (R.drain_at >= 0 && !R.drain_fired && ctx->h_ctl[chk].active <= R.drain_at) {
@@ -1827,7 +2089,9 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // as fast: few pairs per query and a mostly empty K=16 MMA; tools/configs.py cfg4)
   // k > 64 or a general-domain tree: the wide path (one CTA per query, wide_search.cuh)
   R.wide = ctx->wide_only || k > kMaxK;
-  R.tc = !R.wide && ctx->has_tc && ctx->residency == 0 && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
+  if (const char* e = std::getenv("BKT_OOC_ROUNDS")) R.drain = std::atoi(e) == 0;
+  // host-resident trees run the tensor-core filter on the drain's resident units
+  R.tc = !R.wide && ctx->has_tc && (ctx->residency == 0 || R.drain) && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));
   R.unfused = false;
   if (const char* e = std::getenv("BKT_TC_N")) R.tc_rows = std::atoi(e) == 64 ? 64 : (std::atoi(e) == 256 ? 256 : 128);
   if (const char* e = std::getenv("BKT_TC_CPS")) R.tc_cps = std::atoi(e) == 3 ? 3 : 2;
@@ -1846,7 +2110,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // M q/s, k = 50 1.4 -> 3.3 M; config 1 (m = 65K) 6.2 -> 4.1 M the other way.
   const bool nw_ok = ctx->split_NW > 1 || (ctx->split_NW == 1 && m >= (1 << 20)) ||
                      (std::getenv("BKT_SPLIT_NW1") && ctx->split_NW == 1);
-  R.split = R.tc && !R.unfused && nw_ok && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 && R.tc_cps == 2;
+  R.split = R.tc && ctx->residency == 0 && !R.unfused && nw_ok && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 && R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
   // graph mode (opt-in, BKT_GRAPH=1): measured slower than eager launches on
@@ -1903,7 +2167,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   //  * deeper trees of short leaves (h >= 12): one warp per query once
   //    <= min(512 per SM, m / 8) remain (config 5 h = 14: 1.27 -> 2.0 M q/s);
   //  * otherwise off (config 1, 256-point leaves: no gain).
-  if (ctx->residency == 0 && ctx->d <= 32 && k <= 64 && !R.wide) {
+  if ((ctx->residency == 0 || R.drain) && ctx->d <= 32 && k <= 64 && !R.wide) {
     if (ctx->n >= 512ll * ctx->nl) {
       R.finish_at = (long long)ctx->sm_count * 48;
       R.finish_cta = true;

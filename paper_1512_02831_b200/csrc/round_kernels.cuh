@@ -38,7 +38,55 @@ struct RoundCtl {
   int items;        // (query, window) work items this round
   // split-round totals of the batch (diagnostics, BKT_VERBOSE)
   unsigned long long sc_tiles, sc_chunks, sc_cands, sc_flushes, sc_items, sc_surv, sc_trips;
+  // out-of-core drain (engine.cu ooc_drain)
+  int park_n;       // queries parked for a later streaming unit
+  int plan_seq;     // plan_kernel launches so far (the host matches it against its mirror slot)
 };
+
+// Out-of-core drain: append `qi` to the park list for the lanes with `pred`
+// (one atomic per warp).
+__device__ __forceinline__ void park_append(bool pred, int qi, int* __restrict__ park, int* park_n) {
+  const unsigned mask = __activemask();
+  const unsigned b = __ballot_sync(mask, pred);
+  if (!b) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(b) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(park_n, __popc(b));
+  base = __shfl_sync(mask, base, leader);
+  if (pred) park[base + __popc(b & ((1u << lane) - 1u))] = qi;
+}
+
+// The park list becomes the list to classify: active = its length, a fresh
+// (empty) park count for the next list.
+__global__ void ooc_switch_kernel(RoundCtl* ctl) {
+  ctl->active = ctl->park_n;
+  ctl->park_n = 0;
+}
+
+// First park list of a batch: every query (start_kernel set its home leaf).
+__global__ void ooc_init_kernel(int* __restrict__ park, long long m, RoundCtl* ctl) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    park[i] = (int)i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->park_n = (int)m;
+}
+
+// Queries of `list` (ctl->active entries) whose next leaf lies in the
+// resident unit [leaf_lo, leaf_hi] take a bucket slot for it; the others are
+// parked again (pos.x = -1: scatter_kernel skips them).
+__global__ void ooc_classify_kernel(const int* __restrict__ list, RoundCtl* ctl, const int* __restrict__ next,
+                                    int leaf_lo, int leaf_hi, int* __restrict__ counts, int2* __restrict__ pos,
+                                    int* __restrict__ park) {
+  const int n = ctl->active;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int qi = __ldg(list + i);
+    const int nx = __ldg(next + qi);
+    const bool in = nx >= leaf_lo && nx <= leaf_hi;
+    int rk = 0;
+    if (in) rk = warp_reserve(counts, nx);
+    park_append(!in && nx >= 0, qi, park, &ctl->park_n);
+    pos[i] = make_int2(in ? nx : -1, rk);
+  }
+}
 
 // Early result drain: remember the queries of the round just scanned (every
 // query still active later is among them; the active set only shrinks).
@@ -231,6 +279,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int* __restrict__ co
     ctl->active = (int)tot_c;
     ctl->num_tiles = (int)tot_t;
     ctl->tile_next = 0;
+    ctl->plan_seq += 1;
     if (tot_c > 0) {
       if (hist && ctl->rounds < hist_cap) hist[ctl->rounds] = (int)tot_c;
       ctl->rounds += 1;
@@ -295,7 +344,8 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
                                 int D, int k, TopTreeView top, const uint64_t* __restrict__ keys,
                                 uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
                                 int* __restrict__ counts, int2* __restrict__ pos, int* seq_log,
-                                unsigned long long* seq_pos, long long seq_cap) {
+                                unsigned long long* seq_pos, long long seq_cap, int leaf_lo = 0,
+                                int leaf_hi = -1, int* __restrict__ park = nullptr, int* park_n = nullptr) {
   // the top tree's split values in shared memory when they fit (dynamic smem)
   extern __shared__ float s_fl_split[];
   const int ntree = start_tree_smem(top.h);
@@ -324,9 +374,13 @@ __global__ void findleaf_kernel(const int* __restrict__ work, const RoundCtl* ct
           seq_log[3 * p] = qi; seq_log[3 * p + 1] = (int)v; seq_log[3 * p + 2] = nxt;
         }
       }
-      rk = warp_reserve(counts, nxt);  // next round's bucket (key = leaf) and slot
     }
-    pos[i] = make_int2(nxt, rk);
+    // out-of-core drain (park != null): a next leaf outside the resident unit
+    // parks the query for a later unit
+    const bool parked = park && nxt >= 0 && (nxt < leaf_lo || nxt > leaf_hi);
+    if (park) park_append(parked, qi, park, park_n);
+    if (nxt >= 0 && !parked) rk = warp_reserve(counts, nxt);  // next round's bucket (key = leaf) and slot
+    pos[i] = make_int2(parked ? -1 : nxt, rk);
   }
 }
 
@@ -382,13 +436,24 @@ __global__ void pad_rows_kernel(const float* __restrict__ src, int d, float* __r
 // round (the top-k after a visit is the best k of the list and the leaf), so
 // results, visit counts, pairs and leaf sequences are unchanged.
 constexpr int kFinishWarps = 8;
+// Finishers inside an out-of-core drain walk only the resident unit's leaves
+// (pts/pidx hold quads [origin, ...)); a query whose next leaf lies outside
+// it keeps that leaf in next[] and is parked.  Default: the whole structure.
+struct FinishUnit {
+  long long origin = 0;
+  int leaf_lo = 0, leaf_hi = 0x7fffffff;
+  int* park = nullptr;
+  int* park_n = nullptr;
+  float* kth = nullptr;  // per-query k-th distance kept by the tensor-core scan (drain)
+};
+
 template <bool FMA>
 __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(
     const int* __restrict__ work, RoundCtl* ctl, const float* __restrict__ q, int D, int k, TopTreeView top,
     uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
     const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base,
     const int* __restrict__ leaf_size, unsigned long long* pairs, int* seq_log, unsigned long long* seq_pos,
-    long long seq_cap) {
+    long long seq_cap, FinishUnit fu) {
   __shared__ uint64_t s_row[kFinishWarps][64];
   __shared__ float s_q[kFinishWarps][32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -412,7 +477,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(
     uint32_t st = state[qi];
     uint32_t lf = st & 0xFFFFu, pend = st >> 16;
     uint32_t vis = visits[qi];
-    while (leaf >= 0) {
+    while (leaf >= fu.leaf_lo && leaf <= fu.leaf_hi) {
       const long long g0 = __ldg(quad_base + leaf), g1 = __ldg(quad_base + leaf + 1);
       uint64_t kkey = row[k - 1];
       for (long long gb = g0; gb < g1; gb += 32) {
@@ -420,7 +485,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(
         float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         bool has = g < g1;
         if (has) {
-          const float4* pq = reinterpret_cast<const float4*>(pts + g * 4 * D);
+          const float4* pq = reinterpret_cast<const float4*>(pts + (g - fu.origin) * 4 * D);
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (j < d) {
@@ -438,7 +503,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           // candidates: keys below the current k-th key (ties by original index)
-          const uint64_t key = has ? pack_key(acc[t], __ldg(pidx + g * 4 + t)) : ~0ull;
+          const uint64_t key = has ? pack_key(acc[t], __ldg(pidx + (g - fu.origin) * 4 + t)) : ~0ull;
           unsigned bal = __ballot_sync(0xffffffffu, key < kkey);
           while (bal) {
             const int src = __ffs(bal) - 1;
@@ -477,8 +542,10 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(
     for (int j = lane; j < k; j += 32) kp[j] = row[j];
     if (lane == 0) {
       state[qi] = (pend << 16) | lf;
-      next[qi] = -1;
+      next[qi] = leaf < 0 ? -1 : leaf;
       visits[qi] = vis;
+      if (leaf >= 0) fu.park[atomicAdd(fu.park_n, 1)] = qi;  // left the resident unit
+      if (fu.kth) fu.kth[qi] = key_dist(row[k - 1]);
     }
     __syncwarp();
   }
@@ -500,7 +567,7 @@ __global__ void __launch_bounds__(kFinishT) finish_cta_kernel(
     uint64_t* __restrict__ keys, uint32_t* __restrict__ state, int* __restrict__ next, uint32_t* __restrict__ visits,
     const float* __restrict__ pts, const uint32_t* __restrict__ pidx, const long long* __restrict__ quad_base,
     const int* __restrict__ leaf_size, unsigned long long* pairs, int* seq_log, unsigned long long* seq_pos,
-    long long seq_cap) {
+    long long seq_cap, FinishUnit fu) {
   __shared__ uint64_t s_row[64];
   __shared__ float s_q[32];
   __shared__ uint64_t s_cand[kFinishT * 4];
@@ -529,14 +596,14 @@ __global__ void __launch_bounds__(kFinishT) finish_cta_kernel(
       pend = st >> 16;
       vis = visits[qi];
     }
-    while (leaf >= 0) {
+    while (leaf >= fu.leaf_lo && leaf <= fu.leaf_hi) {
       const long long g0 = __ldg(quad_base + leaf), g1 = __ldg(quad_base + leaf + 1);
       for (long long gb = g0; gb < g1; gb += kFinishT) {
         const uint64_t kkey = s_row[k - 1];
         const long long g = gb + tid;
         if (g < g1) {
           float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          const float4* pq = reinterpret_cast<const float4*>(pts + g * 4 * D);
+          const float4* pq = reinterpret_cast<const float4*>(pts + (g - fu.origin) * 4 * D);
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (j < d) {
@@ -552,7 +619,7 @@ __global__ void __launch_bounds__(kFinishT) finish_cta_kernel(
           }
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const uint64_t key = pack_key(acc[t], __ldg(pidx + g * 4 + t));
+            const uint64_t key = pack_key(acc[t], __ldg(pidx + (g - fu.origin) * 4 + t));
             if (key < kkey) s_cand[atomicAdd(&s_nc, 1)] = key;
           }
         }
@@ -601,8 +668,10 @@ __global__ void __launch_bounds__(kFinishT) finish_cta_kernel(
     if (tid < k) kp[tid] = s_row[tid];
     if (tid == 0) {
       state[qi] = (pend << 16) | lf;
-      next[qi] = -1;
+      next[qi] = leaf < 0 ? -1 : leaf;
       visits[qi] = vis;
+      if (leaf >= 0) fu.park[atomicAdd(fu.park_n, 1)] = qi;  // left the resident unit
+      if (fu.kth) fu.kth[qi] = key_dist(s_row[k - 1]);
     }
   }
   if (tid == 0 && (pairs_acc || scans_acc)) {

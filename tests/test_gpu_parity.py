@@ -131,6 +131,34 @@ def test_out_of_core_chunked_plan_exact(rng, gpu_device, num_chunks):
     assert np.array_equal(stats.visited_per_query, O.knn_tree(ot, queries, 5)["visited"])
 
 
+@pytest.mark.parametrize("num_chunks,h,k", [(2, 7, 7), (5, 9, 10), (16, 10, 33)])
+def test_out_of_core_drain_equals_round_schedule(rng, gpu_device, monkeypatch, num_chunks, h, k):
+    """The drain schedule (each resident unit drained before the next,
+    engine.cu ooc_drain) against the one-round-per-leaf schedule
+    (BKT_OOC_ROUNDS=1): identical keys, visited counts and per-query leaf
+    sequences; keys equal the oracle's brute force.  (Bytes streamed: the
+    drain also ships the tensor-core rows, so with two chunks -- both
+    resident in the two slots under either schedule -- it moves more; the
+    config-5 runs in profiles/ show the cut at scale.)"""
+    refs = rng.random((30_011, 8), dtype=np.float32)
+    queries = rng.random((3_000, 8), dtype=np.float32)
+    tree = bkt.build_buffer_tree(refs, h)
+    plan = bkt.ChunkPlan.build(refs.shape[0], num_chunks)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BKT_OOC_ROUNDS", mode)
+        st = bkt.SearchStats(record_sequences=True)
+        res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), None, gpu_device, plan, stats=st)
+        out[mode] = (res, st)
+    (rd, sd), (rr, sr) = out["0"], out["1"]
+    assert np.array_equal(rd.keys, O.brute_keys(refs, queries, k, threads=4))
+    assert np.array_equal(rd.keys, rr.keys)
+    assert np.array_equal(sd.visited_per_query, sr.visited_per_query)
+    assert sd.leaf_scan_events == sr.leaf_scan_events
+    assert sd.leaf_sequences == sr.leaf_sequences
+    assert sd.stream_bytes > 0 and sr.stream_bytes > 0
+
+
 def test_out_of_core_config1_digest(gpu_device):
     gold = json.load(open(GOLDEN / "c1_digest.json"))
     refs, queries = bkt.datasets.config_inputs(1)

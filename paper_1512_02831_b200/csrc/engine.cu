@@ -155,6 +155,7 @@ struct bkt_ctx {
   int cap_nl = 0;
   int cap_keys = 0;
   int* counts = nullptr;    // per bucket key
+  int* counts_alt = nullptr;  // fused plan+scatter rounds: odd rounds' counts (plan_scatter_kernel)
   int* key_off = nullptr;   // nkeys + 1: first work-list slot of each key
   int* qkey = nullptr;      // per query: bucket key of its next leaf visit
   int2* pos = nullptr;      // per work-list position: {next leaf or -1, slot in its next bucket}
@@ -396,7 +397,7 @@ int ensure_alt(bkt_ctx* ctx, long long m, int k) {
 }
 
 void free_leafbufs(bkt_ctx* c) {
-  dfree(c->counts); dfree(c->key_off); dfree(c->leaf_off); dfree(c->tile_off);
+  dfree(c->counts); dfree(c->counts_alt); dfree(c->key_off); dfree(c->leaf_off); dfree(c->tile_off);
   hfree(c->h_tile_off);
   c->cap_nl = 0;
   c->cap_keys = 0;
@@ -409,6 +410,8 @@ int ensure_leafbufs(bkt_ctx* ctx, int nl, int nkeys) {
   CU(cudaMalloc(&ctx->counts, sizeof(int) * nkeys));
   CU(cudaMalloc(&ctx->key_off, sizeof(int) * (nkeys + 1)));
   CU(cudaMemset(ctx->counts, 0, sizeof(int) * nkeys));
+  CU(cudaMalloc(&ctx->counts_alt, sizeof(int) * nkeys));
+  CU(cudaMemset(ctx->counts_alt, 0, sizeof(int) * nkeys));
   CU(cudaMalloc(&ctx->leaf_off, sizeof(int) * (nl + 1)));
   CU(cudaMalloc(&ctx->tile_off, sizeof(int) * (nl + 1)));
   CU(cudaHostAlloc(&ctx->h_tile_off, sizeof(int) * (nl + 1), cudaHostAllocDefault));
@@ -1966,6 +1969,13 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
   // is read back asynchronously and checked kRing-1 rounds later
   cudaEvent_t* ring = ctx->ring_ev;
   const bool ooc = ctx->residency == 1;
+  // leaf-level rounds over a small bucket table: plan and scatter fused
+  // (plan_scatter_kernel; BKT_FUSED_PS=0 keeps two launches)
+  bool fused_ps = !ooc && !R.split && (long long)ctx->nl * ctx->sub_w <= kPsMaxKeys;
+  if (const char* e = std::getenv("BKT_FUSED_PS")) fused_ps = fused_ps && std::atoi(e) != 0;
+  int* counts_buf[2] = {ctx->counts, ctx->counts_alt};
+  const int ps_grid = ctx->sm_count * 2;
+  if (fused_ps) CU(cudaMemsetAsync(ctx->counts_alt, 0, sizeof(int) * ctx->nbuckets, ctx->stream));
   if (ooc && R.drain) {
     int rc = ooc_drain(ctx, R);
     if (rc != BKT_OK) return rc;
@@ -1974,9 +1984,19 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
     // queries with a next leaf -> bucket keys (leaf, block) + counts
     // home visits (round 0) are sub-bucketed per block; later rounds key by leaf only
     const int sw = round == 0 ? ctx->sub_w : 1;
-    plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, sw, ctx->nl * sw,
-                                                     ctx->leaf_off, ctx->tile_off, ctx->ctl, ctx->nl, kNT,
-                                                     ctx->hist, kHistCap, ctx->d_ctl_mirror + round % kRing);
+    int* const cnt_now = fused_ps ? counts_buf[round & 1] : ctx->counts;
+    if (fused_ps) {
+      // plan + scatter in one launch (small bucket tables, leaf-level rounds)
+      plan_scatter_kernel<<<ps_grid, kPsThreads, 0, ctx->stream>>>(
+          cnt_now, counts_buf[(round + 1) & 1], ctx->key_off, sw, ctx->nl * sw, ctx->leaf_off, ctx->tile_off,
+          ctx->ctl, ctx->nl, kNT, ctx->hist, kHistCap, ctx->d_ctl_mirror + round % kRing, ctx->work[cur ^ 1],
+          round == 0 ? 1 : 0, ctx->pos, ctx->qkey, ctx->work[cur], ctx->tiles,
+          (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
+    } else {
+      plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, sw, ctx->nl * sw,
+                                                       ctx->leaf_off, ctx->tile_off, ctx->ctl, ctx->nl, kNT,
+                                                       ctx->hist, kHistCap, ctx->d_ctl_mirror + round % kRing);
+    }
     CU(cudaGetLastError());
     R.launches++;
     const int slot = (int)(round % kRing);
@@ -1986,18 +2006,21 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
       CU(cudaEventSynchronize(ring[slot]));
       if (ctx->h_ctl[slot].active == 0) break;
     }
-    scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->pos,
-                                                           ctx->qkey, ctx->key_off, ctx->work[cur],
-                                                           ctx->ctl, ctx->leaf_off, ctx->tile_off, ctx->nl, sw, kNT,
-                                                           ctx->tiles,
-                                                           (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
-    CU(cudaGetLastError());
-    R.launches++;
+    if (!fused_ps) {
+      scatter_kernel<<<R.grid_small, 256, 0, ctx->stream>>>(ctx->work[cur ^ 1], round == 0 ? 1 : 0, ctx->pos,
+                                                             ctx->qkey, ctx->key_off, ctx->work[cur],
+                                                             ctx->ctl, ctx->leaf_off, ctx->tile_off, ctx->nl, sw, kNT,
+                                                             ctx->tiles,
+                                                             (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
+      CU(cudaGetLastError());
+      R.launches++;
+    }
     if (ooc) {
       int rc = ooc_round(ctx, R, cur);
       if (rc != BKT_OK) return rc;
     } else {
       ScanArgs a = make_scan_args(ctx, R, cur);
+      if (fused_ps) a.counts = counts_buf[(round + 1) & 1];  // next round's buckets
       const bool unfused = R.tc && R.unfused;
       const bool to_split = R.split && round == R.split_from - 1;
       if (unfused || to_split) a.fused = 0;
@@ -2015,7 +2038,7 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
         // then overlap across many warps instead of stalling the scan's epilogue
         findleaf_kernel<<<R.grid_small, 256, start_tree_smem(ctx->h) * 4, ctx->stream>>>(
             ctx->work[cur], ctx->ctl, ctx->q, ctx->D, R.k, TopTreeView{ctx->split, ctx->h, ctx->d}, ctx->keys,
-            ctx->state, ctx->next, ctx->visits, ctx->counts, ctx->pos, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
+            ctx->state, ctx->next, ctx->visits, fused_ps ? counts_buf[(round + 1) & 1] : ctx->counts, ctx->pos, R.seq ? ctx->seq_dev : nullptr, ctx->seq_pos,
             R.seq_cap);
         CU(cudaGetLastError());
         R.launches++;

@@ -41,6 +41,7 @@ struct RoundCtl {
   // out-of-core drain (engine.cu ooc_drain)
   int park_n;       // queries parked for a later streaming unit
   int plan_seq;     // plan_kernel launches so far (the host matches it against its mirror slot)
+  unsigned ps_done; // plan_scatter_kernel: CTAs finished this launch (the last one publishes the round)
 };
 
 // Out-of-core drain: append `qi` to the park list for the lanes with `pred`
@@ -335,6 +336,119 @@ __global__ void scatter_kernel(const int* __restrict__ prev, int identity, const
       if (__ldg(key_off + mid) <= p) e0 = mid; else e1 = mid;
     }
     tiles[t] = make_int4(l, p, min(tile_q, c - j * tile_q), e0 - l * sub_w);
+  }
+}
+
+// plan_kernel + scatter_kernel in one launch for small bucket tables
+// (nkeys <= kPsMaxKeys: config 1's 256 leaves): every CTA scans the whole
+// count table in shared memory, places its share of the previous list and
+// writes its share of the tile records; the last CTA to finish publishes the
+// round's control block.  Counts are double-buffered by round parity: this
+// round reads `counts` and zeroes `counts_next`, which the round's scan then
+// fills (it was last read by the previous round's launch).
+constexpr int kPsMaxKeys = 4096;
+constexpr int kPsThreads = 512;
+__global__ void __launch_bounds__(kPsThreads) plan_scatter_kernel(
+    const int* __restrict__ counts, int* __restrict__ counts_next, int* __restrict__ key_off_g, int sub_w, int nkeys,
+    int* __restrict__ leaf_off_g, int* __restrict__ tile_off_g, RoundCtl* ctl, int nl, int tile_q, int* hist,
+    int hist_cap, RoundCtl* mirror, const int* __restrict__ prev, int identity, const int2* __restrict__ pos,
+    const int* __restrict__ qkey, int* __restrict__ work, int4* __restrict__ tiles, int tiles_cap) {
+  __shared__ int s_key_off[kPsMaxKeys + 1];
+  __shared__ int s_tile_off[kPsMaxKeys + 1];
+  __shared__ int s_tot[2];
+  __shared__ bool s_last;
+  const int n_prev = ctl->active;  // read before this launch's last CTA rewrites it
+  // exclusive scans of the counts (per key) and of the tiles (per leaf)
+  {
+    const int per = (nkeys + kPsThreads - 1) / kPsThreads;
+    const int lo = min(nkeys, (int)threadIdx.x * per), hi = min(nkeys, lo + per);
+    long long sc = 0, dummy = 0, tot_c, tot_dummy;
+    for (int e = lo; e < hi; ++e) sc += __ldg(counts + e);
+    long long ec = sc;
+    block_scan2(ec, dummy, tot_c, tot_dummy);
+    for (int e = lo; e < hi; ++e) {
+      s_key_off[e] = (int)ec;
+      ec += __ldg(counts + e);
+    }
+    if (threadIdx.x == 0) {
+      s_key_off[nkeys] = (int)tot_c;
+      s_tot[0] = (int)tot_c;
+    }
+  }
+  __syncthreads();
+  {
+    const int per = (nl + kPsThreads - 1) / kPsThreads;
+    const int lo = min(nl, (int)threadIdx.x * per), hi = min(nl, lo + per);
+    long long st = 0;
+    for (int l = lo; l < hi; ++l) st += (s_key_off[(l + 1) * sub_w] - s_key_off[l * sub_w] + tile_q - 1) / tile_q;
+    long long et = st, dummy = 0, tot_t, tot_dummy;
+    block_scan2(et, dummy, tot_t, tot_dummy);
+    for (int l = lo; l < hi; ++l) {
+      s_tile_off[l] = (int)et;
+      et += (s_key_off[(l + 1) * sub_w] - s_key_off[l * sub_w] + tile_q - 1) / tile_q;
+    }
+    if (threadIdx.x == 0) {
+      s_tile_off[nl] = (int)tot_t;
+      s_tot[1] = (int)tot_t;
+    }
+  }
+  __syncthreads();
+  const int stride = gridDim.x * blockDim.x;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e <= nkeys; e += blockDim.x) key_off_g[e] = s_key_off[e];
+    for (int l = threadIdx.x; l <= nl; l += blockDim.x) {
+      tile_off_g[l] = s_tile_off[l];
+      leaf_off_g[l] = s_key_off[l * sub_w];
+    }
+  }
+  for (int e = gtid; e < nkeys; e += stride) counts_next[e] = 0;
+  for (int i = gtid; i < n_prev; i += stride) {
+    const int2 pr = __ldg(pos + i);
+    if (pr.x >= 0) {
+      const int qi = identity ? i : __ldg(prev + i);
+      const int key = identity ? __ldg(qkey + i) : pr.x;
+      work[s_key_off[key] + pr.y] = qi;
+    }
+  }
+  const int nt = min(s_tot[1], tiles_cap);
+  for (int t = gtid; t < nt; t += stride) {
+    int lo = 0, hi = nl;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_tile_off[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int l = lo, j = t - s_tile_off[l];
+    const int ec = s_key_off[l * sub_w], c = s_key_off[(l + 1) * sub_w] - ec;
+    const int p = ec + j * tile_q;
+    int e0 = l * sub_w, e1 = e0 + sub_w;
+    while (e1 - e0 > 1) {
+      const int mid = (e0 + e1) >> 1;
+      if (s_key_off[mid] <= p) e0 = mid; else e1 = mid;
+    }
+    tiles[t] = make_int4(l, p, min(tile_q, c - j * tile_q), e0 - l * sub_w);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&ctl->ps_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    const int tot_c = s_tot[0], tot_t = s_tot[1];
+    ctl->ps_done = 0;
+    ctl->prev_active = n_prev;
+    ctl->active = tot_c;
+    ctl->num_tiles = tot_t;
+    ctl->tile_next = 0;
+    ctl->plan_seq += 1;
+    if (tot_c > 0) {
+      if (hist && ctl->rounds < hist_cap) hist[ctl->rounds] = tot_c;
+      ctl->rounds += 1;
+      ctl->scans += tot_c;
+    }
+    __threadfence();
+    if (mirror) *mirror = *ctl;
   }
 }
 

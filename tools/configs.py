@@ -208,7 +208,12 @@ def cfg5(a):
                       "pairs_per_query": st["pairs"] / m, "sample_rows_match_oracle": ok,
                       **({"stream_gb": st["stream_bytes"] / 1e9, "stream_copies": st["stream_copies"],
                           "stream_gbs_over_search": st["stream_bytes"] / 1e9 / (st["search_ms"] / 1e3),
-                          "pcie_peak_gbs": "~55 (PCIe Gen5 x16 H2D, nominal 64)"} if num_chunks > 1 else {})})
+                          "pcie_peak_gbs": "~55 (PCIe Gen5 x16 H2D, nominal 64)",
+                          # PCIe roofline of the streamed structure: its bytes at the H2D peak, as a share of the search
+                          "pcie_floor_ms": st["stream_bytes"] / 55e9 * 1e3,
+                          "pcie_floor_share": st["stream_bytes"] / 55e9 / (st["search_ms"] / 1e3),
+                          "schedule": "round schedule (BKT_OOC_ROUNDS=1)" if os.environ.get("BKT_OOC_ROUNDS", "0") != "0"
+                          else "drain (DESIGN 3d)"} if num_chunks > 1 else {})})
             dev.close()
 
 

@@ -101,6 +101,15 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
                   const float* leaf_points, const int64_t* original_index, const int64_t* leaf_starts,
                   int32_t residency, int32_t num_chunks, const int64_t* chunk_bounds);
 
+/* Host-resident structures (residency 1) loaded after this call live in
+ * file-backed pages under `dir` (unlinked files mapped MAP_SHARED) instead of
+ * page-locked memory, so the structure may exceed host RAM: the drain
+ * streams each unit disk -> host -> device (sec. 3.2).  NULL or ""
+ * restores page-locked memory.  The general-domain path (k > 64, d > 32,
+ * h > 16) needs a page-locked structure and fails with BKT_EINVAL on a
+ * spilled one. */
+int bkt_set_spill_dir(bkt_ctx* ctx, const char* dir);
+
 /* k-NN search of m queries (replaces lazy_search, buffer_tree.py:523-646).
  * out_keys: (m, k) uint64 ascending packed keys (f32 bits << 32 | index),
  * exactly NeighborBatch.keys (core.py:230-262).  Domain: the reference's --

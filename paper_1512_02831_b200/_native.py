@@ -28,7 +28,7 @@ BKT_ESTATE = -5
 EXPORTS = ("bkt_open", "bkt_close", "bkt_last_error", "bkt_device_info", "bkt_build_tree",
            "bkt_build_tree_device", "bkt_build_tree_device_error", "bkt_load_tree", "bkt_search",
            "bkt_scan_groups", "bkt_seam_copy", "bkt_seam_sync", "bkt_seam_scan", "bkt_fp32_peak",
-           "bkt_host_alloc", "bkt_host_free")
+           "bkt_host_alloc", "bkt_host_free", "bkt_set_spill_dir")
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         L.bkt_build_tree_device_error.argtypes = []
         L.bkt_build_tree_device_error.restype = ctypes.c_char_p
         L.bkt_load_tree.argtypes = [P, i32, i32, i64, P, P, P, P, i32, i32, P]
+        L.bkt_set_spill_dir.argtypes = [P, ctypes.c_char_p]
         L.bkt_search.argtypes = [P, P, i64, i32, ctypes.POINTER(SearchOpts), P, ctypes.POINTER(Stats)]
         L.bkt_scan_groups.argtypes = [P, P, P, i64, i32, P, i64, i32, P, i32, P, P, P, P, i32]
         L.bkt_seam_copy.argtypes = [P, i32, P, P, i64, i32]

@@ -22,6 +22,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 #include <functional>
 #include <mutex>
 #include <string>
@@ -110,6 +113,9 @@ struct bkt_ctx {
   float* slot_tcB[2] = {nullptr, nullptr};
   uint32_t* slot_tcidx[2] = {nullptr, nullptr};
   float* slot_tcrows[2] = {nullptr, nullptr};
+  // file-backed host structure (bkt_set_spill_dir): mappings of unlinked files
+  std::string spill_dir;
+  std::vector<std::pair<void*, size_t>> spill_maps;
   // tensor-core filter layout (resident trees with d <= 31)
   bool has_tc = false;
   int KT = 0;
@@ -296,6 +302,48 @@ int leafscan_grid(bkt_ctx* ctx, int D, int kb, bool fma, int* grid) {
   return BKT_OK;
 }
 
+// Host memory of a host-resident structure: page-locked, or -- with a spill
+// directory -- a shared mapping of an unlinked file there, so the kernel can
+// write clean pages back and the structure may exceed host RAM (PAPER.md
+// sec. 3.2: disk -> host -> device; the drain streams each unit once per pass).
+int host_alloc(bkt_ctx* ctx, void** out, size_t bytes, const char* tag) {
+  bkt_ctx* c = ctx;
+  *out = nullptr;
+  if (c->spill_dir.empty()) {
+    CU(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+    return BKT_OK;
+  }
+  std::string path = c->spill_dir + "/bkt_" + std::to_string((long long)getpid()) + "_" +
+                     std::to_string(reinterpret_cast<uintptr_t>(c)) + "_" + tag + ".bin";
+  const int fd = open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
+  if (fd < 0) return set_err(c, BKT_EINVAL, "spill directory: cannot create " + path);
+  const size_t len = std::max<size_t>(bytes, 1);
+  if (ftruncate(fd, (off_t)len) != 0) {
+    close(fd);
+    unlink(path.c_str());
+    return set_err(c, BKT_ECONFIG, "spill directory: cannot size " + path);
+  }
+  void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  unlink(path.c_str());  // the mapping keeps the file; its blocks go when it is unmapped
+  if (p == MAP_FAILED) return set_err(c, BKT_ECONFIG, "spill directory: cannot map " + path);
+  c->spill_maps.emplace_back(p, len);
+  *out = p;
+  return BKT_OK;
+}
+
+void free_spill(bkt_ctx* c) {
+  for (auto& m : c->spill_maps) {
+    if (c->h_pts == m.first) c->h_pts = nullptr;
+    if (c->h_pidx == m.first) c->h_pidx = nullptr;
+    if (c->h_tcB == m.first) c->h_tcB = nullptr;
+    if (c->h_tcidx == m.first) c->h_tcidx = nullptr;
+    if (c->h_tcrows == m.first) c->h_tcrows = nullptr;
+    munmap(m.first, m.second);
+  }
+  c->spill_maps.clear();
+}
+
 void free_tree(bkt_ctx* c) {
   dfree(c->tc_B); dfree(c->tc_idx); dfree(c->tc_rowsxyz); dfree(c->tc_row_base); dfree(c->tc_centroid); dfree(c->tc_pnmax); dfree(c->tc_cbase); dfree(c->tc_box);
   c->has_tc = false;
@@ -304,6 +352,7 @@ void free_tree(bkt_ctx* c) {
   c->split_W = 0; c->split_NW = 0;
   c->nkeys = 0;
   dfree(c->split); dfree(c->quad_base); dfree(c->leaf_size); dfree(c->pts); dfree(c->pidx);
+  free_spill(c);
   hfree(c->h_pts); hfree(c->h_pidx);
   for (int s = 0; s < 2; ++s) {
     dfree(c->slot_pts[s]); dfree(c->slot_idx[s]);
@@ -800,6 +849,13 @@ void bkt_close(bkt_ctx* ctx) {
   delete ctx;
 }
 
+int bkt_set_spill_dir(bkt_ctx* ctx, const char* dir) {
+  if (!ctx) return set_err(nullptr, BKT_EINVAL, "ctx is NULL");
+  ctx->spill_dir = dir ? dir : "";
+  while (ctx->spill_dir.size() > 1 && ctx->spill_dir.back() == '/') ctx->spill_dir.pop_back();
+  return BKT_OK;
+}
+
 int bkt_device_info(bkt_ctx* ctx, int32_t* sm_count, int32_t* sm_clock_khz, int64_t* free_bytes,
                     int64_t* total_bytes) {
   if (!ctx) return set_err(nullptr, BKT_EINVAL, "ctx is NULL");
@@ -861,9 +917,16 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
 
   const size_t pts_bytes = sizeof(float) * (size_t)TQ * 4 * D;
   const size_t idx_bytes = sizeof(uint32_t) * (size_t)TQ * 4;
-  // mapped: the wide path reads a host-resident structure in place
-  CU(cudaHostAlloc(&ctx->h_pts, pts_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
-  CU(cudaHostAlloc(&ctx->h_pidx, idx_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  // mapped: the wide path reads a host-resident structure in place; a
+  // host-resident structure with a spill directory lives in file-backed pages
+  const bool spill = residency == 1 && !ctx->spill_dir.empty();
+  if (spill) {
+    if (int rc = host_alloc(ctx, reinterpret_cast<void**>(&ctx->h_pts), pts_bytes, "pts")) return rc;
+    if (int rc = host_alloc(ctx, reinterpret_cast<void**>(&ctx->h_pidx), idx_bytes, "pidx")) return rc;
+  } else {
+    CU(cudaHostAlloc(&ctx->h_pts, pts_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    CU(cudaHostAlloc(&ctx->h_pidx, idx_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  }
   build_quad_layout(leaf_points, original_index, leaf_starts, nl, d, D, ctx->h_quad_base, ctx->h_pts, ctx->h_pidx);
 
   // tensor-core filter layout (d + 1 <= 32); host_big: its row arrays stay in
@@ -874,15 +937,35 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       std::vector<long long> rb(nl + 1, 0);
       for (int l = 0; l < nl; ++l) rb[l + 1] = rb[l] + ((long long)ctx->h_leaf_size[l] + 31) / 32 * 32;
       const long long R = rb[nl];
-      std::vector<float> hB((size_t)R * KT), hrows((size_t)R * d), hcen((size_t)nl * KT), hpn((size_t)nl);
-      std::vector<uint32_t> hidx((size_t)R);
+      std::vector<float> hBv, hrowsv, hcen((size_t)nl * KT), hpn((size_t)nl);
+      std::vector<uint32_t> hidxv;
+      float *hB = nullptr, *hrows = nullptr;
+      uint32_t* hidx = nullptr;
+      if (host_big) {
+        // host-resident structure: the filter rows are built in place in
+        // page-locked memory (or file-backed pages, bkt_set_spill_dir) and
+        // stream into the drain's slots per unit (ooc_drain)
+        if (int rc = host_alloc(ctx, reinterpret_cast<void**>(&ctx->h_tcB), sizeof(float) * R * KT, "tcB")) return rc;
+        if (int rc = host_alloc(ctx, reinterpret_cast<void**>(&ctx->h_tcidx), sizeof(uint32_t) * R, "tcidx")) return rc;
+        if (int rc = host_alloc(ctx, reinterpret_cast<void**>(&ctx->h_tcrows), sizeof(float) * R * d, "tcrows")) return rc;
+        hB = ctx->h_tcB;
+        hidx = ctx->h_tcidx;
+        hrows = ctx->h_tcrows;
+      } else {
+        hBv.resize((size_t)R * KT);
+        hrowsv.resize((size_t)R * d);
+        hidxv.resize((size_t)R);
+        hB = hBv.data();
+        hidx = hidxv.data();
+        hrows = hrowsv.data();
+      }
       LeafBlocks lb;
       build_leaf_blocks(leaf_points, leaf_starts, nl, d, kBlockRows, lb);
       if (std::getenv("BKT_NO_PERM"))
         for (int l = 0; l < nl; ++l)
           for (long long i = leaf_starts[l]; i < leaf_starts[l + 1]; ++i) lb.perm[i] = (uint32_t)(i - leaf_starts[l]);
-      build_tc_layout(leaf_points, original_index, leaf_starts, nl, d, KT, rb, lb.perm, hB.data(), hidx.data(),
-                      hrows.data(), hcen.data(), hpn.data());
+      build_tc_layout(leaf_points, original_index, leaf_starts, nl, d, KT, rb, lb.perm, hB, hidx,
+                      hrows, hcen.data(), hpn.data());
       ctx->nkeys = lb.blk_base[nl];
       CU(cudaMalloc(&ctx->blk_base, sizeof(int) * (nl + 1)));
       CU(cudaMemcpy(ctx->blk_base, lb.blk_base.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice));
@@ -894,22 +977,13 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
       CU(cudaMemcpy(ctx->tc_pnmax, hpn.data(), sizeof(float) * nl, cudaMemcpyHostToDevice));
       CU(cudaMalloc(&ctx->tc_row_base, sizeof(long long) * (nl + 1)));
       CU(cudaMalloc(&ctx->tc_centroid, sizeof(float) * nl * KT));
-      if (host_big) {
-        // host-resident structure: the filter operands stay in page-locked
-        // memory and stream into the drain's slots per unit (ooc_drain)
-        CU(cudaHostAlloc(&ctx->h_tcB, sizeof(float) * R * KT, cudaHostAllocPortable));
-        CU(cudaHostAlloc(&ctx->h_tcidx, sizeof(uint32_t) * R, cudaHostAllocPortable));
-        CU(cudaHostAlloc(&ctx->h_tcrows, sizeof(float) * R * d, cudaHostAllocPortable));
-        std::memcpy(ctx->h_tcB, hB.data(), sizeof(float) * R * KT);
-        std::memcpy(ctx->h_tcidx, hidx.data(), sizeof(uint32_t) * R);
-        std::memcpy(ctx->h_tcrows, hrows.data(), sizeof(float) * R * d);
-      } else {
+      if (!host_big) {
         CU(cudaMalloc(&ctx->tc_B, sizeof(float) * R * KT));
         CU(cudaMalloc(&ctx->tc_idx, sizeof(uint32_t) * R));
         CU(cudaMalloc(&ctx->tc_rowsxyz, sizeof(float) * R * d));
-        CU(cudaMemcpy(ctx->tc_B, hB.data(), sizeof(float) * R * KT, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(ctx->tc_idx, hidx.data(), sizeof(uint32_t) * R, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(ctx->tc_rowsxyz, hrows.data(), sizeof(float) * R * d, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->tc_B, hB, sizeof(float) * R * KT, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->tc_idx, hidx, sizeof(uint32_t) * R, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->tc_rowsxyz, hrows, sizeof(float) * R * d, cudaMemcpyHostToDevice));
       }
       ctx->h_row_base = rb;
       CU(cudaMemcpy(ctx->tc_row_base, rb.data(), sizeof(long long) * (nl + 1), cudaMemcpyHostToDevice));
@@ -1002,7 +1076,7 @@ int bkt_load_tree(bkt_ctx* ctx, int32_t h, int32_t d, int64_t n, const float* sp
     // containing quad of the padded layout; results do not depend on where a
     // chunk boundary falls (reference scheduler.py:1-10, acceptance crit. 2).
     ctx->num_chunks = num_chunks;
-    {
+    if (!spill) {
       float* dp = nullptr;
       uint32_t* di = nullptr;
       CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), ctx->h_pts, 0));
@@ -2112,6 +2186,9 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
   // as fast: few pairs per query and a mostly empty K=16 MMA; tools/configs.py cfg4)
   // k > 64 or a general-domain tree: the wide path (one CTA per query, wide_search.cuh)
   R.wide = ctx->wide_only || k > kMaxK;
+  if (R.wide && ctx->residency == 1 && !ctx->wide_pts)
+    return set_err(ctx, BKT_EINVAL, "the general-domain path (k > 64, d > 32 or h > 16) needs a page-locked "
+                                    "structure; this one is spilled to files (bkt_set_spill_dir)");
   if (const char* e = std::getenv("BKT_OOC_ROUNDS")) R.drain = std::atoi(e) == 0;
   // host-resident trees run the tensor-core filter on the drain's resident units
   R.tc = !R.wide && ctx->has_tc && (ctx->residency == 0 || R.drain) && (o.kernel == 2 || (o.kernel == 0 && ctx->d >= 8));

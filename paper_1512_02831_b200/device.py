@@ -21,6 +21,7 @@ and real device buffers:
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -102,6 +103,10 @@ class DeviceSpec:
     worker_lanes: int = 1
     simulated_copy_rate: float | None = None
     cuda_device: int = 0
+    # host-resident (chunked) structures in file-backed pages under this
+    # directory instead of page-locked RAM (bkt_set_spill_dir): disk -> host
+    # -> device streaming for structures larger than host memory
+    spill_dir: str | None = None
 
 
 class GpuDevice:
@@ -139,6 +144,8 @@ class GpuDevice:
         h = ctypes.c_void_p()
         _native.check(_native.lib().bkt_open(int(spec.cuda_device), ctypes.byref(h)))
         self._ctx = h
+        if spec.spill_dir:
+            _native.check(_native.lib().bkt_set_spill_dir(h, os.fsencode(spec.spill_dir)), h)
 
     # ------------------------------------------------------------------ info
     @property

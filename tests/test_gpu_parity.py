@@ -159,6 +159,38 @@ def test_out_of_core_drain_equals_round_schedule(rng, gpu_device, monkeypatch, n
     assert sd.stream_bytes > 0 and sr.stream_bytes > 0
 
 
+def test_out_of_core_spilled_structure(rng, gpu_device, tmp_path):
+    """Disk-resident leaf structure (sec. 3.2, reference
+    buffer_tree.py:187-191): leaf points memory-mapped from store_path and the
+    device's host-resident layouts in file-backed pages under spill_dir
+    (bkt_set_spill_dir), streamed unit by unit by the drain.  Keys and visited
+    counts equal the oracle and the page-locked host-resident search; the
+    spill files are unlinked (nothing is left in spill_dir)."""
+    refs = rng.random((50_021, 10), dtype=np.float32)
+    queries = rng.random((3_000, 10), dtype=np.float32)
+    k = 10
+    tree = bkt.build_buffer_tree(refs, 8, str(tmp_path / "leaves"))
+    assert isinstance(tree.leaves.points, np.memmap)
+    plan = bkt.ChunkPlan.build(refs.shape[0], 5)
+    spill = tmp_path / "spill"
+    spill.mkdir()
+    dev = bkt.device_init(bkt.DeviceSpec(spill_dir=str(spill)))
+    try:
+        st = bkt.SearchStats()
+        res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), None, dev, plan, stats=st)
+        assert list(spill.iterdir()) == []
+        assert st.stream_bytes > 0
+        with pytest.raises(ValueError, match="general-domain"):
+            bkt.lazy_search(tree, queries[:10], bkt.SearchParams(k=65), None, dev, plan)
+    finally:
+        dev.close()
+    assert np.array_equal(res.keys, O.brute_keys(refs, queries, k, threads=4))
+    ot = O.build_tree(refs, 8)
+    assert np.array_equal(st.visited_per_query, O.knn_tree(ot, queries, k)["visited"])
+    pinned = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), None, gpu_device, plan)
+    assert np.array_equal(res.keys, pinned.keys)
+
+
 def test_out_of_core_config1_digest(gpu_device):
     gold = json.load(open(GOLDEN / "c1_digest.json"))
     refs, queries = bkt.datasets.config_inputs(1)

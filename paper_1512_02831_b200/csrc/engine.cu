@@ -2212,6 +2212,16 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
                      (std::getenv("BKT_SPLIT_NW1") && ctx->split_NW == 1);
   R.split = R.tc && ctx->residency == 0 && !R.unfused && nw_ok && k <= 64 && ctx->min_leaf >= k && R.tc_rows == 128 && R.tc_cps == 2;
   if (const char* e = std::getenv("BKT_SPLIT")) R.split = R.split && std::atoi(e) != 0;
+  // Leaf-level tensor-core rounds over short leaves (no split rounds, KT = 16,
+  // <= 1,024 points per leaf): three CTAs per SM with one 128-column
+  // accumulator each -- a tile is a few chunks, so more CTAs in flight beat a
+  // second accumulator (config 1, 256-point leaves: 6.5 -> 7.2 M q/s; config
+  // 4 d = 15, 3,906-point leaves, measured 18.7 -> 16.4 M the other way, and
+  // the home-round scan under split rounds 52.5 -> 51.7 M: kept at two;
+  // profiles/r2h/cps3_ab.txt)
+  if (R.tc && !R.split && ctx->KT == 16 && ctx->n <= 1024ll * ctx->nl && !std::getenv("BKT_TC_CPS") &&
+      !std::getenv("BKT_TC_N"))
+    R.tc_cps = 3;
   if (const char* e = std::getenv("BKT_SPLIT_FROM")) R.split_from = std::max(1, std::atoi(e));
   // graph mode (opt-in, BKT_GRAPH=1): measured slower than eager launches on
   // config 1 (3.9 vs 5.0 M q/s: its rounds are bound by the kernels' own

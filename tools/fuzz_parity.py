@@ -80,13 +80,17 @@ def main():
             q[: take.size] = refs[take]
         kernel = str(rng.choice(["auto", "tc", "direct"])) if d <= 31 and k <= 64 and h <= 16 else "auto"
         dev_build = rng.random() < 0.5
+        # host-resident structure streamed in chunks (the out-of-core drain)
+        chunks = int(rng.integers(2, 10)) if rng.random() < 0.3 else 1
         if a.only >= 0 and case != a.only:
             continue
-        print(json.dumps({"running": case, "fam": fam, "n": n, "m": m, "d": d, "k": k, "h": h, "kernel": kernel}),
+        print(json.dumps({"running": case, "fam": fam, "n": n, "m": m, "d": d, "k": k, "h": h, "kernel": kernel,
+                          "chunks": chunks}),
               file=sys.stderr, flush=True)
         tree = bkt.build_buffer_tree(refs, h, device=0 if dev_build else None)
         st = bkt.SearchStats()
-        res = bkt.lazy_search(tree, q, bkt.SearchParams(k=k), device=dev, stats=st, kernel=kernel)
+        plan = bkt.ChunkPlan.build(n, chunks) if chunks > 1 else None
+        res = bkt.lazy_search(tree, q, bkt.SearchParams(k=k), device=dev, plan=plan, stats=st, kernel=kernel)
         want = O.knn_tree(O.build_tree(refs, h), q, k, threads=8)
         ok = bool(np.array_equal(res.keys, want["keys"])) and bool(
             np.array_equal(st.visited_per_query, want["visited"].astype(np.int64)))
@@ -101,7 +105,7 @@ def main():
                           bkt.unpack_keys(want["keys"][r:r + 1]), "visited", int(st.visited_per_query[r]),
                           int(want["visited"][r]), file=sys.stderr)
             print(json.dumps({"case": case, "fam": fam, "n": n, "m": m, "d": d, "k": k, "h": h, "kernel": kernel,
-                              "rows_differing": bad}), flush=True)
+                              "chunks": chunks, "rows_differing": bad}), flush=True)
     print(json.dumps({"cases": done, "failures": fails, "seconds": round(time.time() - t0, 1)}), flush=True)
     dev.close()
 

@@ -159,6 +159,36 @@ def test_out_of_core_drain_equals_round_schedule(rng, gpu_device, monkeypatch, n
     assert sd.stream_bytes > 0 and sr.stream_bytes > 0
 
 
+@pytest.mark.parametrize("cta", ["0", "1"])
+def test_out_of_core_drain_unit_finisher(rng, gpu_device, monkeypatch, cta):
+    """The drain's unit-restricted tail finisher (warp and CTA variants,
+    forced on from 2,000 queries per unit) keeps keys, visited counts and leaf
+    sequences equal to the round schedule's, and its parked queries resume in
+    later units."""
+    refs = rng.random((40_009, 6), dtype=np.float32)
+    queries = rng.random((4_000, 6), dtype=np.float32)
+    k = 9
+    tree = bkt.build_buffer_tree(refs, 8)
+    plan = bkt.ChunkPlan.build(refs.shape[0], 6)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BKT_OOC_ROUNDS", mode)
+        if mode == "0":
+            monkeypatch.setenv("BKT_FINISH_AT", "2000")
+            monkeypatch.setenv("BKT_FINISH_CTA", cta)
+        else:
+            monkeypatch.delenv("BKT_FINISH_AT", raising=False)
+            monkeypatch.delenv("BKT_FINISH_CTA", raising=False)
+        st = bkt.SearchStats(record_sequences=True)
+        res = bkt.lazy_search(tree, queries, bkt.SearchParams(k=k), None, gpu_device, plan, stats=st)
+        out[mode] = (res, st)
+    (rd, sd), (rr, sr) = out["0"], out["1"]
+    assert np.array_equal(rd.keys, O.brute_keys(refs, queries, k, threads=4))
+    assert np.array_equal(rd.keys, rr.keys)
+    assert np.array_equal(sd.visited_per_query, sr.visited_per_query)
+    assert sd.leaf_sequences == sr.leaf_sequences
+
+
 def test_out_of_core_spilled_structure(rng, gpu_device, tmp_path):
     """Disk-resident leaf structure (sec. 3.2, reference
     buffer_tree.py:187-191): leaf points memory-mapped from store_path and the

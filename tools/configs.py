@@ -217,9 +217,39 @@ def cfg5(a):
             dev.close()
 
 
+def brute(a):
+    """GPU brute force (reference brute.py:41-113): the engine's leaf scans over
+    the exhaustive two-leaf structure (every (query, reference) pair), uniform
+    d = 10, k = 10; q/s, pairs/s and the TF32 roofline of the scan; 256 rows
+    against the oracle's brute force."""
+    from oracle import oracle as O
+    from paper_1512_02831_b200.brute import exhaustive_tree
+    d, k = 10, 10
+    m = int(a.m) if a.m else 65536
+    for n in (65536, 1 << 20):
+        rng = np.random.default_rng(7)
+        refs = rng.random((n, d), dtype=np.float32)
+        q = rng.random((m, d), dtype=np.float32)
+        tree = exhaustive_tree(refs)
+        dev = bkt.device_init(bkt.DeviceSpec(cuda_device=0))
+        bkt.lazy_search(tree, q[:4096], bkt.SearchParams(k=k), device=dev)  # warm-up
+        st = bkt.SearchStats()
+        t0 = time.perf_counter()
+        res = bkt.lazy_search(tree, q, bkt.SearchParams(k=k), device=dev, stats=st)
+        wall = time.perf_counter() - t0
+        ok = bool(np.array_equal(res.keys[:256], O.brute_keys(refs, q[:256], k, threads=os.cpu_count() or 1)))
+        pairs = float(m) * n
+        emit({"config": f"brute uniform n={n} m={m} d={d} k={k}", "qps_device": m / (st.search_ms / 1e3),
+              "qps_wall": m / wall, "pairs_per_s": pairs / (st.search_ms / 1e3),
+              "leafscan_tflops_tf32": pairs * 32 / (st.leafscan_ms / 1e3) / 1e12,
+              "roofline_frac_tf32": pairs * 32 / (st.leafscan_ms / 1e3) / 1e12 / _tf32_peak(),
+              "leafscan_share": st.leafscan_ms / st.search_ms, "sample_rows_match_oracle": ok})
+        dev.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["cfg1", "cfg3", "cfg4", "cfg5", "uniform2m"])
+    ap.add_argument("which", choices=["cfg1", "cfg3", "cfg4", "cfg5", "uniform2m", "brute"])
     ap.add_argument("--m", type=float, default=None)
     ap.add_argument("--gpus", type=int, default=1, help="cfg3: devices the stream is spread over")
     ap.add_argument("--heights", default="8,11,14", help="cfg5: tree heights")
@@ -227,7 +257,7 @@ def main():
     ap.add_argument("--resident", default="both", choices=["hbm", "host", "both"], help="cfg5: leaf structure residency")
     a = ap.parse_args()
     if a.m is None:
-        a.m = {"cfg1": 65536, "cfg3": 2e8, "cfg4": 10e6, "cfg5": 1e6, "uniform2m": 10e6}[a.which]
+        a.m = {"cfg1": 65536, "cfg3": 2e8, "cfg4": 10e6, "cfg5": 1e6, "uniform2m": 10e6, "brute": 262144}[a.which]
     globals()[a.which](a)
 
 

@@ -2259,7 +2259,12 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
     // two CTAs per SM: the variants are sized for it (2 x 256 TMEM columns,
     // shared memory and registers); the occupancy query is only a sanity check
     int per_sm = (ctx->KT == 16) ? R.tc_cps : 2;
-    if (R.kb >= 32) per_sm = 1;  // register-heavy top-k variants (leafscan_tc.cuh launch bounds)
+    if (R.kb >= 32) {
+      // register-heavy top-k variants (leafscan_tc.cuh launch bounds); BKT_TC_BIGK_CTAS
+      // for builds with BKT_TC_BIGK_MINB = 2 (experiment)
+      per_sm = 1;
+      if (const char* e = std::getenv("BKT_TC_BIGK_CTAS")) per_sm = std::max(1, std::min(2, std::atoi(e)));
+    }
     if (occ < 1) return set_err(ctx, BKT_ECUDA, "tensor-core leaf kernel cannot be resident");
     if (const char* e = std::getenv("BKT_TC_CTAS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     if (std::getenv("BKT_VERBOSE")) std::fprintf(stderr, "tc kernel: occupancy %d CTAs/SM, grid %d\n", occ, per_sm * ctx->sm_count);

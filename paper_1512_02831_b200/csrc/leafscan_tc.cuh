@@ -268,10 +268,13 @@ template <int KT, int KB, bool FMA, int NR, int CPS>
 #ifndef BKT_TC_MINB
 #define BKT_TC_MINB CPS
 #endif
+#ifndef BKT_TC_BIGK_MINB
+#define BKT_TC_BIGK_MINB 1  // experiments: 2 = two CTAs per SM for KB >= 32 (registers capped, spills)
+#endif
 // KB >= 32 (k > 16): the register top-k alone needs 64-128 registers, so
 // these variants run one CTA per SM with the full register file instead of
 // spilling at two (engine.cu launches them one per SM)
-__global__ void __launch_bounds__(tc_threads(CPS), (KB >= 32 ? 1 : BKT_TC_MINB)) leafscan_tc_kernel(const TcArgs A) {
+__global__ void __launch_bounds__(tc_threads(CPS), (KB >= 32 ? BKT_TC_BIGK_MINB : BKT_TC_MINB)) leafscan_tc_kernel(const TcArgs A) {
   using S = TcSmem<KT, NR, CPS>;
   constexpr int kTcRows = NR;
   constexpr int kTcBufs = S::kBufs;

@@ -1223,6 +1223,8 @@ struct SearchRun {
   const float* unit_B = nullptr;       // drain: the resident unit's filter rows (row-indexed, origin applied)
   const uint32_t* unit_idx = nullptr;
   const float* unit_rows = nullptr;
+  bool pdl = true;           // fused leaf-level rounds: programmatic dependent launches (BKT_PDL=0: off)
+  bool scan_pdl = false;     // the next leaf-scan launch uses PDL
   bool drain = true;         // out-of-core: drain schedule (ooc_drain); BKT_OOC_ROUNDS=1: one round per leaf visit
   bool graph = false;        // split rounds replayed from a captured CUDA graph (launch-bound searches)
   long long stream_bytes = 0;   // out-of-core chunk streaming (bkt_stats.stream_bytes)
@@ -1300,6 +1302,7 @@ int launch_scan(bkt_ctx* ctx, SearchRun& R, const ScanArgs& a) {
     t.ctr = R.counters ? ctx->tc_ctr : nullptr;
     t.sub_w = ctx->sub_w;
     t.tile_next = &ctx->ctl->tile_next;
+    t.pdl = R.scan_pdl && !R.timing ? 1 : 0;  // (timed launches keep their events adjacent)
     if (const char* e = std::getenv("BKT_TC_SPIN")) t.spin = std::atoi(e);
     const char* dbg_env = std::getenv("BKT_TC_DEBUG");
     if (dbg_env && R.leafscan_launches == (*dbg_env ? std::atoi(dbg_env) : 5)) {
@@ -2060,12 +2063,27 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
     const int sw = round == 0 ? ctx->sub_w : 1;
     int* const cnt_now = fused_ps ? counts_buf[round & 1] : ctx->counts;
     if (fused_ps) {
-      // plan + scatter in one launch (small bucket tables, leaf-level rounds)
-      plan_scatter_kernel<<<ps_grid, kPsThreads, 0, ctx->stream>>>(
-          cnt_now, counts_buf[(round + 1) & 1], ctx->key_off, sw, ctx->nl * sw, ctx->leaf_off, ctx->tile_off,
-          ctx->ctl, ctx->nl, kNT, ctx->hist, kHistCap, ctx->d_ctl_mirror + round % kRing, ctx->work[cur ^ 1],
-          round == 0 ? 1 : 0, ctx->pos, ctx->qkey, ctx->work[cur], ctx->tiles,
-          (int)std::min<long long>(ctx->tiles_cap, INT32_MAX));
+      // plan + scatter in one launch (small bucket tables, leaf-level rounds);
+      // with PDL its launch overlaps the previous scan's tail
+      int* const cnt_next = counts_buf[(round + 1) & 1];
+      const int nkeys_r = ctx->nl * sw;
+      RoundCtl* const mir = ctx->d_ctl_mirror + round % kRing;
+      const int* const prevw = ctx->work[cur ^ 1];
+      const int ident = round == 0 ? 1 : 0;
+      int* const outw = ctx->work[cur];
+      const int tcap = (int)std::min<long long>(ctx->tiles_cap, INT32_MAX);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(ps_grid);
+      cfg.blockDim = dim3(kPsThreads);
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = R.pdl ? 1 : 0;
+      CU(cudaLaunchKernelEx(&cfg, plan_scatter_kernel, (const int*)cnt_now, cnt_next, ctx->key_off, sw, nkeys_r,
+                            ctx->leaf_off, ctx->tile_off, ctx->ctl, ctx->nl, (int)kNT, ctx->hist, (int)kHistCap, mir,
+                            prevw, ident, (const int2*)ctx->pos, (const int*)ctx->qkey, outw, ctx->tiles, tcap));
     } else {
       plan_kernel<<<1, kPlanThreads, 0, ctx->stream>>>(ctx->counts, ctx->key_off, sw, ctx->nl * sw,
                                                        ctx->leaf_off, ctx->tile_off, ctx->ctl, ctx->nl, kNT,
@@ -2074,7 +2092,7 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
     CU(cudaGetLastError());
     R.launches++;
     const int slot = (int)(round % kRing);
-    CU(cudaEventRecord(ring[slot], ctx->stream));
+    if (!(fused_ps && R.pdl)) CU(cudaEventRecord(ring[slot], ctx->stream));
     if (ooc) {
       // out-of-core needs the plan on the host anyway; check synchronously
       CU(cudaEventSynchronize(ring[slot]));
@@ -2095,11 +2113,14 @@ int search_batch_impl(bkt_ctx* ctx, SearchRun& R) {
     } else {
       ScanArgs a = make_scan_args(ctx, R, cur);
       if (fused_ps) a.counts = counts_buf[(round + 1) & 1];  // next round's buckets
+      R.scan_pdl = fused_ps && R.pdl;
       const bool unfused = R.tc && R.unfused;
       const bool to_split = R.split && round == R.split_from - 1;
       if (unfused || to_split) a.fused = 0;
       int rc = launch_scan(ctx, R, a);
+      R.scan_pdl = false;
       if (rc != BKT_OK) return rc;
+      if (fused_ps && R.pdl) CU(cudaEventRecord(ring[slot], ctx->stream));  // the plan's mirror is older still
       if (to_split) {
         // this round's rows and kth are final: the split rounds start with
         // its queries' advance (FindLeaf, next-leaf buckets, A rows)
@@ -2231,6 +2252,7 @@ extern "C" int bkt_search(bkt_ctx* ctx, const float* queries, int64_t m, int32_t
             !std::getenv("BKT_SPLIT_DEBUG");
   R.renumber = ctx->residency == 0 && !R.wide && !std::getenv("BKT_EARLY_DRAIN");
   R.verbose = std::getenv("BKT_VERBOSE") != nullptr;
+  if (const char* e = std::getenv("BKT_PDL")) R.pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("BKT_RENUMBER")) R.renumber = R.renumber && std::atoi(e) != 0;
   int rc = BKT_OK;
   if (R.wide) {

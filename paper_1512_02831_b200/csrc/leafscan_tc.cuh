@@ -102,6 +102,7 @@ struct TcArgs {
   long long* dbg;              // diagnostics (BKT_TC_DEBUG): per-chunk timestamps of CTA 0
   int dbg_cap;
   unsigned long long* ctr;     // diagnostics (BKT_TC_COUNTERS): filter/survivor counters, see engine.cu
+  int pdl;                     // host: launch with programmatic stream serialization (prologue overlaps the previous kernel)
 };
 
 // Chunk order of a tile: starting at the chunk of the block its first query
@@ -343,6 +344,12 @@ __global__ void __launch_bounds__(tc_threads(CPS), (KB >= 32 ? BKT_TC_BIGK_MINB 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Programmatic dependent launch: everything above (barriers, TMEM, the
+  // static top tree) may overlap the previous kernel; every read of its
+  // results comes after this wait (a no-op for a normal launch).  The next
+  // kernel may be scheduled as soon as this grid's CTAs leave the SMs.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t tmem = *s_tmem;
   const int tiles_end = a.tile_hi >= 0 ? a.tile_hi : *a.num_tiles;
   // Tile order.  CPS < 3: dynamic -- the epilogue's thread 0 takes tiles from

@@ -55,6 +55,20 @@ cudaError_t launch_tc_one(int grid, cudaStream_t s, const TcArgs& a0, int* occ) 
     configured.fetch_or(bit, std::memory_order_release);
   }
   if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, tc_threads(CPS), smem);
+  if (a.pdl) {
+    // programmatic stream serialization: the prologue overlaps the previous kernel (griddepcontrol.wait)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc_threads(CPS));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, a);
+  }
   fn<<<grid, tc_threads(CPS), smem, s>>>(a);
   return cudaGetLastError();
 }

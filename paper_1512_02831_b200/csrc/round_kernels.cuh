@@ -357,6 +357,10 @@ __global__ void __launch_bounds__(kPsThreads) plan_scatter_kernel(
   __shared__ int s_tile_off[kPsMaxKeys + 1];
   __shared__ int s_tot[2];
   __shared__ bool s_last;
+  // programmatic dependent launch (engine.cu fused rounds): the previous
+  // scan's results are read only after this wait (a no-op for a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int n_prev = ctl->active;  // read before this launch's last CTA rewrites it
   // exclusive scans of the counts (per key) and of the tiles (per leaf)
   {

@@ -54,6 +54,12 @@
 namespace bkt {
 
 
+#ifndef BKT_SPLIT_MMA_SPIN
+#define BKT_SPLIT_MMA_SPIN 0  // experiments: the MMA warp spins on its barriers instead of suspending
+#endif
+#ifndef BKT_SPLIT_EPI_SPIN
+#define BKT_SPLIT_EPI_SPIN 0  // experiments: the epilogue spins on the accumulator-full barrier
+#endif
 #ifndef BKT_SPLIT_ONEPASS
 #define BKT_SPLIT_ONEPASS 1
 #endif
@@ -305,9 +311,17 @@ __global__ void __launch_bounds__(kSplitThreads, kSplitCtas) splitscan_tc_kernel
         for (int c = win.cb; c < win.ce; ++c, ++g) {
           const int s = g % kSplitStages;
           const uint32_t b = g % kSplitAcc, use = g / kSplitAcc;
+#if BKT_SPLIT_MMA_SPIN
+          mbar_wait_spin(&full[s], (g / kSplitStages) & 1u);
+#else
           mbar_wait(&full[s], (g / kSplitStages) & 1u);
+#endif
           if (A.dbg && blockIdx.x == 0 && (int)g < A.dbg_cap) A.dbg[8 * A.dbg_cap + 8 * g + 6] = clock64();
+#if BKT_SPLIT_MMA_SPIN
+          if (use > 0) mbar_wait_spin(&tempty[b], (use - 1) & 1u);
+#else
           if (use > 0) mbar_wait(&tempty[b], (use - 1) & 1u);
+#endif
           tc_fence_after();
           const int nr = (int)dmin_ll(128, win.r1 - (win.r0 + (long long)c * 128));
           const uint32_t idesc = idesc_tf32(nr);
@@ -372,7 +386,11 @@ __global__ void __launch_bounds__(kSplitThreads, kSplitCtas) splitscan_tc_kernel
         const uint32_t b = g % kSplitAcc;
         const bool dbg_c = dbg_on && (int)g < A.dbg_cap;
         if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 2] = clock64();
+#if BKT_SPLIT_EPI_SPIN
+        mbar_wait_spin(&tfull[b], (g / kSplitAcc) & 1u);
+#else
         mbar_wait(&tfull[b], (g / kSplitAcc) & 1u);
+#endif
         if (dbg_c) A.dbg[8 * A.dbg_cap + 8 * g + 3] = clock64();
         tc_fence_after();
         const long long row0 = win.r0 + (long long)c * 128;

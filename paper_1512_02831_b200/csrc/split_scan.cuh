@@ -54,6 +54,9 @@
 namespace bkt {
 
 
+#ifndef BKT_ADV_Q2
+#define BKT_ADV_Q2 1  // advance_kernel loads query rows as float pairs (even strides; 52.55 -> 52.69 M q/s, r4w)
+#endif
 #ifndef BKT_SPLIT_MMA_SPIN
 #define BKT_SPLIT_MMA_SPIN 0  // experiments: the MMA warp spins on its barriers instead of suspending
 #endif
@@ -721,8 +724,23 @@ __global__ void __launch_bounds__(kAdvThreads, 4) advance_kernel(const AdvanceAr
     const uint64_t word0 = valid ? counts8(0) : 0ull;
     float qv[kSplitMaxD];
     const float* qp = a.q + (long long)qi * a.D;
+#if BKT_ADV_Q2
+    if ((a.D & 1) == 0) {
+      // even row stride: the row in 8-byte pairs (half the load instructions)
+      const float2* qp2 = reinterpret_cast<const float2*>(qp);
 #pragma unroll
-    for (int j = 0; j < kSplitMaxD; ++j) qv[j] = (valid && j < d) ? __ldg(qp + j) : 0.0f;
+      for (int j = 0; j < (kSplitMaxD + 1) / 2; ++j) {
+        float2 v = make_float2(0.0f, 0.0f);
+        if (valid && 2 * j < d) v = __ldg(qp2 + j);
+        qv[2 * j] = v.x;
+        if (2 * j + 1 < kSplitMaxD) qv[2 * j + 1] = (2 * j + 1 < d) ? v.y : 0.0f;
+      }
+    } else
+#endif
+    {
+#pragma unroll
+      for (int j = 0; j < kSplitMaxD; ++j) qv[j] = (valid && j < d) ? __ldg(qp + j) : 0.0f;
+    }
 #pragma unroll
     for (int j = 0; j < kSplitMaxD; ++j)
       if (j < d) myq[j * kAdvThreads] = qv[j];  // (FindLeaf and the survivor evaluation read it)
